@@ -1,0 +1,138 @@
+/*
+ * spmmm.h — C ABI of libspmmm.so, the B200 (sm_100a) CSR x CSR sparse
+ * matrix-matrix product C = A·B (fp64 values, uint64 indices, sorted columns).
+ *
+ * This is the drop-in boundary for the reference's row-major spMMM entry point
+ *     sparsemm.kernels.multiply_rowmajor(a, b, strategy=COMBINED, stats=None)
+ *     (/root/reference/pkg/src/sparsemm/kernels.py:302-332)
+ * The reference has no FFI of its own (it is pure Python); the ctypes binding a
+ * maintainer adds on the reference side is shown in INTEGRATION.md, and the
+ * Python mirror of the entry point lives in paper_1303_1651_b200/kernels.py.
+ *
+ * Data layout (formats.py:15-16, 40-58): CsrMatrix = (rows, cols,
+ * row_ptr u64[rows+1], col_idx u64[nnz], values f64[nnz]) with strictly
+ * increasing columns per row. Results follow the reference bit for bit in
+ * structure; values follow its accumulation order exactly (left fold over the
+ * A-row entries in ascending column order, separately rounded multiply and add,
+ * exact zeros dropped: kernels.py:163-180, 285-299).
+ *
+ * Threading: every entry point is re-entrant per context; a context owns one
+ * CUDA stream on one device. Errors are reported as status codes; the message
+ * of the last failure on the calling thread is available from spmmm_last_error().
+ */
+#ifndef SPMMM_H
+#define SPMMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMMM_ABI_VERSION 1
+
+/* Status codes. The Python shim maps 1 and 2 to ValueError and the rest to
+ * RuntimeError (kernels.py:312-313 raises ValueError on dimension mismatch). */
+typedef enum {
+  SPMMM_OK = 0,
+  SPMMM_ERR_DIMENSION = 1,   /* a.cols != b.rows                         (kernels.py:312-313) */
+  SPMMM_ERR_INVALID = 2,     /* bad argument, malformed CSR, unknown strategy (kernels.py:77) */
+  SPMMM_ERR_CUDA = 3,        /* CUDA runtime error                                          */
+  SPMMM_ERR_NCCL = 4,        /* reserved for collective failures                           */
+  SPMMM_ERR_OOM = 5,         /* device or host allocation failed                            */
+  SPMMM_ERR_UNSUPPORTED = 6  /* shape outside the supported range (cols >= 2^32-1, ...)    */
+} spmmm_status;
+
+/* Where a CSR view's arrays live. */
+typedef enum { SPMMM_MEM_HOST = 0, SPMMM_MEM_DEVICE = 1 } spmmm_memory;
+
+/* Borrowed, read-only CSR view. For device views row_ptr[0] need not be 0:
+ * a row block of a bigger matrix is passed as (row_ptr + r0, col_idx, values)
+ * with `nnz` = length of the col_idx/values arrays. */
+typedef struct {
+  uint64_t rows;
+  uint64_t cols;
+  uint64_t nnz;
+  const uint64_t* row_ptr;
+  const uint64_t* col_idx;
+  const double* values;
+  int32_t memory; /* spmmm_memory */
+  int32_t reserved;
+} spmmm_csr;
+
+/* Mirrors sparsemm.kernels.StrategyKind (kernels.py:38-47). Every strategy
+ * yields the same bytes (kernels.py:1-17); the GPU validates and records it. */
+typedef enum {
+  SPMMM_STRATEGY_BFDOUBLE = 0,
+  SPMMM_STRATEGY_BFBOOL = 1,
+  SPMMM_STRATEGY_BFCHAR = 2,
+  SPMMM_STRATEGY_MINMAX = 3,
+  SPMMM_STRATEGY_MINMAXCHAR = 4,
+  SPMMM_STRATEGY_SORT = 5,
+  SPMMM_STRATEGY_COMBINED = 6
+} spmmm_strategy;
+
+/* spmmm_multiply flags */
+#define SPMMM_FLAG_ROW_STATS 1u /* record per-row touched-range stats (KernelStats.row_choices) */
+#define SPMMM_FLAG_TIMING 2u    /* record per-kernel CUDA-event durations on the context      */
+
+typedef struct spmmm_context spmmm_context;
+typedef struct spmmm_product spmmm_product;
+
+int spmmm_abi_version(void);
+const char* spmmm_last_error(void);
+int spmmm_device_count(int* count);
+
+/* One context per (device, stream). cuda_stream may be NULL (the context
+ * creates its own non-blocking stream) or a cudaStream_t owned by the caller. */
+int spmmm_context_create(int device, void* cuda_stream, spmmm_context** out);
+int spmmm_context_destroy(spmmm_context* ctx);
+int spmmm_synchronize(spmmm_context* ctx);
+
+/* C = A·B.  Replaces kernels.py:302-332 (multiply_rowmajor). A and B may be
+ * host or device views; C stays device-resident in the returned product until
+ * spmmm_product_destroy. Host inputs are uploaded on the context stream (A and
+ * B that alias the same host arrays are uploaded once). */
+int spmmm_multiply(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b, int strategy,
+                   uint32_t flags, spmmm_product** out);
+
+/* Shape, nnz(C) and the multiplication count (KernelStats.multiplications,
+ * kernels.py:330-331 == perfmodel.count_mults). */
+int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
+                        uint64_t* multiplications);
+/* Device pointers of C (valid until spmmm_product_destroy). */
+int spmmm_product_device_arrays(const spmmm_product* p, const uint64_t** row_ptr,
+                                const uint64_t** col_idx, const double** values);
+/* Copies C into caller-owned host buffers (rows+1, nnz, nnz entries). */
+int spmmm_product_download(spmmm_product* p, uint64_t* row_ptr, uint64_t* col_idx,
+                           double* values);
+/* Same, into caller-owned DEVICE buffers on the product's device (ordered on
+ * the context stream; e.g. tensors that a collective then sends). */
+int spmmm_product_copy_device(spmmm_product* p, uint64_t* row_ptr, uint64_t* col_idx,
+                              double* values);
+/* With SPMMM_FLAG_ROW_STATS: per row the smallest and largest touched column
+ * and the length of the reference's touched list (kernels.py:170-178), from
+ * which combined_select (kernels.py:186-191) gives row_choices. Rows that
+ * touched nothing report min = UINT64_MAX, max = 0, touched = 0. */
+int spmmm_product_row_stats(spmmm_product* p, uint64_t* min_col, uint64_t* max_col,
+                            uint64_t* touched);
+int spmmm_product_destroy(spmmm_product* p);
+
+/* estimate_nnz (formats.py:276-289) == count_mults (perfmodel.py:63-76). */
+int spmmm_estimate_nnz(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b,
+                       uint64_t* out);
+/* Inclusive prefix of per-row product counts into a host array of rows+1
+ * entries (out[0] = 0): the input of product-balanced row partitioning. */
+int spmmm_row_products_prefix(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b,
+                              uint64_t* out);
+
+/* Per-kernel timings of the last spmmm_multiply with SPMMM_FLAG_TIMING:
+ * names[i] (static strings) and milliseconds ms[i], i < *count (<= cap). */
+int spmmm_last_timings(spmmm_context* ctx, const char** names, double* ms, int cap, int* count);
+/* Number of kernels the last spmmm_multiply launched. */
+int spmmm_last_launch_count(spmmm_context* ctx, int* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMMM_H */

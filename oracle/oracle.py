@@ -1,0 +1,164 @@
+"""ctypes front end of the CPU oracle (oracle/spmmm_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py, always as the checker or the
+CPU baseline, never as the measured product. The product package
+(paper_1303_1651_b200) does not import this module.
+
+Every function takes plain numpy CSR triples (uint64 row_ptr, uint64 col_idx,
+float64 values) so it can check the CUDA library and the reference package
+alike. See spmmm_oracle.c for the reference file:line each routine restates.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_i8p = ctypes.POINTER(ctypes.c_int8)
+
+
+def build() -> str:
+    """Compile liboracle.so in place (gcc; a few seconds)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        build()
+    lib = ctypes.CDLL(_LIB_PATH)
+    lib.oracle_estimate_nnz.restype = ctypes.c_uint64
+    lib.oracle_estimate_nnz.argtypes = [ctypes.c_uint64, _u64p, _u64p, _u64p]
+    lib.oracle_count_mults.restype = ctypes.c_uint64
+    lib.oracle_count_mults.argtypes = [ctypes.c_uint64, _u64p, _u64p, _u64p]
+    lib.oracle_row_products.restype = None
+    lib.oracle_row_products.argtypes = [ctypes.c_uint64, _u64p, _u64p, _u64p, _u64p]
+    lib.oracle_multiply_rowmajor.restype = ctypes.c_int
+    lib.oracle_multiply_rowmajor.argtypes = (
+        [ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p, _f64p]
+        + [ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p, _f64p]
+        + [_u64p, _u64p, _f64p, ctypes.c_uint64, _i8p, _u64p, _u64p]
+    )
+    lib.oracle_multiply_rowmajor_mt.restype = ctypes.c_int
+    lib.oracle_multiply_rowmajor_mt.argtypes = (
+        [ctypes.c_int]
+        + [ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p, _f64p]
+        + [ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p, _f64p]
+        + [_u64p, _u64p, _f64p, ctypes.c_uint64, _u64p]
+    )
+    _lib = lib
+    return lib
+
+
+def _p(arr, typ):
+    return arr.ctypes.data_as(typ)
+
+
+def _arrays(m):
+    rp = np.ascontiguousarray(m.row_ptr, dtype=np.uint64)
+    ci = np.ascontiguousarray(m.col_idx, dtype=np.uint64)
+    v = np.ascontiguousarray(m.values, dtype=np.float64)
+    if ci.size == 0:
+        ci = np.zeros(1, np.uint64)
+        v = np.zeros(1, np.float64)
+    return rp, ci, v
+
+
+@dataclass
+class OracleResult:
+    rows: int
+    cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    multiplications: int
+    row_choices: np.ndarray | None  # int8 per row: -1 none, 0 MinMax, 1 Sort
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+
+def estimate_nnz(a, b) -> int:
+    """formats.py:276-289."""
+    if a.cols != b.rows:
+        raise ValueError(f"dimension mismatch: {a.cols} (cols of a) != {b.rows} (rows of b)")
+    lib = _load()
+    arp, aci, _ = _arrays(a)
+    brp, _, _ = _arrays(b)
+    return int(lib.oracle_estimate_nnz(a.rows, _p(arp, _u64p), _p(aci, _u64p), _p(brp, _u64p)))
+
+
+def row_products(a, b) -> np.ndarray:
+    lib = _load()
+    arp, aci, _ = _arrays(a)
+    brp, _, _ = _arrays(b)
+    out = np.zeros(a.rows, np.uint64)
+    lib.oracle_row_products(a.rows, _p(arp, _u64p), _p(aci, _u64p), _p(brp, _u64p),
+                            _p(out, _u64p))
+    return out
+
+
+def multiply_rowmajor(a, b, *, row_choices: bool = False, threads: int = 1) -> OracleResult:
+    """kernels.py:302-332 with StrategyKind.COMBINED (all strategies are
+    bit-identical by the reference's contract, kernels.py:1-17)."""
+    if a.cols != b.rows:
+        raise ValueError(f"dimension mismatch: {a.cols} (cols of a) != {b.rows} (rows of b)")
+    lib = _load()
+    arp, aci, av = _arrays(a)
+    brp, bci, bv = _arrays(b)
+    cap = estimate_nnz(a, b)
+    out_rp = np.zeros(a.rows + 1, np.uint64)
+    out_ci = np.empty(max(cap, 1), np.uint64)
+    out_v = np.empty(max(cap, 1), np.float64)
+    nnz = ctypes.c_uint64(0)
+    mults = ctypes.c_uint64(0)
+    choice = None
+    if threads > 1 and not row_choices:
+        rc = lib.oracle_multiply_rowmajor_mt(
+            threads, a.rows, a.cols, _p(arp, _u64p), _p(aci, _u64p), _p(av, _f64p),
+            b.rows, b.cols, _p(brp, _u64p), _p(bci, _u64p), _p(bv, _f64p),
+            _p(out_rp, _u64p), _p(out_ci, _u64p), _p(out_v, _f64p), cap, ctypes.byref(nnz))
+        mults.value = cap
+    else:
+        choice = np.full(a.rows, -1, np.int8) if row_choices else None
+        rc = lib.oracle_multiply_rowmajor(
+            a.rows, a.cols, _p(arp, _u64p), _p(aci, _u64p), _p(av, _f64p),
+            b.rows, b.cols, _p(brp, _u64p), _p(bci, _u64p), _p(bv, _f64p),
+            _p(out_rp, _u64p), _p(out_ci, _u64p), _p(out_v, _f64p), cap,
+            _p(choice, _i8p) if choice is not None else None,
+            ctypes.byref(nnz), ctypes.byref(mults))
+    if rc != 0:
+        raise RuntimeError(f"oracle failed with status {rc}")
+    n = int(nnz.value)
+    return OracleResult(a.rows, b.cols, out_rp, out_ci[:n].copy(), out_v[:n].copy(),
+                        int(mults.value), choice)
+
+
+def dense_multiply(a_dense, b_dense):
+    """kernels.py:441-457: triple loop, k ascending, returns (C, mults)."""
+    a = np.asarray(a_dense, dtype=np.float64)
+    b = np.asarray(b_dense, dtype=np.float64)
+    if a.shape[1] != b.shape[0]:
+        raise ValueError("dimension mismatch")
+    out = np.zeros((a.shape[0], b.shape[1]), np.float64)
+    for k in range(a.shape[1]):
+        # rank-1 update per k, ascending: every C entry is a left fold over k
+        # of separately rounded products
+        out += np.multiply.outer(a[:, k], b[k, :])
+    mults = int(np.count_nonzero(a, axis=0) @ np.count_nonzero(b, axis=1))
+    return out, mults

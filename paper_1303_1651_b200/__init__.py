@@ -1,0 +1,36 @@
+"""B200-native CSR x CSR spMMM: a drop-in for the reference package's
+row-major product `sparsemm.kernels.multiply_rowmajor` (arXiv 1303.1651's
+Gustavson kernel), running as hand-written sm_100a CUDA in libspmmm.so.
+
+Public surface (mirrors the reference's names for this path):
+    multiply_rowmajor, StrategyKind, KernelStats, combined_select,
+    CsrMatrix, estimate_nnz, count_mults, install
+"""
+
+from ._lib import build as _build_lib
+from .formats import INDEX_DTYPE, VALUE_DTYPE, CsrMatrix, validate_csr
+from .install import install
+from .kernels import (
+    KernelStats,
+    StrategyKind,
+    combined_select,
+    estimate_nnz,
+    multiply_rowmajor,
+    row_products_prefix,
+)
+from .perfmodel import FlopCount, bytes_alg, count_mults, inner_loop_balance, roofline
+
+__version__ = "0.1.0"
+
+
+def build(verbose: bool = False) -> str:
+    """Compile libspmmm.so (sm_100a) in place; returns its path."""
+    return _build_lib(verbose)
+
+
+__all__ = [
+    "CsrMatrix", "FlopCount", "INDEX_DTYPE", "KernelStats", "StrategyKind", "VALUE_DTYPE",
+    "build", "bytes_alg", "combined_select", "count_mults", "estimate_nnz",
+    "inner_loop_balance", "install", "multiply_rowmajor", "roofline", "row_products_prefix",
+    "validate_csr",
+]

@@ -1,0 +1,325 @@
+// Count, long-row-listing and long-row kernels (used only by spmmm.cu).
+#pragma once
+
+#include "device.cuh"
+
+namespace spmmm {
+
+// ctrl words (device, zeroed before every multiply)
+enum Ctrl : int {
+  kCtrlTotal = 0,     // Σ products (estimate_nnz)
+  kCtrlMaxProd = 1,   // max products of one row
+  kCtrlNeedTable = 2, // some row needs the medium/long machinery
+  kCtrlError = 3,     // bit flags: 1 A.row_ptr, 2 A.col_idx range, 4 B.row_ptr, 8 row too long
+  kCtrlLongRows = 4,  // number of rows listed by k_collect
+  kCtrlStageCursor = 5,
+  kCtrlWords = 8
+};
+
+// ---------------------------------------------------------------------------
+// K1: per-row product counts. formats.py:276-289 per row.
+__global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
+                                               unsigned long long* __restrict__ ctrl) {
+  uint64_t tot = 0, mx = 0;
+  uint32_t need = 0, err = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < A.rows; r += stride) {
+    const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
+    uint64_t p = 0;
+    if (hi < lo || hi > A.nnz) {
+      err |= 1u;
+    } else {
+      for (uint64_t e = lo; e < hi; ++e) {
+        const uint64_t k = ld_idx(A.ci + e);
+        if (k >= B.rows) { err |= 2u; continue; }
+        const uint64_t b0 = ld_idx(B.rp + k), b1 = ld_idx(B.rp + k + 1);
+        if (b1 < b0 || b1 > B.nnz) { err |= 4u; continue; }
+        p += b1 - b0;
+      }
+    }
+    if (p > 0x7fffffffull) err |= 8u;
+    prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
+    tot += p;
+    mx = p > mx ? p : mx;
+    if (p > 32 || (p > 0 && hi - lo > 32)) need = 1;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    tot += __shfl_xor_sync(kFull, tot, d);
+    const uint64_t o = __shfl_xor_sync(kFull, mx, d);
+    mx = o > mx ? o : mx;
+    need |= __shfl_xor_sync(kFull, need, d);
+    err |= __shfl_xor_sync(kFull, err, d);
+  }
+  if (lane_id() == 0) {
+    if (tot) atomicAdd(ctrl + kCtrlTotal, (unsigned long long)tot);
+    if (mx) atomicMax(ctrl + kCtrlMaxProd, (unsigned long long)mx);
+    if (need) atomicOr(ctrl + kCtrlNeedTable, 1ull);
+    if (err) atomicOr(ctrl + kCtrlError, (unsigned long long)err);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: list the long rows (warp-aggregated append; order is irrelevant).
+__global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __restrict__ prod,
+                                                 uint32_t medium_limit, uint32_t* __restrict__ list,
+                                                 uint32_t* __restrict__ lmap,
+                                                 unsigned long long* __restrict__ ctrl) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // warp-uniform trip count so the ballots are full-warp
+  const uint64_t span = (A.rows + stride - 1) / stride;
+  for (uint64_t it = 0; it < span; ++it) {
+    const uint64_t r = start + it * stride;
+    bool is_long = false;
+    if (r < A.rows) {
+      const uint64_t na = ld_idx(A.rp + r + 1) - ld_idx(A.rp + r);
+      is_long = classify(prod[r], na, medium_limit) == kRowLong;
+    }
+    const uint32_t m = __ballot_sync(kFull, is_long);
+    if (!m) continue;
+    uint32_t base = 0;
+    if (lane_id() == 0) base = uint32_t(atomicAdd(ctrl + kCtrlLongRows, (unsigned long long)__popc(m)));
+    base = __shfl_sync(kFull, base, 0);
+    if (is_long) {
+      const uint32_t idx = base + __popc(m & lanemask_lt());
+      list[idx] = uint32_t(r);
+      lmap[r] = idx;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: long rows, one 512-thread block per row, workspace in global memory
+// (hash table + column bitmap per resident block, restored after each row).
+//
+// Order: products are enumerated in chunks of 512 in (k, j) order. Within a
+// chunk, products hitting the same column are applied in rounds: each round
+// every pending product bids its global product index with atomicMin on its
+// slot's owner word; the lowest index wins and adds, so each column sees its
+// products in ascending order — the reference's left fold (kernels.py:167-174).
+// Output order: the bitmap over [min col, max col] is scanned in order, so the
+// row comes out sorted without a comparison sort (the paper's BruteForce-bool
+// lookup idea, kernels.py:106-113 / 216-227, on the GPU).
+constexpr int kLongThreads = 512;
+
+struct LongParams {
+  DevCsr A, B;
+  const uint32_t* prod;
+  const uint32_t* list;
+  unsigned long long* ctrl;
+  uint64_t* l_off;
+  uint32_t* l_nnz;
+  uint64_t* l_ci;
+  double* l_v;
+  uint32_t* ws_keys;   // [grid][slots]
+  double* ws_vals;     // [grid][slots]
+  uint32_t* ws_owner;  // [grid][slots]
+  uint32_t* ws_bits;   // [grid][words]
+  uint64_t ws_slots;   // power of two >= 2 * max products of a long row
+  uint64_t ws_words;   // ceil(cols / 32)
+  uint32_t* st_min;
+  uint32_t* st_max;
+  uint32_t* st_touch;
+};
+
+// full-avalanche 32-bit mixer (the table is masked to its low bits)
+__device__ __forceinline__ uint32_t long_hash(uint32_t x, uint32_t mask) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x & mask;
+}
+
+__device__ __forceinline__ uint32_t long_probe(const uint32_t* keys, uint32_t col, uint32_t mask) {
+  uint32_t h = long_hash(col, mask);
+  while (__ldcg(keys + h) != col) h = (h + 1) & mask;
+  return h;
+}
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* scratch, uint32_t& total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t incl = warp_incl_scan(x);
+  if (lane == 31) scratch[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < uint32_t(NT / 32) ? scratch[lane] : 0u;
+    const uint32_t wi = warp_incl_scan(w);
+    if (lane < uint32_t(NT / 32)) scratch[lane] = wi - w;
+    if (lane == 31) scratch[NT / 32] = wi;
+  }
+  __syncthreads();
+  const uint32_t res = scratch[warp] + incl - x;
+  total = scratch[NT / 32];
+  __syncthreads();
+  return res;
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
+  constexpr int NT = kLongThreads;
+  __shared__ uint32_t s_excl[NT + 1];
+  __shared__ uint64_t s_bs[NT];
+  __shared__ double s_av[NT];
+  __shared__ uint32_t s_scan[NT / 32 + 1];
+  __shared__ uint32_t s_min, s_max, s_touch;
+  __shared__ unsigned long long s_off;
+
+  const uint32_t tid = threadIdx.x;
+  uint32_t* keys = p.ws_keys + uint64_t(blockIdx.x) * p.ws_slots;
+  double* vals = p.ws_vals + uint64_t(blockIdx.x) * p.ws_slots;
+  uint32_t* owner = p.ws_owner + uint64_t(blockIdx.x) * p.ws_slots;
+  uint32_t* bits = p.ws_bits + uint64_t(blockIdx.x) * p.ws_words;
+  const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
+
+  for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
+    const uint32_t r = p.list[li];
+    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
+    const uint32_t prod = p.prod[r];
+    uint32_t tsize = 64;
+    while (uint64_t(tsize) < 2ull * prod && uint64_t(tsize) < p.ws_slots) tsize <<= 1;
+    const uint32_t mask = tsize - 1;
+    if (tid == 0) { s_min = kEmptyKey; s_max = 0; s_touch = 0; }
+    __syncthreads();
+    uint32_t touches = 0;
+    uint32_t seq_base = 0;
+    for (uint64_t abase = lo; abase < hi; abase += NT) {
+      const uint64_t e = abase + tid;
+      uint32_t len = 0;
+      uint64_t bs = 0;
+      double av = 0.0;
+      if (e < hi) {
+        const uint64_t k = ld_idx(p.A.ci + e);
+        av = ld_val(p.A.v + e);
+        bs = ld_idx(p.B.rp + k);
+        len = uint32_t(ld_idx(p.B.rp + k + 1) - bs);
+      }
+      uint32_t total;
+      const uint32_t ex = block_excl_scan<NT>(len, s_scan, total);
+      s_excl[tid] = ex;
+      s_bs[tid] = bs;
+      s_av[tid] = av;
+      if (tid == 0) s_excl[NT] = total;
+      __syncthreads();
+      for (uint32_t cb = 0; cb < total; cb += NT) {
+        const uint32_t q = cb + tid;
+        const bool act = q < total;
+        uint32_t col = 0, slot = 0;
+        double pv = 0.0;
+        if (act) {
+          // largest i with s_excl[i] <= q
+          int i = 0;
+#pragma unroll
+          for (int st = NT / 2; st > 0; st >>= 1)
+            if (s_excl[i + st] <= q) i += st;
+          const uint64_t src = s_bs[i] + (q - s_excl[i]);
+          col = uint32_t(ld_idx(p.B.ci + src));
+          pv = __dmul_rn(s_av[i], ld_val(p.B.v + src));
+          uint32_t h = long_hash(col, mask);
+          while (true) {
+            const uint32_t k = __ldcg(keys + h);
+            if (k == col) break;
+            if (k == kEmptyKey) {
+              const uint32_t old = atomicCAS(keys + h, kEmptyKey, col);
+              if (old == kEmptyKey) {
+                atomicOr(bits + (col >> 5), 1u << (col & 31));
+                atomicMin(&s_min, col);
+                atomicMax(&s_max, col);
+                break;
+              }
+              if (old == col) break;
+            }
+            h = (h + 1) & mask;
+          }
+          slot = h;
+        }
+        const uint32_t seq = seq_base + q;
+        bool pending = act;
+        while (__syncthreads_or(pending)) {
+          if (pending) atomicMin(owner + slot, seq);
+          __syncthreads();
+          if (pending && atomicAdd(owner + slot, 0u) == seq) {
+            const double cur = __ldcg(vals + slot);
+            if (STATS && cur == 0.0) ++touches;
+            __stcg(vals + slot, __dadd_rn(cur, pv));
+            atomicExch(owner + slot, kEmptyKey);
+            pending = false;
+          }
+          __syncthreads();
+        }
+      }
+      seq_base += total;
+      __syncthreads();
+    }
+    // ---- ordered extraction over the bitmap, dropping exact zeros ----
+    const uint32_t cmin = s_min, cmax = s_max;
+    uint32_t nz_total = 0;
+    uint32_t mine = 0, w_begin = 0, w_end = 0;
+    if (cmin <= cmax) {
+      const uint32_t w0 = cmin >> 5, w1 = cmax >> 5;
+      const uint32_t nw = w1 - w0 + 1;
+      const uint32_t per = (nw + NT - 1) / NT;
+      w_begin = w0 + tid * per;
+      w_end = w_begin + per;
+      if (w_begin > w1 + 1) w_begin = w1 + 1;
+      if (w_end > w1 + 1) w_end = w1 + 1;
+      for (uint32_t w = w_begin; w < w_end; ++w) {
+        uint32_t b = __ldcg(bits + w), nzb = 0;
+        while (b) {
+          const uint32_t bit = __ffs(b) - 1;
+          b &= b - 1;
+          const uint32_t col = (w << 5) | bit;
+          const uint32_t s = long_probe(keys, col, mask);
+          if (__ldcg(vals + s) != 0.0) nzb |= 1u << bit;
+        }
+        mine += __popc(nzb);
+        __stcg(bits + w, nzb);
+      }
+    }
+    const uint32_t my_base = block_excl_scan<NT>(mine, s_scan, nz_total);
+    if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)nz_total);
+    __syncthreads();
+    uint64_t pos = s_off + my_base;
+    for (uint32_t w = w_begin; w < w_end; ++w) {
+      uint32_t b = __ldcg(bits + w);
+      while (b) {
+        const uint32_t bit = __ffs(b) - 1;
+        b &= b - 1;
+        const uint32_t col = (w << 5) | bit;
+        const uint32_t s = long_probe(keys, col, mask);
+        p.l_ci[pos] = col;
+        p.l_v[pos] = __ldcg(vals + s);
+        ++pos;
+      }
+    }
+    if (STATS) {
+      uint32_t t = touches;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
+      if (lane_id() == 0 && t) atomicAdd(&s_touch, t);
+    }
+    __syncthreads();
+    // restore the workspace for the next row
+    for (uint32_t s = tid; s < tsize; s += NT) {
+      __stcg(keys + s, kEmptyKey);
+      __stcg(vals + s, 0.0);
+    }
+    if (cmin <= cmax)
+      for (uint32_t w = (cmin >> 5) + tid; w <= (cmax >> 5); w += NT) __stcg(bits + w, 0u);
+    if (tid == 0) {
+      p.l_off[li] = s_off;
+      p.l_nnz[li] = nz_total;
+      if (STATS) {
+        p.st_min[r] = cmin;
+        p.st_max[r] = cmax;
+        p.st_touch[r] = s_touch;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace spmmm

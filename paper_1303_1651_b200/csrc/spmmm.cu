@@ -1,0 +1,694 @@
+// Host side of libspmmm.so: contexts, device memory, the launch sequence of
+// one C = A·B, and the C ABI declared in include/spmmm.h.
+//
+// One multiply (device-resident operands) is:
+//   memset(ctrl) -> k_count -> [D2H 64 B, sync]          (size C, pick the kernel)
+//   [k_collect -> k_long]            only when some row is too long for k_fused
+//   memset(C.row_ptr[0]) -> k_fused (cooperative, persistent)
+//   [D2H 8 B of C.row_ptr[rows], sync]                    (nnz(C) for the caller)
+// The reference does the same two steps host-side: estimate_nnz then one
+// reservation (kernels.py:314, formats.py:199-205), then the row loop.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/spmmm.h"
+#include "aux_kernels.cuh"
+#include "fused_launch.cuh"
+
+using namespace spmmm;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      return fail(_e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,       \
+                  "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__,        \
+                  __LINE__);                                                              \
+    }                                                                                     \
+  } while (0)
+
+// Grow-only device buffer allocated from the stream-ordered pool.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+cudaError_t ensure(DevBuf& b, size_t bytes, cudaStream_t s, bool* grown = nullptr) {
+  if (grown) *grown = false;
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) {
+    cudaError_t e = cudaFreeAsync(b.p, s);
+    if (e != cudaSuccess) return e;
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t want = std::max(bytes, size_t(256));
+  cudaError_t e = cudaMallocAsync(&b.p, want, s);
+  if (e != cudaSuccess) return e;
+  b.cap = want;
+  if (grown) *grown = true;
+  return cudaSuccess;
+}
+
+void release(DevBuf& b, cudaStream_t s) {
+  if (b.p) cudaFreeAsync(b.p, s);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused"};
+constexpr int kNumKernels = 4;
+
+}  // namespace
+
+struct spmmm_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sms = 148;
+  std::mutex mu;
+  DevBuf ctrl, prod, lmap, list, status, l_off, l_nnz, ws;
+  DevBuf a_rp, a_ci, a_v, b_rp, b_ci, b_v;
+  unsigned long long* h_ctrl = nullptr;  // pinned mirror of ctrl
+  uint32_t epoch = 0;
+  uint64_t status_cap_tiles = 0;
+  uint64_t ws_slots = 0, ws_words = 0;
+  int ws_grid = 0;
+  cudaEvent_t ev[2 * kNumKernels] = {};
+  bool ev_used[kNumKernels] = {};
+  double last_ms[kNumKernels] = {};
+  int last_count = 0;
+  int last_launches = 0;
+};
+
+struct spmmm_product {
+  spmmm_context* ctx = nullptr;
+  uint64_t rows = 0, cols = 0, nnz = 0, mults = 0;
+  uint64_t* rp = nullptr;
+  uint64_t* ci = nullptr;
+  double* v = nullptr;
+  uint32_t* st = nullptr;  // 3 * rows (min, max, touched) when row stats were requested
+};
+
+namespace {
+
+// ---- operand views --------------------------------------------------------
+
+int check_view(const spmmm_csr* m, const char* name) {
+  if (!m) return fail(SPMMM_ERR_INVALID, "%s is NULL", name);
+  if (!m->row_ptr) return fail(SPMMM_ERR_INVALID, "%s.row_ptr is NULL", name);
+  if (m->nnz && (!m->col_idx || !m->values))
+    return fail(SPMMM_ERR_INVALID, "%s has nnz=%llu but NULL arrays", name,
+                (unsigned long long)m->nnz);
+  if (m->memory != SPMMM_MEM_HOST && m->memory != SPMMM_MEM_DEVICE)
+    return fail(SPMMM_ERR_INVALID, "%s.memory=%d is not host/device", name, m->memory);
+  return SPMMM_OK;
+}
+
+// Upload a host CSR view into context buffers; return a device view.
+int upload(spmmm_context* c, const spmmm_csr* m, DevBuf& rp, DevBuf& ci, DevBuf& v, DevCsr* out) {
+  const size_t rpb = (m->rows + 1) * sizeof(uint64_t);
+  const size_t cib = m->nnz * sizeof(uint64_t), vb = m->nnz * sizeof(double);
+  CUDA_TRY(ensure(rp, rpb, c->stream));
+  CUDA_TRY(ensure(ci, cib, c->stream));
+  CUDA_TRY(ensure(v, vb, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(rp.p, m->row_ptr, rpb, cudaMemcpyHostToDevice, c->stream));
+  if (m->nnz) {
+    CUDA_TRY(cudaMemcpyAsync(ci.p, m->col_idx, cib, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(v.p, m->values, vb, cudaMemcpyHostToDevice, c->stream));
+  }
+  out->rp = static_cast<const uint64_t*>(rp.p);
+  out->ci = static_cast<const uint64_t*>(ci.p);
+  out->v = static_cast<const double*>(v.p);
+  out->rows = m->rows;
+  out->cols = m->cols;
+  out->nnz = m->nnz;
+  return SPMMM_OK;
+}
+
+int resolve(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, DevCsr* A, DevCsr* B) {
+  if (a->memory == SPMMM_MEM_DEVICE) {
+    *A = DevCsr{a->row_ptr, a->col_idx, a->values, a->rows, a->cols, a->nnz};
+  } else {
+    int rc = upload(c, a, c->a_rp, c->a_ci, c->a_v, A);
+    if (rc) return rc;
+  }
+  if (b->memory == SPMMM_MEM_DEVICE) {
+    *B = DevCsr{b->row_ptr, b->col_idx, b->values, b->rows, b->cols, b->nnz};
+  } else if (a->memory == SPMMM_MEM_HOST && a->row_ptr == b->row_ptr &&
+             a->col_idx == b->col_idx && a->values == b->values && a->rows == b->rows &&
+             a->nnz == b->nnz) {
+    *B = *A;  // C = A·A: one upload (C1, C2, C4 are squares of one matrix)
+    B->cols = b->cols;
+  } else {
+    int rc = upload(c, b, c->b_rp, c->b_ci, c->b_v, B);
+    if (rc) return rc;
+  }
+  return SPMMM_OK;
+}
+
+// ---- timing helpers ---------------------------------------------------------
+
+struct Timer {
+  spmmm_context* c;
+  bool on;
+  void begin(int k) {
+    if (on) { cudaEventRecord(c->ev[2 * k], c->stream); c->ev_used[k] = true; }
+  }
+  void end(int k) {
+    if (on) cudaEventRecord(c->ev[2 * k + 1], c->stream);
+  }
+};
+
+// ---- the count pass ----------------------------------------------------------
+
+int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm) {
+  CUDA_TRY(ensure(c->prod, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
+  if (A.rows) {
+    const uint64_t blocks = std::min<uint64_t>((A.rows + 255) / 256, uint64_t(c->sms) * 8);
+    tm.begin(0);
+    k_count<<<unsigned(blocks), 256, 0, c->stream>>>(
+        A, B, static_cast<uint32_t*>(c->prod.p), static_cast<unsigned long long*>(c->ctrl.p));
+    CUDA_TRY(cudaGetLastError());
+    tm.end(0);
+    ++c->last_launches;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, kCtrlWords * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const unsigned long long err = c->h_ctrl[kCtrlError];
+  if (err & 1) return fail(SPMMM_ERR_INVALID, "malformed a.row_ptr (decreasing or past nnz)");
+  if (err & 2) return fail(SPMMM_ERR_INVALID, "a.col_idx entry >= b.rows");
+  if (err & 4) return fail(SPMMM_ERR_INVALID, "malformed b.row_ptr (decreasing or past nnz)");
+  if (err & 8) return fail(SPMMM_ERR_UNSUPPORTED, "a row of C needs more than 2^31 products");
+  return SPMMM_OK;
+}
+
+// ---- fused-kernel launch: instantiations live in fused_t*.cu (parallel build) ----
+
+constexpr int kWarps = kFusedWarps;
+constexpr int kShortRowsPerWarp = kFusedShortRowsPerWarp;
+
+int rows_per_tile(int table) { return table == 0 ? kWarps * kShortRowsPerWarp : kWarps; }
+
+int dispatch_fused(spmmm_context* c, FusedParams& prm, int table, bool wide, bool stats) {
+  FusedLaunchEnv env{c->device, c->sms, c->stream};
+  cudaError_t e;
+  switch (table) {
+    case 0: e = launch_fused_t0(prm, env, wide, stats); break;
+    case 256: e = launch_fused_t256(prm, env, wide, stats); break;
+    case 512: e = launch_fused_t512(prm, env, wide, stats); break;
+    case 1024: e = launch_fused_t1024(prm, env, wide, stats); break;
+    default: return fail(SPMMM_ERR_INVALID, "no fused kernel for table size %d", table);
+  }
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
+                "k_fused<table=%d> launch: %s", table, cudaGetErrorString(e));
+  return SPMMM_OK;
+}
+
+// ---- the long-row path ------------------------------------------------------
+
+int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_prod,
+             uint32_t medium_limit, uint64_t total, bool stats, spmmm_product* p,
+             DevBuf& stage_ci, DevBuf& stage_v, Timer& tm) {
+  const uint64_t rows = A.rows;
+  CUDA_TRY(ensure(c->lmap, rows * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(c->list, rows * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(c->l_off, rows * sizeof(uint64_t), c->stream));
+  CUDA_TRY(ensure(c->l_nnz, rows * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
+  CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
+  // workspace: one table (>= 2x the distinct columns a row can have) and one
+  // column bitmap per resident block
+  uint64_t distinct = std::min<uint64_t>(max_prod, std::max<uint64_t>(B.cols, 1));
+  uint64_t slots = 64;
+  while (slots < 2 * distinct) slots <<= 1;
+  const uint64_t words = std::max<uint64_t>((B.cols + 31) / 32, 1);
+  const uint64_t per_block = slots * (4 + 8 + 4) + words * 4;
+  int grid = 2 * c->sms;
+  const uint64_t budget = 8ull << 30;  // cap the workspace at 8 GiB
+  while (grid > 1 && uint64_t(grid) * per_block > budget) grid /= 2;
+  if (slots != c->ws_slots || words != c->ws_words || grid != c->ws_grid) {
+    release(c->ws, c->stream);
+    CUDA_TRY(ensure(c->ws, size_t(grid) * per_block, c->stream));
+    char* base = static_cast<char*>(c->ws.p);
+    const size_t n = size_t(grid) * slots;
+    CUDA_TRY(cudaMemsetAsync(base, 0xff, n * 4, c->stream));                   // keys
+    CUDA_TRY(cudaMemsetAsync(base + n * 4, 0, n * 8, c->stream));             // vals
+    CUDA_TRY(cudaMemsetAsync(base + n * 12, 0xff, n * 4, c->stream));         // owner
+    CUDA_TRY(cudaMemsetAsync(base + n * 16, 0, size_t(grid) * words * 4, c->stream));  // bits
+    c->ws_slots = slots;
+    c->ws_words = words;
+    c->ws_grid = grid;
+  }
+  {
+    const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
+    tm.begin(1);
+    k_collect<<<unsigned(blocks), 256, 0, c->stream>>>(
+        A, static_cast<const uint32_t*>(c->prod.p), medium_limit,
+        static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p),
+        static_cast<unsigned long long*>(c->ctrl.p));
+    CUDA_TRY(cudaGetLastError());
+    tm.end(1);
+    ++c->last_launches;
+  }
+  LongParams lp;
+  lp.A = A;
+  lp.B = B;
+  lp.prod = static_cast<const uint32_t*>(c->prod.p);
+  lp.list = static_cast<const uint32_t*>(c->list.p);
+  lp.ctrl = static_cast<unsigned long long*>(c->ctrl.p);
+  lp.l_off = static_cast<uint64_t*>(c->l_off.p);
+  lp.l_nnz = static_cast<uint32_t*>(c->l_nnz.p);
+  lp.l_ci = static_cast<uint64_t*>(stage_ci.p);
+  lp.l_v = static_cast<double*>(stage_v.p);
+  char* base = static_cast<char*>(c->ws.p);
+  const size_t n = size_t(c->ws_grid) * c->ws_slots;
+  lp.ws_keys = reinterpret_cast<uint32_t*>(base);
+  lp.ws_vals = reinterpret_cast<double*>(base + n * 4);
+  lp.ws_owner = reinterpret_cast<uint32_t*>(base + n * 12);
+  lp.ws_bits = reinterpret_cast<uint32_t*>(base + n * 16);
+  lp.ws_slots = c->ws_slots;
+  lp.ws_words = c->ws_words;
+  lp.st_min = p->st;
+  lp.st_max = p->st ? p->st + rows : nullptr;
+  lp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+  tm.begin(2);
+  if (stats) k_long<true><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
+  else k_long<false><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
+  CUDA_TRY(cudaGetLastError());
+  tm.end(2);
+  ++c->last_launches;
+  return SPMMM_OK;
+}
+
+int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
+                  uint32_t flags, spmmm_product** out) {
+  if (!out) return fail(SPMMM_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (strategy < SPMMM_STRATEGY_BFDOUBLE || strategy > SPMMM_STRATEGY_COMBINED)
+    return fail(SPMMM_ERR_INVALID, "unknown strategy %d", strategy);
+  int rc = check_view(a, "a");
+  if (rc) return rc;
+  rc = check_view(b, "b");
+  if (rc) return rc;
+  if (a->cols != b->rows)
+    return fail(SPMMM_ERR_DIMENSION, "dimension mismatch: %llu (cols of a) != %llu (rows of b)",
+                (unsigned long long)a->cols, (unsigned long long)b->rows);
+  if (b->cols > 0xffffffffull)
+    return fail(SPMMM_ERR_UNSUPPORTED, "b.cols=%llu exceeds the 32-bit column range",
+                (unsigned long long)b->cols);
+  if (a->rows >= 0xffffffffull)
+    return fail(SPMMM_ERR_UNSUPPORTED, "a.rows=%llu exceeds the 32-bit row range",
+                (unsigned long long)a->rows);
+  const bool stats = flags & SPMMM_FLAG_ROW_STATS;
+  Timer tm{c, bool(flags & SPMMM_FLAG_TIMING)};
+  for (int k = 0; k < kNumKernels; ++k) c->ev_used[k] = false;
+  c->last_count = 0;
+  c->last_launches = 0;
+  CUDA_TRY(cudaSetDevice(c->device));
+
+  DevCsr A, B;
+  rc = resolve(c, a, b, &A, &B);
+  if (rc) return rc;
+  const uint64_t rows = A.rows;
+
+  rc = run_count(c, A, B, tm);
+  if (rc) return rc;
+  const uint64_t total = c->h_ctrl[kCtrlTotal];
+  const uint64_t max_prod = c->h_ctrl[kCtrlMaxProd];
+  const bool need_table = c->h_ctrl[kCtrlNeedTable] != 0;
+
+  // Table size for medium rows: big enough that a row's distinct columns
+  // (<= its products) stay under 3/4 load; rows beyond 768 products go long.
+  int table = 0;
+  if (need_table) table = max_prod <= 192 ? 256 : (max_prod <= 384 ? 512 : 1024);
+  const uint32_t medium_limit = uint32_t(table * 3 / 4);
+  const int logt = table ? __builtin_ctz(table) : 5;
+  const bool wide = B.cols > (1ull << (32 - logt));
+
+  auto* p = new (std::nothrow) spmmm_product;
+  if (!p) return fail(SPMMM_ERR_OOM, "host allocation failed");
+  p->ctx = c;
+  p->rows = rows;
+  p->cols = B.cols;
+  p->mults = total;
+  auto cleanup = [&](int code) {
+    if (p->rp) cudaFreeAsync(p->rp, c->stream);
+    if (p->ci) cudaFreeAsync(p->ci, c->stream);
+    if (p->v) cudaFreeAsync(p->v, c->stream);
+    if (p->st) cudaFreeAsync(p->st, c->stream);
+    delete p;
+    return code;
+  };
+  // C storage: one reservation of `total` entries (the reference's own
+  // capacity rule: CsrBuilder(..., estimate_nnz(a, b)), kernels.py:314)
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p->rp), (rows + 1) * 8, c->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&p->ci),
+                                            std::max<uint64_t>(total, 1) * 8, c->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&p->v),
+                                            std::max<uint64_t>(total, 1) * 8, c->stream);
+  if (e == cudaSuccess && stats)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&p->st),
+                        std::max<uint64_t>(rows, 1) * 3 * sizeof(uint32_t), c->stream);
+  if (e != cudaSuccess)
+    return cleanup(fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
+                        "allocating C (%llu entries): %s", (unsigned long long)total,
+                        cudaGetErrorString(e)));
+  e = cudaMemsetAsync(p->rp, 0, sizeof(uint64_t), c->stream);
+  if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+
+  DevBuf stage_ci, stage_v;
+  const bool has_long = table > 0 && max_prod > medium_limit;
+  if (rows && has_long) {
+    rc = run_long(c, A, B, max_prod, medium_limit, total, stats, p, stage_ci, stage_v, tm);
+    if (rc) { release(stage_ci, c->stream); release(stage_v, c->stream); return cleanup(rc); }
+  }
+
+  if (rows) {
+    const uint64_t ntiles = (rows + rows_per_tile(table) - 1) / rows_per_tile(table);
+    bool grown = false;
+    e = ensure(c->status, ntiles * sizeof(uint64_t), c->stream, &grown);
+    if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_OOM, "status: %s", cudaGetErrorString(e)));
+    if (grown || c->epoch >= 0xffffu) {
+      e = cudaMemsetAsync(c->status.p, 0, c->status.cap, c->stream);
+      if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+      c->epoch = 0;
+    }
+    c->epoch += 1;
+    FusedParams fp;
+    fp.A = A;
+    fp.B = B;
+    fp.prod = static_cast<const uint32_t*>(c->prod.p);
+    fp.lmap = static_cast<const uint32_t*>(c->lmap.p);
+    fp.l_off = static_cast<const uint64_t*>(c->l_off.p);
+    fp.l_nnz = static_cast<const uint32_t*>(c->l_nnz.p);
+    fp.l_ci = static_cast<const uint64_t*>(stage_ci.p);
+    fp.l_v = static_cast<const double*>(stage_v.p);
+    fp.c_rp = p->rp;
+    fp.c_ci = p->ci;
+    fp.c_v = p->v;
+    fp.status = static_cast<uint64_t*>(c->status.p);
+    fp.ntiles = ntiles;
+    fp.epoch = c->epoch;
+    fp.medium_limit = medium_limit;
+    fp.st_min = p->st;
+    fp.st_max = p->st ? p->st + rows : nullptr;
+    fp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+    tm.begin(3);
+    rc = dispatch_fused(c, fp, table, wide, stats);
+    if (rc) { release(stage_ci, c->stream); release(stage_v, c->stream); return cleanup(rc); }
+    tm.end(3);
+    ++c->last_launches;
+  }
+  release(stage_ci, c->stream);
+  release(stage_v, c->stream);
+  e = cudaMemcpyAsync(c->h_ctrl + kCtrlWords - 1, p->rp + rows, sizeof(uint64_t),
+                      cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
+  p->nnz = c->h_ctrl[kCtrlWords - 1];
+  if (tm.on) {
+    for (int k = 0; k < kNumKernels; ++k) {
+      if (!c->ev_used[k]) continue;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]);
+      c->last_ms[k] = ms;
+    }
+  }
+  *out = p;
+  return SPMMM_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+int spmmm_abi_version(void) { return SPMMM_ABI_VERSION; }
+
+const char* spmmm_last_error(void) { return g_error.c_str(); }
+
+int spmmm_device_count(int* count) {
+  if (!count) return fail(SPMMM_ERR_INVALID, "count is NULL");
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(SPMMM_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  return SPMMM_OK;
+}
+
+int spmmm_context_create(int device, void* cuda_stream, spmmm_context** out) {
+  if (!out) return fail(SPMMM_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n)
+    return fail(SPMMM_ERR_INVALID, "device %d out of range (%d devices)", device, n);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(SPMMM_ERR_UNSUPPORTED, "device %d is sm_%d%d; libspmmm is built for sm_100a",
+                device, prop.major, prop.minor);
+  if (!prop.cooperativeLaunch)
+    return fail(SPMMM_ERR_UNSUPPORTED, "device %d lacks cooperative launch", device);
+  auto* c = new (std::nothrow) spmmm_context;
+  if (!c) return fail(SPMMM_ERR_OOM, "host allocation failed");
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  // keep freed blocks in the pool: repeated products reuse their memory
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaError_t e = cudaSuccess;
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    c->own_stream = true;
+  }
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_ctrl, kCtrlWords * sizeof(unsigned long long));
+  for (int k = 0; k < 2 * kNumKernels && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
+  if (e == cudaSuccess) e = ensure(c->ctrl, kCtrlWords * sizeof(unsigned long long), c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(SPMMM_ERR_CUDA, "context_create: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return SPMMM_OK;
+}
+
+int spmmm_context_destroy(spmmm_context* c) {
+  if (!c) return SPMMM_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
+                    &c->ws, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
+    release(*b, c->stream);
+  cudaStreamSynchronize(c->stream);
+  for (int k = 0; k < 2 * kNumKernels; ++k)
+    if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+  if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return SPMMM_OK;
+}
+
+int spmmm_synchronize(spmmm_context* c) {
+  if (!c) return fail(SPMMM_ERR_INVALID, "context is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPMMM_OK;
+}
+
+int spmmm_multiply(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
+                   uint32_t flags, spmmm_product** out) {
+  if (!c) return fail(SPMMM_ERR_INVALID, "context is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  return multiply_impl(c, a, b, strategy, flags, out);
+}
+
+int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
+                        uint64_t* mults) {
+  if (!p) return fail(SPMMM_ERR_INVALID, "product is NULL");
+  if (rows) *rows = p->rows;
+  if (cols) *cols = p->cols;
+  if (nnz) *nnz = p->nnz;
+  if (mults) *mults = p->mults;
+  return SPMMM_OK;
+}
+
+int spmmm_product_device_arrays(const spmmm_product* p, const uint64_t** rp, const uint64_t** ci,
+                                const double** v) {
+  if (!p) return fail(SPMMM_ERR_INVALID, "product is NULL");
+  if (rp) *rp = p->rp;
+  if (ci) *ci = p->ci;
+  if (v) *v = p->v;
+  return SPMMM_OK;
+}
+
+int spmmm_product_download(spmmm_product* p, uint64_t* rp, uint64_t* ci, double* v) {
+  if (!p) return fail(SPMMM_ERR_INVALID, "product is NULL");
+  spmmm_context* c = p->ctx;
+  std::lock_guard<std::mutex> lock(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (rp) CUDA_TRY(cudaMemcpyAsync(rp, p->rp, (p->rows + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (p->nnz) {
+    if (ci) CUDA_TRY(cudaMemcpyAsync(ci, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (v) CUDA_TRY(cudaMemcpyAsync(v, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPMMM_OK;
+}
+
+int spmmm_product_copy_device(spmmm_product* p, uint64_t* rp, uint64_t* ci, double* v) {
+  if (!p) return fail(SPMMM_ERR_INVALID, "product is NULL");
+  spmmm_context* c = p->ctx;
+  std::lock_guard<std::mutex> lock(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (rp) CUDA_TRY(cudaMemcpyAsync(rp, p->rp, (p->rows + 1) * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (p->nnz) {
+    if (ci) CUDA_TRY(cudaMemcpyAsync(ci, p->ci, p->nnz * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if (v) CUDA_TRY(cudaMemcpyAsync(v, p->v, p->nnz * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPMMM_OK;
+}
+
+int spmmm_product_row_stats(spmmm_product* p, uint64_t* mn, uint64_t* mx, uint64_t* touched) {
+  if (!p) return fail(SPMMM_ERR_INVALID, "product is NULL");
+  if (!p->st) return fail(SPMMM_ERR_INVALID, "product was computed without SPMMM_FLAG_ROW_STATS");
+  spmmm_context* c = p->ctx;
+  std::lock_guard<std::mutex> lock(c->mu);
+  std::vector<uint32_t> h(size_t(p->rows) * 3);
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (p->rows) {
+    CUDA_TRY(cudaMemcpyAsync(h.data(), p->st, h.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  for (uint64_t r = 0; r < p->rows; ++r) {
+    const uint32_t lo = h[r], hi = h[p->rows + r], t = h[2 * p->rows + r];
+    const bool none = t == 0;
+    if (mn) mn[r] = none ? ~0ull : lo;
+    if (mx) mx[r] = none ? 0ull : hi;
+    if (touched) touched[r] = t;
+  }
+  return SPMMM_OK;
+}
+
+int spmmm_product_destroy(spmmm_product* p) {
+  if (!p) return SPMMM_OK;
+  spmmm_context* c = p->ctx;
+  std::lock_guard<std::mutex> lock(c->mu);
+  cudaSetDevice(c->device);
+  if (p->rp) cudaFreeAsync(p->rp, c->stream);
+  if (p->ci) cudaFreeAsync(p->ci, c->stream);
+  if (p->v) cudaFreeAsync(p->v, c->stream);
+  if (p->st) cudaFreeAsync(p->st, c->stream);
+  delete p;
+  return SPMMM_OK;
+}
+
+int spmmm_estimate_nnz(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, uint64_t* out) {
+  if (!c || !out) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  int rc = check_view(a, "a");
+  if (!rc) rc = check_view(b, "b");
+  if (rc) return rc;
+  if (a->cols != b->rows)
+    return fail(SPMMM_ERR_DIMENSION, "dimension mismatch: %llu (cols of a) != %llu (rows of b)",
+                (unsigned long long)a->cols, (unsigned long long)b->rows);
+  CUDA_TRY(cudaSetDevice(c->device));
+  DevCsr A, B;
+  rc = resolve(c, a, b, &A, &B);
+  if (rc) return rc;
+  Timer tm{c, false};
+  c->last_launches = 0;
+  rc = run_count(c, A, B, tm);
+  if (rc) return rc;
+  *out = c->h_ctrl[kCtrlTotal];
+  return SPMMM_OK;
+}
+
+int spmmm_row_products_prefix(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
+                              uint64_t* out) {
+  if (!c || !out) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  int rc = check_view(a, "a");
+  if (!rc) rc = check_view(b, "b");
+  if (rc) return rc;
+  if (a->cols != b->rows)
+    return fail(SPMMM_ERR_DIMENSION, "dimension mismatch: %llu (cols of a) != %llu (rows of b)",
+                (unsigned long long)a->cols, (unsigned long long)b->rows);
+  CUDA_TRY(cudaSetDevice(c->device));
+  DevCsr A, B;
+  rc = resolve(c, a, b, &A, &B);
+  if (rc) return rc;
+  Timer tm{c, false};
+  c->last_launches = 0;
+  rc = run_count(c, A, B, tm);
+  if (rc) return rc;
+  std::vector<uint32_t> h(A.rows);
+  if (A.rows) {
+    CUDA_TRY(cudaMemcpyAsync(h.data(), c->prod.p, A.rows * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  out[0] = 0;
+  for (uint64_t r = 0; r < A.rows; ++r) out[r + 1] = out[r] + h[r];
+  return SPMMM_OK;
+}
+
+int spmmm_last_timings(spmmm_context* c, const char** names, double* ms, int cap, int* count) {
+  if (!c || !count) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  int n = 0;
+  for (int k = 0; k < kNumKernels; ++k) {
+    if (!c->ev_used[k]) continue;
+    if (n < cap) {
+      if (names) names[n] = kKernelNames[k];
+      if (ms) ms[n] = c->last_ms[k];
+    }
+    ++n;
+  }
+  *count = n;
+  return SPMMM_OK;
+}
+
+int spmmm_last_launch_count(spmmm_context* c, int* count) {
+  if (!c || !count) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  *count = c->last_launches;
+  return SPMMM_OK;
+}
+
+}  // extern "C"

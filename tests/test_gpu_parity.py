@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden fixtures) and the pinned CPU oracle.
+
+Bar (north_star): C.row_ptr / C.col_idx bit-exact, values within 1e-12
+relative to the reference — the helper additionally flags any value that is
+not bit-identical, since the kernels reproduce the reference's summation
+order exactly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import (assert_csr_bitwise_equal, fingerprints, golden_case, golden_names,
+                      have_gpu)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not have_gpu(), reason="needs a CUDA device")]
+
+from paper_1303_1651_b200 import _lib, genmat  # noqa: E402
+from paper_1303_1651_b200.formats import CsrMatrix, validate_csr  # noqa: E402
+from paper_1303_1651_b200.kernels import (KernelStats, StrategyKind, estimate_nnz,  # noqa: E402
+                                          multiply_rowmajor, row_products_prefix)
+
+ALL_STRATEGIES = list(StrategyKind)
+
+
+def _oracle_csr(a, b):
+    r = oracle.multiply_rowmajor(a, b, threads=8)
+    return CsrMatrix(r.rows, r.cols, r.row_ptr, r.col_idx, r.values)
+
+
+def _choices_array(stats, rows):
+    out = np.full(rows, -1, np.int8)
+    for r, ch in stats.row_choices:
+        out[r] = 0 if ch == StrategyKind.MIN_MAX else 1
+    return out
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_case(name):
+    a, b, c_ref, mults, choices = golden_case(name)
+    stats = KernelStats()
+    c = multiply_rowmajor(a, b, StrategyKind.COMBINED, stats)
+    assert_csr_bitwise_equal(c, c_ref, name)
+    assert stats.multiplications == mults
+    assert np.array_equal(_choices_array(stats, a.rows), choices), name
+    assert estimate_nnz(a, b) == mults
+    validate_csr(c)
+
+
+def test_strategies_are_bitwise_unanimous():
+    for name in ("random_0", "signed_k40", "long_rows", "medium_rows", "fd_9"):
+        a, b, c_ref, _, _ = golden_case(name)
+        for s in ALL_STRATEGIES:
+            assert_csr_bitwise_equal(multiply_rowmajor(a, b, s), c_ref, f"{name}/{s.value}")
+
+
+def test_errors_match_reference():
+    a, b, _, _, _ = golden_case("rect_7x13_13x5")
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        multiply_rowmajor(b, b)
+    with pytest.raises(ValueError):
+        multiply_rowmajor(a, b, "quicksort")
+
+
+def test_malformed_input_raises_instead_of_faulting():
+    a = CsrMatrix(2, 3, np.array([0, 2, 1], np.uint64), np.array([0, 1], np.uint64),
+                  np.array([1.0, 2.0]))
+    b = CsrMatrix(3, 3, np.array([0, 1, 2, 3], np.uint64), np.array([0, 1, 2], np.uint64),
+                  np.ones(3))
+    with pytest.raises(ValueError, match="row_ptr"):
+        multiply_rowmajor(a, b)
+    a2 = CsrMatrix(1, 3, np.array([0, 1], np.uint64), np.array([7], np.uint64), np.ones(1))
+    with pytest.raises(ValueError):
+        multiply_rowmajor(a2, b)
+
+
+def _rand_csr(rng, rows, cols, per_row_max, values="uniform", min_len=0):
+    lens = rng.integers(min_len, per_row_max + 1, size=rows)
+    lens = np.minimum(lens, cols)
+    rp = np.zeros(rows + 1, np.uint64)
+    rp[1:] = np.cumsum(lens)
+    ci = np.empty(int(rp[-1]), np.uint64)
+    for r in range(rows):
+        picked = np.unique(rng.integers(0, cols, size=lens[r]))
+        while picked.size < lens[r]:
+            picked = np.unique(np.concatenate([picked, rng.integers(0, cols, size=lens[r])]))
+        ci[rp[r]:rp[r + 1]] = np.sort(rng.permutation(picked)[:lens[r]])
+    n = ci.size
+    if values == "uniform":
+        v = rng.uniform(-1.0, 1.0, n)
+    elif values == "quantized":  # many exact cancellations
+        v = rng.choice([-2.0, -1.0, 1.0, 2.0], n)
+    else:
+        v = rng.uniform(0.1, 1.0, n)
+    return CsrMatrix(rows, cols, rp, ci, v)
+
+
+@pytest.mark.parametrize("seed,shape", [
+    (1, (300, 200, 150, 8, 8)),          # short rows
+    (2, (400, 300, 500, 20, 20)),        # medium rows (table 256/512)
+    (3, (200, 150, 400, 40, 30)),        # medium rows, table 1024
+    (4, (60, 2000, 3000, 1500, 6)),      # long rows (k_long)
+    (5, (500, 64, 64, 64, 64)),          # collision heavy, dense-ish
+    (6, (1000, 3000, 5000, 45, 4)),      # A rows longer than 32, short B rows
+])
+@pytest.mark.parametrize("values", ["uniform", "quantized"])
+def test_random_vs_oracle(seed, shape, values):
+    rows, inner, cols, amax, bmax = shape
+    rng = np.random.default_rng(seed)
+    a = _rand_csr(rng, rows, inner, amax, values)
+    b = _rand_csr(rng, inner, cols, bmax, values)
+    stats = KernelStats()
+    c = multiply_rowmajor(a, b, StrategyKind.COMBINED, stats)
+    ref = oracle.multiply_rowmajor(a, b, row_choices=True)
+    assert_csr_bitwise_equal(c, CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx,
+                                          ref.values), f"seed{seed}/{values}")
+    assert stats.multiplications == ref.multiplications
+    assert np.array_equal(_choices_array(stats, rows), ref.row_choices)
+
+
+def test_wide_column_keys():
+    """Columns beyond 2^22 / 2^27 switch the sort keys to 64 bits."""
+    rng = np.random.default_rng(11)
+    for cols in (1 << 23, (1 << 28) + 5, 0xFFFF_FFF0):
+        a = _rand_csr(rng, 200, 300, 12)
+        b = _rand_csr(rng, 300, cols, 40)
+        c = multiply_rowmajor(a, b)
+        assert_csr_bitwise_equal(c, _oracle_csr(a, b), f"cols={cols}")
+
+
+def test_row_block_views_concatenate_to_full_product():
+    """Row blocks of A as zero-copy device views (row_ptr[0] != 0) multiply to
+    the matching row blocks of C (kernels.py:323-329: rows are independent)."""
+    import torch
+
+    from paper_1303_1651_b200 import device as dev
+    from paper_1303_1651_b200.distributed import concat_row_blocks, partition_rows
+
+    a, b = genmat.gen_zipf(20_000, 3), genmat.gen_zipf(20_000, 4)
+    full = _oracle_csr(a, b)
+    d = torch.device("cuda", 0)
+    ad, bd = dev.DeviceCsr.from_host(a, d), dev.DeviceCsr.from_host(b, d)
+    ctx = dev.context_for_current_stream(d)
+    bounds = partition_rows(row_products_prefix(a, b), 5)
+    blocks = []
+    for g in range(5):
+        with dev.multiply(ctx, ad.row_block(int(bounds[g]), int(bounds[g + 1])), bd) as p:
+            blocks.append(p.download())
+    assert_csr_bitwise_equal(concat_row_blocks(blocks, b.cols), full, "row blocks")
+    ctx.close()
+
+
+def test_device_api_and_timings():
+    import torch
+
+    from paper_1303_1651_b200 import device as dev
+
+    a = genmat.gen_fd(64)
+    d = torch.device("cuda", 0)
+    ad = dev.DeviceCsr.from_host(a, d)
+    ctx = _lib.Context(0)
+    with _lib.multiply_views(ctx, ad.view(), ad.view(), 6, _lib.FLAG_TIMING) as p:
+        rp, ci, v = p.download()
+        assert p.multiplications == 100104
+        t = ctx.last_timings()
+        assert "k_count" in t and "k_fused" in t and all(x > 0 for x in t.values())
+        assert ctx.last_launch_count() >= 2
+        out = dev.product_tensors(p, d)
+        assert np.array_equal(out.col_idx.cpu().numpy().view(np.uint64), ci)
+    assert_csr_bitwise_equal(CsrMatrix(a.rows, a.cols, rp, ci, v), _oracle_csr(a, a), "fd64")
+    ctx.close()
+
+
+def test_repeated_calls_reuse_context_state():
+    """Status-word epochs and pooled buffers across many calls and shapes."""
+    cases = [golden_case(n) for n in ("fd_16", "long_rows", "random_5", "medium_rows",
+                                      "zero_rows", "signed_k40")]
+    for rep in range(3):
+        for a, b, c_ref, _, _ in cases:
+            assert_csr_bitwise_equal(multiply_rowmajor(a, b), c_ref, f"rep{rep}")
+
+
+def _config_ops(label):
+    if label.startswith("C1"):
+        a = genmat.gen_fd(100)
+        return a, a
+    if label.startswith("C2"):
+        a = genmat.gen_fd(int(label[len("C2_fd"):]))
+        return a, a
+    if label.startswith("C3"):
+        return genmat.gen_random_k(2_000_000, 5, 0), genmat.gen_random_k(2_000_000, 5, 1)
+    if label.startswith("C4"):
+        a = genmat.gen_fd3(100)
+        return a, a
+    return genmat.gen_zipf(2_000_000, 0), genmat.gen_zipf(2_000_000, 1)
+
+
+FULL = ["C1_fd100", "C2_fd32", "C2_fd64", "C2_fd128", "C2_fd256", "C2_fd512", "C2_fd1024",
+        "C2_fd2048", "C3_random2M", "C4_fd3_100", "C5_zipf2M"]
+
+
+@pytest.mark.parametrize("label", FULL)
+def test_full_size_config_matches_reference(label):
+    """Full BASELINE configs against the reference's own product digests."""
+    fp = fingerprints().get(label)
+    if fp is None:
+        pytest.skip(f"{label} missing from fingerprints.json")
+    a, b = _config_ops(label)
+    stats = KernelStats()
+    c = multiply_rowmajor(a, b, StrategyKind.COMBINED, stats)
+    assert stats.multiplications == fp["multiplications"]
+    d = genmat.digests(c)
+    if d["fingerprint"] != fp["c"]["fingerprint"]:
+        # localise the failure against the (reference-pinned) oracle
+        assert_csr_bitwise_equal(c, _oracle_csr(a, b), label)
+    assert d["row_ptr_sha256"] == fp["c"]["row_ptr_sha256"]
+    assert d["col_idx_sha256"] == fp["c"]["col_idx_sha256"]
+    assert d["values_sha256"] == fp["c"]["values_sha256"]
