@@ -322,4 +322,26 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
   }
 }
 
+// Long rows: staged by k_long, placed at their final offsets after k_fused.
+__global__ void __launch_bounds__(256) k_copy_long(const uint32_t* __restrict__ list,
+                                                   const uint64_t* __restrict__ l_off,
+                                                   const uint32_t* __restrict__ l_nnz,
+                                                   const unsigned long long* __restrict__ n_long,
+                                                   const uint64_t* __restrict__ l_ci,
+                                                   const double* __restrict__ l_v,
+                                                   const uint64_t* __restrict__ c_rp,
+                                                   uint64_t* __restrict__ c_ci,
+                                                   double* __restrict__ c_v) {
+  const uint32_t n = uint32_t(*n_long);
+  for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
+    const uint64_t dst = c_rp[list[li]];
+    const uint64_t src = l_off[li];
+    const uint32_t cnt = l_nnz[li];
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+      c_ci[dst + t] = l_ci[src + t];
+      c_v[dst + t] = l_v[src + t];
+    }
+  }
+}
+
 }  // namespace spmmm

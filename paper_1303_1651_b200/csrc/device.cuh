@@ -1,6 +1,6 @@
 // Device-side building blocks for the sm_100a spMMM pipeline: warp scans, the
-// register bitonic sort, the decoupled look-back, and the per-row
-// accumulation paths (short / medium). Kernels live in kernels.cuh.
+// register bitonic sort and the decoupled look-back. The per-row paths are in
+// rows.cuh, the kernels in kernels.cuh / aux_kernels.cuh.
 //
 // Numerics: every product is fl(a*b) via __dmul_rn and every accumulation
 // step fl(acc + p) via __dadd_rn, so nvcc cannot contract them into DFMA.
@@ -109,8 +109,6 @@ __device__ __forceinline__ void bitonic_sort(K (&key)[N]) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j >= 32) {
-        constexpr int dummy = 0;
-        (void)dummy;
         const int je = j >> 5;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -140,6 +138,28 @@ __device__ __forceinline__ void bitonic_sort(K (&key)[N]) {
   }
 }
 
+// R independent one-key-per-lane bitonic sorts (32 keys each), interleaved so
+// the shuffle chains of different rows overlap.
+template <int R, typename K>
+__device__ __forceinline__ void bitonic32_multi(K (&key)[R]) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const bool up = (lane & uint32_t(k)) == 0;
+      const bool lower = (lane & uint32_t(j)) == 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const K p = shfl_xor_key(key[i], j);
+        const K mn = key[i] < p ? key[i] : p;
+        const K mx = key[i] < p ? p : key[i];
+        key[i] = (lower == up) ? mn : mx;
+      }
+    }
+  }
+}
+
 // Runtime-width dispatch of the bitonic sort (E a power of two <= N).
 template <int N, typename K>
 __device__ __forceinline__ void bitonic_sort_dyn(K (&key)[N], int E) {
@@ -152,274 +172,128 @@ __device__ __forceinline__ void bitonic_sort_dyn(K (&key)[N], int E) {
 }
 
 // ---------------------------------------------------------------------------
-// Decoupled look-back over tiles (single pass exclusive scan of tile nnz).
+// Two-level decoupled look-back (single-pass exclusive scan of tile nnz).
+//
 // Status word: [63:62] flag (0 invalid, 1 aggregate, 2 inclusive prefix),
-// [61:46] epoch (per call, so the array never needs clearing), [45:0] value.
+// [61:46] epoch (per call, so the arrays never need clearing), [45:0] value.
+// Level 1: one word per tile. Level 2: one word per group of 32 tiles,
+// holding the group's aggregate or its inclusive prefix. With thousands of
+// warp tiles in flight a flat look-back would walk a whole wave of tiles;
+// with groups it reads at most its own group's tiles plus a few group words.
+// A walker that meets a group word nobody has written yet builds it from
+// the group's 32 tile words (benign race: every writer stores a correct value).
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 46) - 1;
+constexpr int kGroupShift = 5;
 
-// Warp-collective (call with all 32 lanes). Publishes `agg` for `tile` and
-// returns the exclusive prefix of all earlier tiles.
-__device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t tile, uint64_t agg,
-                                             uint32_t epoch) {
+__device__ __forceinline__ uint32_t status_flag(uint64_t w, uint32_t epoch) {
+  return ((w >> 46) & 0xffffu) == (epoch & 0xffffu) ? uint32_t(w >> 62) : 0u;
+}
+
+__device__ __forceinline__ uint64_t status_word(uint64_t flag, uint32_t epoch, uint64_t v) {
+  return flag | (uint64_t(epoch & 0xffffu) << 46) | v;
+}
+
+// The 32 tile words of group g -> the group's word (its inclusive prefix if
+// some tile already has one, else its aggregate). Warp-collective; every
+// tile word must be published.
+__device__ __forceinline__ uint64_t group_word(const uint64_t* tstat, uint64_t g, uint32_t epoch) {
   const uint32_t lane = lane_id();
-  const uint64_t ep = uint64_t(epoch & 0xffffu) << 46;
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(&status[0], kFlagPrefix | ep | agg);
-    return 0;
+  const uint64_t tw = ld_relaxed(&tstat[(g << kGroupShift) + lane]);
+  const uint32_t tpm = __ballot_sync(kFull, status_flag(tw, epoch) == 2);
+  const uint32_t first = tpm ? 31u - __clz(tpm) : 0u;
+  const uint64_t v = warp_sum64(lane >= first ? (tw & kValMask) : 0ull);
+  return status_word(tpm ? kFlagPrefix : kFlagAgg, epoch, v);
+}
+
+// Publish a tile's aggregate (tile 0 publishes its prefix). The last tile of
+// a group to publish (per-group counter) also publishes the group's word, so
+// walkers never have to assemble it. Warp-collective.
+__device__ __forceinline__ void publish_aggregate(uint64_t* tstat, uint64_t* gstat,
+                                                  uint32_t* gcount, uint64_t tile, uint64_t agg,
+                                                  uint64_t ntiles, uint32_t epoch) {
+  const uint32_t lane = lane_id();
+  const uint64_t g = tile >> kGroupShift;
+  const bool full_group = ((g + 1) << kGroupShift) <= ntiles;
+  uint32_t old = 0;
+  if (lane == 0) {
+    st_relaxed(&tstat[tile], status_word(tile == 0 ? kFlagPrefix : kFlagAgg, epoch, agg));
+    if (full_group) {
+      __threadfence();  // release our word before counting it
+      old = atomicAdd(gcount + g, 1u);
+      __threadfence();  // acquire the other 31 words
+    }
   }
-  if (lane == 0) st_relaxed(&status[tile], kFlagAgg | ep | agg);
+  old = __shfl_sync(kFull, old, 0);
+  if (full_group && old == 31) {
+    const uint64_t gw = group_word(tstat, g, epoch);
+    if (lane == 0) st_relaxed(&gstat[g], gw);
+  }
+}
+
+// Warp-collective. The tile's aggregate must already be published. Returns
+// its exclusive prefix and publishes the inclusive one (and the group's, for
+// the last tile of a group).
+__device__ __forceinline__ uint64_t lookback(uint64_t* tstat, uint64_t* gstat, uint64_t tile,
+                                             uint64_t agg, uint32_t epoch) {
+  const uint32_t lane = lane_id();
+  const uint64_t g = tile >> kGroupShift;
+  const uint32_t q = uint32_t(tile & 31u);
   uint64_t excl = 0;
-  int64_t base = int64_t(tile) - 1;
-  while (true) {
-    const int64_t idx = base - int64_t(lane);
-    uint64_t w = 0;
-    uint32_t flag = 2;  // before tile 0: an implicit prefix of 0
-    uint32_t pmask, lim, inval;
+  bool done = tile == 0;
+  // ---- level 1: earlier tiles of the same group ----
+  if (!done && q > 0) {
+    const bool in = lane < q;
     int spins = 0;
     while (true) {
-      if (idx >= 0) {
-        w = ld_relaxed(&status[idx]);
-        flag = ((w >> 46) & 0xffffu) == (epoch & 0xffffu) ? uint32_t(w >> 62) : 0u;
+      uint64_t w = 0;
+      uint32_t flag = 0;
+      if (in) {
+        w = ld_relaxed(&tstat[(g << kGroupShift) + lane]);
+        flag = status_flag(w, epoch);
       }
-      pmask = __ballot_sync(kFull, flag == 2);
-      lim = pmask ? uint32_t(__ffs(pmask) - 1) : 31u;
+      const uint32_t pm = __ballot_sync(kFull, in && flag == 2);
+      const uint32_t first = pm ? 31u - __clz(pm) : 0u;  // nearest prefix
+      const uint32_t need = ((1u << q) - 1u) & ~((1u << first) - 1u);
+      if (__ballot_sync(kFull, in && flag == 0) & need) {
+        if (++spins > 2) __nanosleep(64);
+        continue;
+      }
+      excl = warp_sum64((in && lane >= first) ? (w & kValMask) : 0ull);
+      done = pm != 0;
+      break;
+    }
+  }
+  // ---- level 2: earlier groups ----
+  if (!done && g > 0) {
+    int64_t gb = int64_t(g) - 1;
+    int spins = 0;
+    while (true) {
+      const int64_t gi = gb - int64_t(lane);
+      uint64_t w = 0;
+      uint32_t flag = 2;  // before group 0: an implicit prefix of 0
+      if (gi >= 0) {
+        w = ld_relaxed(&gstat[gi]);
+        flag = status_flag(w, epoch);
+      }
+      const uint32_t pm = __ballot_sync(kFull, flag == 2);
+      const uint32_t lim = pm ? uint32_t(__ffs(pm) - 1) : 31u;
       const uint32_t window = lim == 31 ? kFull : ((2u << lim) - 1u);
-      inval = __ballot_sync(kFull, flag == 0) & window;
-      if (!inval) break;
-      if (++spins > 4) __nanosleep(64);
+      if (__ballot_sync(kFull, flag == 0) & window) {
+        if (++spins > 2) __nanosleep(64);
+        continue;
+      }
+      excl += warp_sum64((lane <= lim && gi >= 0) ? (w & kValMask) : 0ull);
+      if (pm) break;
+      gb -= 32;
     }
-    const uint64_t val = (lane <= lim && idx >= 0) ? (w & kValMask) : 0ull;
-    excl += warp_sum64(val);
-    if (pmask) break;
-    base -= 32;
   }
-  if (lane == 0) st_relaxed(&status[tile], kFlagPrefix | ep | (excl + agg));
+  if (lane == 0) {
+    if (tile != 0) st_relaxed(&tstat[tile], status_word(kFlagPrefix, epoch, excl + agg));
+    if (q == 31) st_relaxed(&gstat[g], status_word(kFlagPrefix, epoch, excl + agg));
+  }
   return excl;
-}
-
-// ---------------------------------------------------------------------------
-// Short rows: <= 32 products, <= 32 A entries. One product per lane,
-// expand -> bitonic sort by (column, product index) -> segmented left fold.
-//
-// Product q of the row is entry j of B row k where k runs over the A entries
-// in ascending column order; lane order therefore is the reference's k order
-// (kernels.py:167-171), and sorting by (col, lane) keeps each column's
-// products in that order for the fold.
-struct ShortOut {
-  uint32_t col;
-  uint32_t rank;
-  double val;
-  bool keep;
-};
-
-template <bool WIDE, bool STATS>
-__device__ __forceinline__ uint32_t short_row(const DevCsr& A, const DevCsr& B, uint64_t lo,
-                                              uint32_t na, ShortOut& out, uint32_t& smin,
-                                              uint32_t& smax, uint32_t& stouch) {
-  using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
-  const uint32_t lane = lane_id();
-  uint32_t len = 0;
-  uint64_t bs = 0;
-  double av = 0.0;
-  if (lane < na) {
-    const uint64_t k = ld_idx(A.ci + lo + lane);
-    av = ld_val(A.v + lo + lane);
-    bs = ld_idx(B.rp + k);
-    len = uint32_t(ld_idx(B.rp + k + 1) - bs);
-  }
-  const uint32_t incl = warp_incl_scan(len);
-  const uint32_t excl = incl - len;
-  const uint32_t tot = __shfl_sync(kFull, incl, 31);
-  // entry owning product `lane`: largest i with excl_i <= lane
-  int i = 0;
-#pragma unroll
-  for (int st = 16; st > 0; st >>= 1) {
-    const uint32_t ex = __shfl_sync(kFull, excl, i + st);
-    if (ex <= lane) i += st;
-  }
-  const uint64_t bsrc = __shfl_sync(kFull, bs, i);
-  const double a = __shfl_sync(kFull, av, i);
-  const uint32_t j = lane - __shfl_sync(kFull, excl, i);
-  const bool valid = lane < tot;
-  uint32_t col = 0;
-  double p = 0.0;
-  if (valid) {
-    col = uint32_t(ld_idx(B.ci + bsrc + j));
-    p = __dmul_rn(a, ld_val(B.v + bsrc + j));
-  }
-  K key[1];
-  key[0] = valid ? ((K(col) << 5) | K(lane)) : ~K(0);
-  bitonic_sort<1>(key);
-  col = uint32_t(key[0] >> 5);
-  const uint32_t src = uint32_t(key[0]) & 31u;
-  const double v = __shfl_sync(kFull, p, src);
-  const uint32_t prev = __shfl_up_sync(kFull, col, 1);
-  const bool head = valid && (lane == 0 || prev != col);
-  double acc = v;
-  uint32_t touches = 1;
-  for (int d = 1; d < 32; ++d) {
-    const uint32_t c = __shfl_down_sync(kFull, col, d);
-    const double t = __shfl_down_sync(kFull, v, d);
-    const bool cond = head && (lane + uint32_t(d) < tot) && c == col;
-    if (!__any_sync(kFull, cond)) break;
-    if (cond) {
-      if (STATS && acc == 0.0) ++touches;  // re-touch after a transient zero
-      acc = __dadd_rn(acc, t);
-    }
-  }
-  const bool keep = head && (acc != 0.0);  // kernels.py:296 drops exact zeros
-  const uint32_t km = __ballot_sync(kFull, keep);
-  out.col = col;
-  out.val = acc;
-  out.keep = keep;
-  out.rank = __popc(km & lanemask_lt());
-  if (STATS) {
-    smin = __shfl_sync(kFull, col, 0);
-    smax = __shfl_sync(kFull, col, (tot - 1) & 31u);
-    uint32_t t = head ? touches : 0u;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
-    stouch = t;
-  }
-  return __popc(km);
-}
-
-// ---------------------------------------------------------------------------
-// Medium rows: warp + open-addressing table of T slots in shared memory.
-// Products are streamed in chunks of up to 32 in (k, j) order. A chunk is cut
-// at B-row boundaries whenever possible, so most chunks hold one B row whose
-// columns are distinct: all lanes update the table in one step. Chunks that
-// span several B rows are applied in rounds where each column's products go
-// in ascending product order (rank among equal columns via match_any), which
-// keeps every table entry a left fold in reference order.
-
-template <int T>
-__device__ __forceinline__ uint32_t table_hash(uint32_t col) {
-  constexpr int kLog = __builtin_ctz(T);
-  return (col * 0x9E3779B1u) >> (32 - kLog);
-}
-
-template <int T, bool STATS>
-__device__ __forceinline__ void table_apply(uint32_t* keys, double* vals, uint32_t col,
-                                            double p, uint32_t& touches) {
-  volatile uint32_t* vk = keys;
-  uint32_t h = table_hash<T>(col);
-  bool fresh = false;
-  while (true) {
-    const uint32_t k = vk[h];
-    if (k == col) break;
-    if (k == kEmptyKey) {
-      const uint32_t old = atomicCAS(keys + h, kEmptyKey, col);
-      if (old == kEmptyKey) { fresh = true; break; }
-      if (old == col) break;
-    }
-    h = (h + 1) & (T - 1);
-  }
-  volatile double* vv = vals;
-  const double cur = fresh ? 0.0 : vv[h];  // fresh slot == dense[x] == 0.0
-  if (STATS && cur == 0.0) ++touches;
-  vv[h] = __dadd_rn(cur, p);
-}
-
-template <int T, bool STATS>
-__device__ __forceinline__ void medium_accumulate(const DevCsr& A, const DevCsr& B, uint64_t lo,
-                                                  uint64_t hi, uint32_t* keys, double* vals,
-                                                  uint32_t& touches) {
-  const uint32_t lane = lane_id();
-  for (uint64_t abase = lo; abase < hi; abase += 32) {
-    const uint64_t e = abase + lane;
-    uint32_t len = 0;
-    uint64_t bs = 0;
-    double av = 0.0;
-    if (e < hi) {
-      const uint64_t k = ld_idx(A.ci + e);
-      av = ld_val(A.v + e);
-      bs = ld_idx(B.rp + k);
-      len = uint32_t(ld_idx(B.rp + k + 1) - bs);
-    }
-    const uint32_t incl = warp_incl_scan(len);
-    const uint32_t excl = incl - len;
-    const uint32_t gtot = __shfl_sync(kFull, incl, 31);
-    uint32_t cs = 0;
-    while (cs < gtot) {
-      const uint32_t lim = cs + 32;
-      const uint32_t bm = __ballot_sync(kFull, incl > cs && incl <= lim);
-      const uint32_t ce =
-          bm ? __shfl_sync(kFull, incl, 31 - __clz(bm)) : (lim < gtot ? lim : gtot);
-      const uint32_t q = cs + lane;
-      const bool act = q < ce;
-      int i = 0;
-#pragma unroll
-      for (int st = 16; st > 0; st >>= 1) {
-        const uint32_t ex = __shfl_sync(kFull, excl, i + st);
-        if (ex <= q) i += st;
-      }
-      const uint64_t bsrc = __shfl_sync(kFull, bs, i);
-      const double a = __shfl_sync(kFull, av, i);
-      const uint32_t j = q - __shfl_sync(kFull, excl, i);
-      uint32_t col = kEmptyKey;
-      double p = 0.0;
-      if (act) {
-        col = uint32_t(ld_idx(B.ci + bsrc + j));
-        p = __dmul_rn(a, ld_val(B.v + bsrc + j));
-      }
-      const int i_first = __shfl_sync(kFull, i, 0);
-      const int i_last = __shfl_sync(kFull, i, (ce - cs - 1) & 31u);
-      if (i_first == i_last) {
-        if (act) table_apply<T, STATS>(keys, vals, col, p, touches);
-        __syncwarp();
-      } else {
-        const uint32_t am = __ballot_sync(kFull, act);
-        const uint32_t peers = __match_any_sync(kFull, col) & am;
-        const uint32_t rank = __popc(peers & lanemask_lt());
-        const uint32_t rounds = __reduce_max_sync(kFull, act ? rank : 0u) + 1u;
-        for (uint32_t rr = 0; rr < rounds; ++rr) {
-          if (act && rank == rr) table_apply<T, STATS>(keys, vals, col, p, touches);
-          __syncwarp();
-        }
-      }
-      cs = ce;
-    }
-  }
-}
-
-// After accumulation: compact the occupied nonzero slots to the front of the
-// table (in place) and return their count. STATS: min/max over every occupied
-// slot, zero-valued ones included (they were touched: kernels.py:175-178).
-template <int T, bool STATS>
-__device__ __forceinline__ uint32_t medium_compact(uint32_t* keys, double* vals, uint32_t& smin,
-                                                   uint32_t& smax) {
-  const uint32_t lane = lane_id();
-  uint32_t cnt = 0;
-  uint32_t mn = kEmptyKey, mx = 0;
-#pragma unroll 4
-  for (uint32_t s0 = 0; s0 < uint32_t(T); s0 += 32) {
-    const uint32_t s = s0 + lane;
-    const uint32_t k = keys[s];
-    const double v = vals[s];
-    const bool occ = k != kEmptyKey;
-    const bool keep = occ && (v != 0.0);
-    if (STATS && occ) {
-      mn = k < mn ? k : mn;
-      mx = k > mx ? k : mx;
-    }
-    const uint32_t m = __ballot_sync(kFull, keep);
-    __syncwarp();
-    if (keep) {
-      const uint32_t pos = cnt + __popc(m & lanemask_lt());
-      keys[pos] = k;
-      vals[pos] = v;
-    }
-    cnt += __popc(m);
-    __syncwarp();
-  }
-  if (STATS) {
-    smin = __reduce_min_sync(kFull, mn);
-    smax = __reduce_max_sync(kFull, mx);
-  }
-  return cnt;
 }
 
 }  // namespace spmmm

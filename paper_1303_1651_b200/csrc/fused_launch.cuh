@@ -1,5 +1,6 @@
-// Launch entry points of the fused kernel, one translation unit per shared
-// table size (fused_t0.cu ... fused_t1024.cu) so they compile in parallel.
+// Launch entry points of the fused kernel. The short-only and the medium
+// variants live in separate translation units (fused_short.cu,
+// fused_medium.cu) so they compile in parallel.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -9,7 +10,7 @@
 namespace spmmm {
 
 constexpr int kFusedWarps = 8;
-constexpr int kFusedShortRowsPerWarp = 4;
+constexpr int kShortRowsPerTile = 4;  // rows per warp tile without medium rows
 
 struct FusedLaunchEnv {
   int device;
@@ -17,41 +18,57 @@ struct FusedLaunchEnv {
   cudaStream_t stream;
 };
 
-// Cooperative (all blocks co-resident) persistent launch: grid = min(tiles,
-// resident blocks per SM * SMs). The look-back requires co-residency.
-template <int WARPS, int R, int T, bool WIDE, bool STATS>
-cudaError_t launch_fused(const FusedParams& prm_in, const FusedLaunchEnv& env) {
-  auto kern = k_fused<WARPS, R, T, WIDE, STATS>;
-  const size_t smem = size_t(WARPS) * size_t(T) * (sizeof(double) + sizeof(uint32_t));
-  static int occ_cache[64] = {};
-  int& occ = occ_cache[env.device & 63];
-  if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorInvalidConfiguration;
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
+struct FusedVariant {
+  static constexpr size_t smem() {
+    return FusedSmem<R, MEDIUM>::bytes(WARPS);
   }
-  FusedParams prm = prm_in;
-  const unsigned long long max_grid = (unsigned long long)occ * (unsigned long long)env.sms;
-  const unsigned grid = unsigned(prm.ntiles < max_grid ? prm.ntiles : max_grid);
-  void* args[] = {&prm};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(WARPS * 32),
-                                     args, smem, env.stream);
-}
+  // resident blocks per SM (cached per device)
+  static cudaError_t occupancy(int device, int* occ) {
+    static int cache[64] = {};
+    int& c = cache[device & 63];
+    if (c == 0) {
+      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(smem()));
+      if (e != cudaSuccess) return e;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kern, WARPS * 32, smem());
+      if (e != cudaSuccess) return e;
+      if (c < 1) return cudaErrorInvalidConfiguration;
+    }
+    *occ = c;
+    return cudaSuccess;
+  }
+  // cooperative launch: the look-back needs every warp co-resident
+  static cudaError_t launch(const FusedParams& prm_in, const FusedLaunchEnv& env, unsigned grid) {
+    FusedParams prm = prm_in;
+    void* args[] = {&prm};
+    return cudaLaunchCooperativeKernel(
+        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS>), dim3(grid),
+        dim3(WARPS * 32), args, smem(), env.stream);
+  }
+};
 
-template <int WARPS, int R, int T>
-cudaError_t launch_fused_kw(const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
-                            bool stats) {
-  if (wide) return stats ? launch_fused<WARPS, R, T, true, true>(prm, env)
-                         : launch_fused<WARPS, R, T, true, false>(prm, env);
-  return stats ? launch_fused<WARPS, R, T, false, true>(prm, env)
-               : launch_fused<WARPS, R, T, false, false>(prm, env);
-}
+// op 0: occupancy query into *occ; op 1: launch with `grid`
+cudaError_t fused_short(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
+                        bool stats, unsigned grid, int* occ);
+cudaError_t fused_medium(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
+                         bool stats, unsigned grid, int* occ);
 
-cudaError_t launch_fused_t0(const FusedParams&, const FusedLaunchEnv&, bool wide, bool stats);
-cudaError_t launch_fused_t256(const FusedParams&, const FusedLaunchEnv&, bool wide, bool stats);
-cudaError_t launch_fused_t512(const FusedParams&, const FusedLaunchEnv&, bool wide, bool stats);
-cudaError_t launch_fused_t1024(const FusedParams&, const FusedLaunchEnv&, bool wide, bool stats);
+template <int WARPS, int R, bool MEDIUM>
+cudaError_t fused_dispatch(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
+                           bool stats, unsigned grid, int* occ) {
+#define SPMMM_FUSED_CASE(W, S)                                                  \
+  if (wide == W && stats == S) {                                                \
+    using V = FusedVariant<WARPS, R, MEDIUM, W, S>;                             \
+    return op == 0 ? V::occupancy(env.device, occ) : V::launch(prm, env, grid); \
+  }
+  SPMMM_FUSED_CASE(false, false)
+  SPMMM_FUSED_CASE(false, true)
+  SPMMM_FUSED_CASE(true, false)
+  SPMMM_FUSED_CASE(true, true)
+#undef SPMMM_FUSED_CASE
+  return cudaErrorInvalidValue;
+}
 
 }  // namespace spmmm

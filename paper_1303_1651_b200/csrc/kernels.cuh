@@ -1,170 +1,247 @@
-// sm_100a kernels of the spMMM pipeline (see DESIGN.md §3 for the dataflow).
-// k_count / k_collect / k_long are in aux_kernels.cuh:
-//   k_count    per-row product counts (estimate_nnz / count_mults per row),
-//              their total and maximum, structural validation of A and B.
-//   k_collect  lists the rows too long for the fused kernel (only when any).
-//   k_long     block-per-row product of those rows into a staging buffer.
-//   k_fused    one persistent pass over all rows: computes each row (short
-//              rows in registers, medium rows in a shared-memory table),
-//              obtains the row's output offset by a decoupled look-back scan
-//              over tiles, and writes C.row_ptr / C.col_idx / C.values once.
+// The fused, persistent, single-pass spMMM kernel (k_fused) and the copy of
+// pre-computed long rows (k_copy_long). k_count / k_collect / k_long are in
+// aux_kernels.cuh. Dataflow: DESIGN.md §3.
+//
+// k_fused: every warp walks its own sequence of warp tiles (R consecutive
+// rows; tile t belongs to global warp t mod #warps). For a tile it
+//   1. computes its rows — short rows in registers (rows.cuh short_rows),
+//      medium rows in the warp's shared-memory table (global table on
+//      overflow), long rows only contribute their pre-computed nnz;
+//   2. publishes the tile's nnz and reads its exclusive prefix with a
+//      warp-level decoupled look-back (device.cuh lookback) — there is no
+//      block barrier anywhere in the loop;
+//   3. writes C.row_ptr[r+1] and the rows' (col, value) entries once.
+// Launched cooperatively (all warps co-resident): the smallest unfinished
+// tile's warp is always running it and only waits on smaller tiles, so the
+// look-back cannot deadlock.
 #pragma once
 
-#include "device.cuh"
+#include "rows.cuh"
 
 namespace spmmm {
 
-// ---------------------------------------------------------------------------
-// K4: the fused, persistent, single-pass kernel. Must be launched
-// cooperatively (all blocks co-resident): tile t is processed by block
-// t mod gridDim.x and waits only on tiles < t (look-back), so the smallest
-// unfinished tile can always progress.
 struct FusedParams {
   DevCsr A, B;
   const uint32_t* prod;
   const uint32_t* lmap;
-  const uint64_t* l_off;
   const uint32_t* l_nnz;
-  const uint64_t* l_ci;
-  const double* l_v;
   uint64_t* c_rp;
   uint64_t* c_ci;
   double* c_v;
-  uint64_t* status;
+  uint64_t* tstat;   // one status word per tile
+  uint64_t* gstat;   // one status word per group of 32 tiles
+  uint32_t* gcount;  // tiles of each group that published (zeroed per call)
   uint64_t ntiles;
   uint32_t epoch;
   uint32_t medium_limit;
+  uint32_t* g_keys;  // [#warps][kGlobalSlots] overflow tables (medium kernel)
+  double* g_vals;
+  uint32_t* g_scol;  // [#warps][2][kMediumLimit] staging of overflowed rows
+  double* g_sval;
   uint32_t* st_min;
   uint32_t* st_max;
   uint32_t* st_touch;
 };
 
-// WARPS warps per block; each warp owns R consecutive rows of a tile
-// (R > 1 only without a table). T = shared-memory table slots per warp (0 =
-// short rows only). WIDE = 64-bit sort keys (columns too large to pack).
-template <int WARPS, int R, int T, bool WIDE, bool STATS>
-__global__ void __launch_bounds__(WARPS * 32) k_fused(const FusedParams p) {
-  static_assert(WARPS * R <= 32, "tile rows must fit one warp scan");
-  static_assert(T == 0 || R == 1, "medium rows keep their table until written");
-  constexpr int kRows = WARPS * R;
-  constexpr int EMAX = T > 0 ? T / 32 : 1;
-  constexpr int LOGT = T > 0 ? __builtin_ctz(T) : 5;
+// Shared memory per warp: two staging buffers of kStage entries (a tile's
+// finished rows wait there until its offset is known), the per-row nnz of
+// both, and for the medium kernel the warp's hash table.
+template <int R, bool MEDIUM>
+struct FusedSmem {
+  static constexpr int kStage = MEDIUM ? kSmemSlots * 3 / 4 : 32 * R;
+  static constexpr int kTable = MEDIUM ? kSmemSlots : 0;
+  static constexpr int kWords64 = 2 * kStage + kTable;          // doubles per warp
+  static constexpr int kWords32 = 2 * kStage + kTable + 2 * R;  // u32 per warp
+  static constexpr size_t bytes(int warps) {
+    return size_t(warps) * (kWords64 * sizeof(double) + kWords32 * sizeof(uint32_t));
+  }
+};
+
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
+__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const FusedParams p) {
+  static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
+  static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  using SM = FusedSmem<R, MEDIUM>;
+  constexpr int EMAX = MEDIUM ? int(kMediumLimit / 32) : 1;
+  constexpr int kStage = SM::kStage;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t s_nnz[kRows];
-  __shared__ uint64_t s_base[kRows];
-
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  uint32_t* keys = nullptr;
-  double* vals = nullptr;
-  if constexpr (T > 0) {
-    vals = reinterpret_cast<double*>(smem_raw) + size_t(warp) * T;
-    keys = reinterpret_cast<uint32_t*>(smem_raw + size_t(WARPS) * T * sizeof(double)) +
-           size_t(warp) * T;
-    for (uint32_t s = lane; s < uint32_t(T); s += 32) keys[s] = kEmptyKey;
-    __syncwarp();
+  const uint64_t gwarp = uint64_t(blockIdx.x) * WARPS + warp;
+  const uint64_t nwarps = uint64_t(gridDim.x) * WARPS;
+  double* s_val = reinterpret_cast<double*>(smem_raw) + size_t(warp) * SM::kWords64;
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem_raw + size_t(WARPS) * SM::kWords64 * 8) +
+                    size_t(warp) * SM::kWords32;
+  uint32_t* s_hdr = s_col + 2 * kStage + SM::kTable;
+  Table<kSmemSlots, false> st{s_col + 2 * kStage, s_val + 2 * kStage};
+  Table<kGlobalSlots, true> gt{nullptr, nullptr};
+  uint32_t* g_scol = nullptr;
+  double* g_sval = nullptr;
+  if constexpr (MEDIUM) {
+    gt.keys = p.g_keys + gwarp * kGlobalSlots;
+    gt.vals = p.g_vals + gwarp * kGlobalSlots;
+    g_scol = p.g_scol + gwarp * 2 * kMediumLimit;
+    g_sval = p.g_sval + gwarp * 2 * kMediumLimit;
+    st.clear();
   }
+  const uint64_t rows = p.A.rows;
 
-  for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const uint64_t r0 = tile * kRows + uint64_t(warp) * R;
-    ShortOut so[R];
+  // the tile waiting for its offset (finished one iteration later)
+  bool pend = false;
+  uint64_t pd_tile = 0, pd_agg = 0;
+  uint32_t pd_staged = 0;
+  bool pd_global = false;
+  int buf = 0;
+
+  auto finish = [&](uint64_t tile, uint64_t agg, uint32_t staged, bool global, int b) {
+    const uint64_t excl = lookback(p.tstat, p.gstat, tile, agg, p.epoch);
+    const uint64_t r0 = tile * R;
+    if (lane < uint32_t(R) && r0 + lane < rows) {
+      uint64_t s = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (uint32_t(j) <= lane) s += s_hdr[b * R + j];
+      p.c_rp[r0 + lane + 1] = excl + s;
+    }
+    if (global) {
+      for (uint32_t t = lane; t < staged; t += 32) {
+        p.c_ci[excl + t] = __ldcg(g_scol + b * kMediumLimit + t);
+        p.c_v[excl + t] = __ldcg(g_sval + b * kMediumLimit + t);
+      }
+    } else {
+      for (uint32_t t = lane; t < staged; t += 32) {
+        p.c_ci[excl + t] = s_col[b * kStage + t];
+        p.c_v[excl + t] = s_val[b * kStage + t];
+      }
+    }
+    __syncwarp();
+  };
+
+  for (uint64_t tile = gwarp; tile < p.ntiles; tile += nwarps) {
+    const uint64_t r0 = tile * R;
+    // ---- row bounds and classes of the tile ----
+    uint64_t rpv = 0;
+    uint32_t prv = 0;
+    if (lane <= uint32_t(R) && r0 + lane <= rows) rpv = ld_idx(p.A.rp + r0 + lane);
+    if (lane < uint32_t(R) && r0 + lane < rows) prv = p.prod[r0 + lane];
+    uint64_t lo[R];
+    uint32_t na[R], nnz[R], smin[R], smax[R], stouch[R];
     int cls[R];
-    uint32_t nnz[R];
-    K mk[EMAX];
-    int mE = 1;
-    uint64_t lidx = 0;
+    bool on[R];
+    bool any_short = false;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const uint64_t r = r0 + i;
-      cls[i] = kRowZero;
+      lo[i] = __shfl_sync(kFull, rpv, i);
+      const uint64_t hi = __shfl_sync(kFull, rpv, i + 1);
+      const uint32_t pr = __shfl_sync(kFull, prv, i);
+      cls[i] = (r0 + i < rows) ? classify(pr, hi - lo[i], p.medium_limit) : kRowZero;
+      na[i] = uint32_t(hi - lo[i]);
+      on[i] = cls[i] == kRowShort;
+      any_short |= on[i];
       nnz[i] = 0;
-      if (r < p.A.rows) {
-        const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
-        const uint32_t pr = p.prod[r];
-        cls[i] = classify(pr, hi - lo, p.medium_limit);
-        uint32_t smin = kEmptyKey, smax = 0, stouch = 0;
-        if (cls[i] == kRowShort) {
-          nnz[i] = short_row<WIDE, STATS>(p.A, p.B, lo, uint32_t(hi - lo), so[i], smin, smax,
-                                          stouch);
-        } else if (cls[i] == kRowMedium) {
-          if constexpr (T > 0) {
-            uint32_t touches = 0;
-            medium_accumulate<T, STATS>(p.A, p.B, lo, hi, keys, vals, touches);
-            __syncwarp();
-            const uint32_t cnt = medium_compact<T, STATS>(keys, vals, smin, smax);
-            nnz[i] = cnt;
-            int E = 1;
-            while (uint32_t(E) * 32u < cnt) E <<= 1;
-            mE = E;
+      smin[i] = kEmptyKey;
+      smax[i] = 0;
+      stouch[i] = 0;
+    }
+    uint32_t staged = 0;
+    bool global = false;
+    if (any_short) {
+      ShortOut so[R];
+      short_rows<R, WIDE, STATS>(p.A, p.B, lo, na, on, so, nnz, smin, smax, stouch);
 #pragma unroll
-            for (int e = 0; e < EMAX; ++e) {
-              const uint32_t idx = uint32_t(e) * 32u + lane;
-              mk[e] = (e < E && idx < cnt) ? ((K(keys[idx]) << LOGT) | K(idx)) : ~K(0);
-            }
-            bitonic_sort_dyn(mk, E);
-            if (STATS) {
+      for (int i = 0; i < R; ++i) {
+        if (!on[i]) nnz[i] = 0;
+        if (on[i] && so[i].keep) {
+          s_col[buf * kStage + staged + so[i].rank] = so[i].col;
+          s_val[buf * kStage + staged + so[i].rank] = so[i].val;
+        }
+        staged += nnz[i];
+      }
+    }
+
+    // ---- medium / long row (R == 1 in the medium kernel) ----
+    if constexpr (MEDIUM) {
+      if (cls[0] == kRowMedium) {
+        const uint64_t hi = lo[0] + na[0];
+        uint32_t touches = 0, cnt;
+        if (medium_accumulate<decltype(st), STATS>(p.A, p.B, lo[0], hi, st, kSmemSlots * 3 / 4,
+                                                    touches)) {
+          cnt = st.template compact<STATS>(smin[0], smax[0]);
+        } else {
+          st.clear();
+          touches = 0;
+          global = true;
+          medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo[0], hi, gt, kGlobalSlots, touches);
+          cnt = gt.template compact<STATS>(smin[0], smax[0]);
+        }
+        nnz[0] = cnt;
+        staged = cnt;
+        int E = 1;
+        while (uint32_t(E) * 32u < cnt) E <<= 1;
+        K mk[EMAX];
 #pragma unroll
-              for (int d = 16; d > 0; d >>= 1) touches += __shfl_xor_sync(kFull, touches, d);
-              stouch = touches;
+        for (int e = 0; e < EMAX; ++e) {
+          const uint32_t idx = uint32_t(e) * 32u + lane;
+          uint32_t kcol = kEmptyKey;
+          if (e < E && idx < cnt) kcol = global ? gt.ldk(idx) : st.ldk(idx);
+          mk[e] = (e < E && idx < cnt) ? ((K(kcol) << kPosBits) | K(idx)) : ~K(0);
+        }
+        bitonic_sort_dyn(mk, E);
+        // sorted (col, value) into this tile's staging buffer
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          const uint32_t idx = uint32_t(e) * 32u + lane;
+          if (e < E && idx < cnt) {
+            const uint32_t pos = uint32_t(mk[e]) & uint32_t(kGlobalSlots - 1);
+            const uint32_t col = uint32_t(mk[e] >> kPosBits);
+            if (global) {
+              __stcg(g_scol + buf * kMediumLimit + idx, col);
+              __stcg(g_sval + buf * kMediumLimit + idx, gt.ldv(pos));
+            } else {
+              s_col[buf * kStage + idx] = col;
+              s_val[buf * kStage + idx] = st.ldv(pos);
             }
           }
-        } else if (cls[i] == kRowLong) {
-          lidx = p.lmap[r];
-          nnz[i] = p.l_nnz[lidx];
         }
-        if (STATS && lane == 0 && cls[i] != kRowLong) {
-          p.st_min[r] = smin;
-          p.st_max[r] = smax;
-          p.st_touch[r] = stouch;
+        __syncwarp();
+        if (global) gt.clear();
+        else st.clear();
+        if (STATS) {
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) touches += __shfl_xor_sync(kFull, touches, d);
+          stouch[0] = touches;
         }
+      } else if (cls[0] == kRowLong) {
+        nnz[0] = p.l_nnz[p.lmap[r0]];  // copied into place by k_copy_long
       }
-      if (lane == 0) s_nnz[warp * R + i] = nnz[i];
     }
-    __syncthreads();
-    if (warp == 0) {
-      const uint64_t v = lane < uint32_t(kRows) ? uint64_t(s_nnz[lane]) : 0ull;
-      const uint64_t incl = warp_incl_scan64(v);
-      const uint64_t agg = __shfl_sync(kFull, incl, 31);
-      const uint64_t excl = lookback(p.status, tile, agg, p.epoch);
-      if (lane < uint32_t(kRows)) s_base[lane] = excl + incl - v;
-    }
-    __syncthreads();
+
+    // ---- per-row stats, tile header, aggregate ----
+    uint64_t agg = 0;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const uint64_t r = r0 + i;
-      if (r >= p.A.rows) break;
-      const uint64_t base = s_base[warp * R + i];
-      if (lane == 0) p.c_rp[r + 1] = base + nnz[i];
-      if (cls[i] == kRowShort) {
-        if (so[i].keep) {
-          p.c_ci[base + so[i].rank] = so[i].col;
-          p.c_v[base + so[i].rank] = so[i].val;
-        }
-      } else if (cls[i] == kRowMedium) {
-        if constexpr (T > 0) {
-#pragma unroll
-          for (int e = 0; e < EMAX; ++e) {
-            const uint32_t idx = uint32_t(e) * 32u + lane;
-            if (e < mE && idx < nnz[i]) {
-              const K key = mk[e];
-              p.c_ci[base + idx] = uint64_t(key >> LOGT);
-              p.c_v[base + idx] = vals[uint32_t(key) & uint32_t(T - 1)];
-            }
-          }
-          __syncwarp();
-          for (uint32_t s = lane; s < uint32_t(T); s += 32) keys[s] = kEmptyKey;
-          __syncwarp();
-        }
-      } else if (cls[i] == kRowLong) {
-        const uint64_t off = p.l_off[lidx];
-        for (uint32_t t = lane; t < nnz[i]; t += 32) {
-          p.c_ci[base + t] = p.l_ci[off + t];
-          p.c_v[base + t] = p.l_v[off + t];
-        }
+      agg += nnz[i];
+      if (lane == uint32_t(i)) s_hdr[buf * R + i] = nnz[i];
+      if (STATS && lane == 0 && r0 + i < rows && cls[i] != kRowLong) {
+        p.st_min[r0 + i] = smin[i];
+        p.st_max[r0 + i] = smax[i];
+        p.st_touch[r0 + i] = stouch[i];
       }
     }
+    __syncwarp();
+    publish_aggregate(p.tstat, p.gstat, p.gcount, tile, agg, p.ntiles, p.epoch);
+
+    // ---- finish the previous tile: its predecessors published long ago ----
+    if (pend) finish(pd_tile, pd_agg, pd_staged, pd_global, buf ^ 1);
+    pend = true;
+    pd_tile = tile;
+    pd_agg = agg;
+    pd_staged = staged;
+    pd_global = global;
+    buf ^= 1;
   }
+  if (pend) finish(pd_tile, pd_agg, pd_staged, pd_global, buf ^ 1);
 }
 
 }  // namespace spmmm

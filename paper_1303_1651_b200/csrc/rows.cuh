@@ -1,0 +1,368 @@
+// Per-row accumulation paths of the fused kernel.
+//
+// Order contract (the reason parity is bit-exact, kernels.py:163-180): for an
+// output column x the value is the left fold, from 0.0, of fl(a_rk * b_kx)
+// over the A-row entries k in ascending column order, each step one
+// separately rounded fp64 add. Product q of a row is entry j of B row k, with
+// q running through (k, j) in A-entry order — that is, q order *is* the
+// reference's k order, and every path below applies a column's products in
+// ascending q.
+#pragma once
+
+#include "device.cuh"
+
+namespace spmmm {
+
+// ---------------------------------------------------------------------------
+// Short rows (<= 32 products, <= 32 A entries): one product per lane,
+// expand -> bitonic sort by (column, q) -> segmented left fold. R rows of a
+// warp tile go through every phase together, so their four dependent load
+// levels (A.row_ptr, A entries, B.row_ptr, B entries) overlap.
+struct ShortOut {
+  uint32_t col;
+  uint32_t rank;
+  double val;
+  bool keep;
+};
+
+template <int R, bool WIDE, bool STATS>
+__device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
+                                           const uint64_t (&lo)[R], const uint32_t (&na)[R],
+                                           const bool (&on)[R], ShortOut (&out)[R],
+                                           uint32_t (&nnz)[R], uint32_t (&smin)[R],
+                                           uint32_t (&smax)[R], uint32_t (&stouch)[R]) {
+  using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  const uint32_t lane = lane_id();
+  uint64_t kk[R];
+  double av[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    kk[i] = 0;
+    av[i] = 0.0;
+    if (on[i] && lane < na[i]) {
+      kk[i] = ld_idx(A.ci + lo[i] + lane);
+      av[i] = ld_val(A.v + lo[i] + lane);
+    }
+  }
+  uint64_t bs[R];
+  uint32_t len[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    bs[i] = 0;
+    len[i] = 0;
+    if (on[i] && lane < na[i]) {
+      bs[i] = ld_idx(B.rp + kk[i]);
+      len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1) - bs[i]);
+    }
+  }
+  uint32_t incl[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) incl[i] = len[i];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint32_t t = __shfl_up_sync(kFull, incl[i], d);
+      if (lane >= uint32_t(d)) incl[i] += t;
+    }
+  }
+  uint32_t excl[R], tot[R];
+  int src[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    excl[i] = incl[i] - len[i];
+    tot[i] = __shfl_sync(kFull, incl[i], 31);
+    src[i] = 0;
+  }
+  // entry owning product q = lane: the largest i with excl_i <= lane
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint32_t ex = __shfl_sync(kFull, excl[i], src[i] + st);
+      if (ex <= lane) src[i] += st;
+    }
+  }
+  uint32_t col[R];
+  double p[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint64_t bsrc = __shfl_sync(kFull, bs[i], src[i]);
+    const double a = __shfl_sync(kFull, av[i], src[i]);
+    const uint32_t j = lane - __shfl_sync(kFull, excl[i], src[i]);
+    col[i] = 0;
+    p[i] = a;
+    if (lane < tot[i]) {
+      col[i] = uint32_t(ld_idx(B.ci + bsrc + j));
+      p[i] = ld_val(B.v + bsrc + j);  // multiplied below, after the loads are in flight
+    }
+  }
+  K key[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const bool valid = lane < tot[i];
+    const double a = __shfl_sync(kFull, av[i], src[i]);
+    p[i] = valid ? __dmul_rn(a, p[i]) : 0.0;
+    key[i] = valid ? ((K(col[i]) << 5) | K(lane)) : ~K(0);
+  }
+  bitonic32_multi<R>(key);
+  double v[R], acc[R];
+  bool head[R];
+  uint32_t touches[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    col[i] = uint32_t(key[i] >> 5);
+    v[i] = __shfl_sync(kFull, p[i], uint32_t(key[i]) & 31u);
+    const uint32_t prev = __shfl_up_sync(kFull, col[i], 1);
+    head[i] = lane < tot[i] && (lane == 0 || prev != col[i]);
+    acc[i] = v[i];
+    touches[i] = 1;
+  }
+  for (int d = 1; d < 32; ++d) {
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint32_t c = __shfl_down_sync(kFull, col[i], d);
+      const double t = __shfl_down_sync(kFull, v[i], d);
+      const bool cond = head[i] && (lane + uint32_t(d) < tot[i]) && c == col[i];
+      if (cond) {
+        if (STATS && acc[i] == 0.0) ++touches[i];  // re-touch after a transient zero
+        acc[i] = __dadd_rn(acc[i], t);
+      }
+      any |= cond;
+    }
+    if (!__any_sync(kFull, any)) break;
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const bool keep = head[i] && (acc[i] != 0.0);  // kernels.py:296 drops exact zeros
+    const uint32_t km = __ballot_sync(kFull, keep);
+    out[i].col = col[i];
+    out[i].val = acc[i];
+    out[i].keep = keep;
+    out[i].rank = __popc(km & lanemask_lt());
+    nnz[i] = __popc(km);
+    if (STATS && on[i]) {
+      smin[i] = __shfl_sync(kFull, col[i], 0);
+      smax[i] = __shfl_sync(kFull, col[i], (tot[i] - 1) & 31u);
+      uint32_t t = head[i] ? touches[i] : 0u;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
+      stouch[i] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Medium rows: a warp and an open-addressing table (column -> running sum).
+// The table lives in shared memory (kSmemSlots per warp); a row whose distinct
+// columns pass 3/4 of that restarts on the warp's slice of a global table
+// (kGlobalSlots, sized for the medium product limit), so correctness never
+// depends on guessing the row's output size.
+
+constexpr int kSmemSlots = 256;
+constexpr int kGlobalSlots = 2048;
+constexpr int kPosBits = 11;  // log2(kGlobalSlots): packed sort key = col << 11 | position
+constexpr uint32_t kMediumLimit = 1024;  // products; longer rows go to k_long
+
+template <int T, bool GLOBAL>
+struct Table {
+  uint32_t* keys;
+  double* vals;
+  static constexpr int kSlots = T;
+  __device__ __forceinline__ uint32_t ldk(uint32_t h) const {
+    if constexpr (GLOBAL) return __ldcg(keys + h);
+    else return static_cast<volatile uint32_t*>(keys)[h];
+  }
+  __device__ __forceinline__ double ldv(uint32_t h) const {
+    if constexpr (GLOBAL) return __ldcg(vals + h);
+    else return static_cast<volatile double*>(vals)[h];
+  }
+  __device__ __forceinline__ void stv(uint32_t h, double v) const {
+    if constexpr (GLOBAL) __stcg(vals + h, v);
+    else static_cast<volatile double*>(vals)[h] = v;
+  }
+  __device__ __forceinline__ void stk(uint32_t h, uint32_t k) const {
+    if constexpr (GLOBAL) __stcg(keys + h, k);
+    else static_cast<volatile uint32_t*>(keys)[h] = k;
+  }
+  __device__ __forceinline__ static uint32_t hash(uint32_t col) {
+    constexpr int kLog = __builtin_ctz(T);
+    return (col * 0x9E3779B1u) >> (32 - kLog);
+  }
+  // dense[col] += p with the reference's touch accounting; returns true if
+  // the column was new. Columns applied in one call are distinct across lanes.
+  template <bool STATS>
+  __device__ __forceinline__ bool apply(uint32_t col, double p, uint32_t& touches) const {
+    uint32_t h = hash(col);
+    bool fresh = false;
+    while (true) {
+      const uint32_t k = ldk(h);
+      if (k == col) break;
+      if (k == kEmptyKey) {
+        const uint32_t old = atomicCAS(keys + h, kEmptyKey, col);
+        if (old == kEmptyKey) { fresh = true; break; }
+        if (old == col) break;
+      }
+      h = (h + 1) & (T - 1);
+    }
+    const double cur = fresh ? 0.0 : ldv(h);  // fresh slot == dense[x] == 0.0
+    if (STATS && cur == 0.0) ++touches;
+    stv(h, __dadd_rn(cur, p));
+    return fresh;
+  }
+  __device__ __forceinline__ void clear() const {
+    const uint32_t lane = lane_id();
+    for (uint32_t s = lane; s < uint32_t(T); s += 32) stk(s, kEmptyKey);
+    __syncwarp();
+  }
+  // Compact the occupied nonzero slots to the front (in place); returns the
+  // count. STATS: min/max over every occupied slot, zero-valued ones included.
+  template <bool STATS>
+  __device__ __forceinline__ uint32_t compact(uint32_t& smin, uint32_t& smax) const {
+    const uint32_t lane = lane_id();
+    uint32_t cnt = 0, mn = kEmptyKey, mx = 0;
+    for (uint32_t s0 = 0; s0 < uint32_t(T); s0 += 32) {
+      const uint32_t s = s0 + lane;
+      const uint32_t k = ldk(s);
+      const double v = ldv(s);
+      const bool occ = k != kEmptyKey;
+      const bool keep = occ && (v != 0.0);
+      if (STATS && occ) {
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+      }
+      const uint32_t m = __ballot_sync(kFull, keep);
+      __syncwarp();
+      if (keep) {
+        const uint32_t pos = cnt + __popc(m & lanemask_lt());
+        stk(pos, k);
+        stv(pos, v);
+      }
+      cnt += __popc(m);
+      __syncwarp();
+    }
+    if (STATS) {
+      smin = __reduce_min_sync(kFull, mn);
+      smax = __reduce_max_sync(kFull, mx);
+    }
+    return cnt;
+  }
+};
+
+// One chunk of up to 32 consecutive products of a group of <= 32 A entries,
+// cut at B-row boundaries when possible. The B loads are issued when the
+// chunk is made and consumed when it is applied (register prefetch).
+struct Chunk {
+  uint32_t cs, ce;
+  bool single;  // all products come from one B row: columns distinct
+  uint64_t col;
+  double bv;
+  double a;
+};
+
+__device__ __forceinline__ Chunk make_chunk(const DevCsr& B, uint32_t cs, uint32_t gtot,
+                                            uint32_t incl, uint32_t excl, uint64_t bs,
+                                            double av) {
+  Chunk c;
+  c.cs = cs;
+  c.col = kEmptyKey;
+  c.bv = 0.0;
+  c.a = 0.0;
+  c.single = true;
+  if (cs >= gtot) {
+    c.ce = cs;
+    return c;
+  }
+  const uint32_t lane = lane_id();
+  const uint32_t lim = cs + 32;
+  const uint32_t bm = __ballot_sync(kFull, incl > cs && incl <= lim);
+  c.ce = bm ? __shfl_sync(kFull, incl, 31 - __clz(bm)) : (lim < gtot ? lim : gtot);
+  const uint32_t q = cs + lane;
+  int i = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+    const uint32_t ex = __shfl_sync(kFull, excl, i + st);
+    if (ex <= q) i += st;
+  }
+  const uint64_t bsrc = __shfl_sync(kFull, bs, i);
+  c.a = __shfl_sync(kFull, av, i);
+  const uint32_t j = q - __shfl_sync(kFull, excl, i);
+  c.single = __shfl_sync(kFull, i, 0) == __shfl_sync(kFull, i, (c.ce - cs - 1) & 31u);
+  if (q < c.ce) {
+    c.col = ld_idx(B.ci + bsrc + j);
+    c.bv = ld_val(B.v + bsrc + j);
+  }
+  return c;
+}
+
+// Apply one chunk; returns the number of new columns it inserted.
+template <class Tab, bool STATS>
+__device__ __forceinline__ uint32_t apply_chunk(const Tab& tab, const Chunk& c,
+                                                uint32_t& touches) {
+  const uint32_t lane = lane_id();
+  const bool act = c.cs + lane < c.ce;
+  const uint32_t col = uint32_t(c.col);
+  const double p = __dmul_rn(c.a, c.bv);
+  bool fresh = false;
+  if (c.single) {
+    if (act) fresh = tab.template apply<STATS>(col, p, touches);
+    __syncwarp();
+  } else {
+    // equal columns from different B rows: apply in rounds, lowest q first
+    const uint32_t am = __ballot_sync(kFull, act);
+    const uint32_t peers = __match_any_sync(kFull, act ? col : kEmptyKey) & am;
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    const uint32_t rounds = __reduce_max_sync(kFull, act ? rank : 0u) + 1u;
+    for (uint32_t rr = 0; rr < rounds; ++rr) {
+      if (act && rank == rr) fresh |= tab.template apply<STATS>(col, p, touches);
+      __syncwarp();
+    }
+  }
+  return __popc(__ballot_sync(kFull, fresh));
+}
+
+// Accumulate the whole row into `tab`. Returns false (and leaves the table
+// dirty) if the row's distinct columns exceed `limit`.
+template <class Tab, bool STATS>
+__device__ __forceinline__ bool medium_accumulate(const DevCsr& A, const DevCsr& B, uint64_t lo,
+                                                  uint64_t hi, const Tab& tab, uint32_t limit,
+                                                  uint32_t& touches) {
+  const uint32_t lane = lane_id();
+  uint32_t inserted = 0;
+  for (uint64_t abase = lo; abase < hi; abase += 32) {
+    const uint64_t e = abase + lane;
+    uint32_t len = 0;
+    uint64_t bs = 0;
+    double av = 0.0;
+    if (e < hi) {
+      const uint64_t k = ld_idx(A.ci + e);
+      av = ld_val(A.v + e);
+      bs = ld_idx(B.rp + k);
+      len = uint32_t(ld_idx(B.rp + k + 1) - bs);
+    }
+    const uint32_t incl = warp_incl_scan(len);
+    const uint32_t excl = incl - len;
+    const uint32_t gtot = __shfl_sync(kFull, incl, 31);
+    // three chunks in flight
+    Chunk c0 = make_chunk(B, 0, gtot, incl, excl, bs, av);
+    Chunk c1 = make_chunk(B, c0.ce, gtot, incl, excl, bs, av);
+    Chunk c2 = make_chunk(B, c1.ce, gtot, incl, excl, bs, av);
+    while (c0.cs < gtot) {
+      inserted += apply_chunk<Tab, STATS>(tab, c0, touches);
+      if (inserted > limit) return false;
+      c0 = make_chunk(B, c2.ce, gtot, incl, excl, bs, av);
+      if (c1.cs >= gtot) break;
+      inserted += apply_chunk<Tab, STATS>(tab, c1, touches);
+      if (inserted > limit) return false;
+      c1 = make_chunk(B, c0.ce, gtot, incl, excl, bs, av);
+      if (c2.cs >= gtot) break;
+      inserted += apply_chunk<Tab, STATS>(tab, c2, touches);
+      if (inserted > limit) return false;
+      c2 = make_chunk(B, c1.ce, gtot, incl, excl, bs, av);
+    }
+  }
+  return true;
+}
+
+}  // namespace spmmm

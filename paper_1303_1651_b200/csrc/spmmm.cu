@@ -78,8 +78,8 @@ void release(DevBuf& b, cudaStream_t s) {
   b.cap = 0;
 }
 
-const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused"};
-constexpr int kNumKernels = 4;
+const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long"};
+constexpr int kNumKernels = 5;
 
 }  // namespace
 
@@ -89,7 +89,8 @@ struct spmmm_context {
   bool own_stream = false;
   int sms = 148;
   std::mutex mu;
-  DevBuf ctrl, prod, lmap, list, status, l_off, l_nnz, ws;
+  DevBuf ctrl, prod, lmap, list, status, l_off, l_nnz, ws, gtab;
+  uint64_t gtab_warps = 0;
   DevBuf a_rp, a_ci, a_v, b_rp, b_ci, b_v;
   unsigned long long* h_ctrl = nullptr;  // pinned mirror of ctrl
   uint32_t epoch = 0;
@@ -207,26 +208,17 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm) {
   return SPMMM_OK;
 }
 
-// ---- fused-kernel launch: instantiations live in fused_t*.cu (parallel build) ----
+// ---- fused-kernel launch: instantiations live in fused_short.cu / fused_medium.cu ----
 
-constexpr int kWarps = kFusedWarps;
-constexpr int kShortRowsPerWarp = kFusedShortRowsPerWarp;
-
-int rows_per_tile(int table) { return table == 0 ? kWarps * kShortRowsPerWarp : kWarps; }
-
-int dispatch_fused(spmmm_context* c, FusedParams& prm, int table, bool wide, bool stats) {
+int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bool wide,
+               bool stats, unsigned grid, int* occ) {
   FusedLaunchEnv env{c->device, c->sms, c->stream};
-  cudaError_t e;
-  switch (table) {
-    case 0: e = launch_fused_t0(prm, env, wide, stats); break;
-    case 256: e = launch_fused_t256(prm, env, wide, stats); break;
-    case 512: e = launch_fused_t512(prm, env, wide, stats); break;
-    case 1024: e = launch_fused_t1024(prm, env, wide, stats); break;
-    default: return fail(SPMMM_ERR_INVALID, "no fused kernel for table size %d", table);
-  }
+  cudaError_t e = medium ? fused_medium(op, prm, env, wide, stats, grid, occ)
+                         : fused_short(op, prm, env, wide, stats, grid, occ);
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
-                "k_fused<table=%d> launch: %s", table, cudaGetErrorString(e));
+                "k_fused<%s> %s: %s", medium ? "medium" : "short", op ? "launch" : "occupancy",
+                cudaGetErrorString(e));
   return SPMMM_OK;
 }
 
@@ -343,13 +335,13 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   const uint64_t max_prod = c->h_ctrl[kCtrlMaxProd];
   const bool need_table = c->h_ctrl[kCtrlNeedTable] != 0;
 
-  // Table size for medium rows: big enough that a row's distinct columns
-  // (<= its products) stay under 3/4 load; rows beyond 768 products go long.
-  int table = 0;
-  if (need_table) table = max_prod <= 192 ? 256 : (max_prod <= 384 ? 512 : 1024);
-  const uint32_t medium_limit = uint32_t(table * 3 / 4);
-  const int logt = table ? __builtin_ctz(table) : 5;
-  const bool wide = B.cols > (1ull << (32 - logt));
+  // Medium kernel (per-warp tables) only when some row needs it; rows past
+  // kMediumLimit products are computed by k_long before the fused pass.
+  const bool medium = need_table;
+  const uint32_t medium_limit = medium ? kMediumLimit : 0u;
+  const int pos_bits = medium ? kPosBits : 5;
+  const bool wide = B.cols > (1ull << (32 - pos_bits));
+  const int rows_per_tile = medium ? 1 : kShortRowsPerTile;
 
   auto* p = new (std::nothrow) spmmm_product;
   if (!p) return fail(SPMMM_ERR_OOM, "host allocation failed");
@@ -383,47 +375,101 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
 
   DevBuf stage_ci, stage_v;
-  const bool has_long = table > 0 && max_prod > medium_limit;
+  auto fail_staged = [&](int code) {
+    release(stage_ci, c->stream);
+    release(stage_v, c->stream);
+    return cleanup(code);
+  };
+  const bool has_long = medium && max_prod > medium_limit;
   if (rows && has_long) {
     rc = run_long(c, A, B, max_prod, medium_limit, total, stats, p, stage_ci, stage_v, tm);
-    if (rc) { release(stage_ci, c->stream); release(stage_v, c->stream); return cleanup(rc); }
+    if (rc) return fail_staged(rc);
   }
 
   if (rows) {
-    const uint64_t ntiles = (rows + rows_per_tile(table) - 1) / rows_per_tile(table);
+    const uint64_t ntiles = (rows + rows_per_tile - 1) / rows_per_tile;
+    const uint64_t ngroups = (ntiles + 31) / 32;
     bool grown = false;
-    e = ensure(c->status, ntiles * sizeof(uint64_t), c->stream, &grown);
-    if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_OOM, "status: %s", cudaGetErrorString(e)));
+    e = ensure(c->status, (ntiles + ngroups) * sizeof(uint64_t) + ngroups * sizeof(uint32_t),
+               c->stream, &grown);
+    if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "status: %s", cudaGetErrorString(e)));
     if (grown || c->epoch >= 0xffffu) {
       e = cudaMemsetAsync(c->status.p, 0, c->status.cap, c->stream);
-      if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
       c->epoch = 0;
     }
     c->epoch += 1;
+    uint32_t* gcount = reinterpret_cast<uint32_t*>(static_cast<uint64_t*>(c->status.p) + ntiles +
+                                                   ngroups);
+    e = cudaMemsetAsync(gcount, 0, ngroups * sizeof(uint32_t), c->stream);
+    if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
     FusedParams fp;
     fp.A = A;
     fp.B = B;
     fp.prod = static_cast<const uint32_t*>(c->prod.p);
     fp.lmap = static_cast<const uint32_t*>(c->lmap.p);
-    fp.l_off = static_cast<const uint64_t*>(c->l_off.p);
     fp.l_nnz = static_cast<const uint32_t*>(c->l_nnz.p);
-    fp.l_ci = static_cast<const uint64_t*>(stage_ci.p);
-    fp.l_v = static_cast<const double*>(stage_v.p);
     fp.c_rp = p->rp;
     fp.c_ci = p->ci;
     fp.c_v = p->v;
-    fp.status = static_cast<uint64_t*>(c->status.p);
+    fp.tstat = static_cast<uint64_t*>(c->status.p);
+    fp.gstat = static_cast<uint64_t*>(c->status.p) + ntiles;
+    fp.gcount = gcount;
     fp.ntiles = ntiles;
     fp.epoch = c->epoch;
     fp.medium_limit = medium_limit;
+    fp.g_keys = nullptr;
+    fp.g_vals = nullptr;
+    fp.g_scol = nullptr;
+    fp.g_sval = nullptr;
     fp.st_min = p->st;
     fp.st_max = p->st ? p->st + rows : nullptr;
     fp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+    int occ = 0;
+    rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ);
+    if (rc) return fail_staged(rc);
+    const unsigned grid = unsigned(std::min<uint64_t>(
+        (ntiles + kFusedWarps - 1) / kFusedWarps, uint64_t(occ) * uint64_t(c->sms)));
+    if (medium) {
+      // per warp: an overflow table (all keys empty; each warp restores its
+      // own) and two staging buffers for overflowed rows
+      const uint64_t warps = uint64_t(grid) * kFusedWarps;
+      const size_t per_warp = kGlobalSlots * (sizeof(uint32_t) + sizeof(double)) +
+                              2 * kMediumLimit * (sizeof(uint32_t) + sizeof(double));
+      bool g_grown = false;
+      e = ensure(c->gtab, warps * per_warp, c->stream, &g_grown);
+      if (e == cudaSuccess && (g_grown || c->gtab_warps < warps)) {
+        e = cudaMemsetAsync(c->gtab.p, 0xff, c->gtab.cap, c->stream);
+        c->gtab_warps = c->gtab.cap / per_warp;
+      }
+      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "overflow tables: %s",
+                                                    cudaGetErrorString(e)));
+      char* g = static_cast<char*>(c->gtab.p);
+      const uint64_t n = c->gtab_warps;
+      fp.g_vals = reinterpret_cast<double*>(g);
+      fp.g_sval = reinterpret_cast<double*>(g + n * kGlobalSlots * 8);
+      fp.g_keys = reinterpret_cast<uint32_t*>(g + n * (kGlobalSlots + 2 * kMediumLimit) * 8);
+      fp.g_scol = fp.g_keys + n * kGlobalSlots;
+    }
     tm.begin(3);
-    rc = dispatch_fused(c, fp, table, wide, stats);
-    if (rc) { release(stage_ci, c->stream); release(stage_v, c->stream); return cleanup(rc); }
+    rc = fused_call(c, medium, 1, fp, wide, stats, grid, nullptr);
+    if (rc) return fail_staged(rc);
     tm.end(3);
     ++c->last_launches;
+    if (has_long) {
+      tm.begin(4);
+      k_copy_long<<<c->sms * 4, 256, 0, c->stream>>>(
+          static_cast<const uint32_t*>(c->list.p), static_cast<const uint64_t*>(c->l_off.p),
+          static_cast<const uint32_t*>(c->l_nnz.p),
+          static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlLongRows,
+          static_cast<const uint64_t*>(stage_ci.p), static_cast<const double*>(stage_v.p),
+          p->rp, p->ci, p->v);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "k_copy_long: %s",
+                                                    cudaGetErrorString(e)));
+      tm.end(4);
+      ++c->last_launches;
+    }
   }
   release(stage_ci, c->stream);
   release(stage_v, c->stream);
@@ -515,7 +561,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
+                    &c->ws, &c->gtab, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
     release(*b, c->stream);
   cudaStreamSynchronize(c->stream);
   for (int k = 0; k < 2 * kNumKernels; ++k)
