@@ -220,9 +220,10 @@ __device__ __forceinline__ void publish_aggregate(uint64_t* tstat, uint64_t* gst
   if (lane == 0) {
     st_relaxed(&tstat[tile], status_word(tile == 0 ? kFlagPrefix : kFlagAgg, epoch, agg));
     if (full_group) {
-      __threadfence();  // release our word before counting it
-      old = atomicAdd(gcount + g, 1u);
-      __threadfence();  // acquire the other 31 words
+      // acq_rel: our word is released before it is counted, and the 31 words
+      // counted before us are visible if we are the last
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(old) : "l"(gcount + g) : "memory");
     }
   }
   old = __shfl_sync(kFull, old, 0);
@@ -257,7 +258,7 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* tstat, uint64_t* gstat, u
       const uint32_t first = pm ? 31u - __clz(pm) : 0u;  // nearest prefix
       const uint32_t need = ((1u << q) - 1u) & ~((1u << first) - 1u);
       if (__ballot_sync(kFull, in && flag == 0) & need) {
-        if (++spins > 2) __nanosleep(64);
+        __nanosleep(32u << (spins < 5 ? spins++ : 5));
         continue;
       }
       excl = warp_sum64((in && lane >= first) ? (w & kValMask) : 0ull);
@@ -281,7 +282,7 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* tstat, uint64_t* gstat, u
       const uint32_t lim = pm ? uint32_t(__ffs(pm) - 1) : 31u;
       const uint32_t window = lim == 31 ? kFull : ((2u << lim) - 1u);
       if (__ballot_sync(kFull, flag == 0) & window) {
-        if (++spins > 2) __nanosleep(64);
+        __nanosleep(32u << (spins < 5 ? spins++ : 5));
         continue;
       }
       excl += warp_sum64((lane <= lim && gi >= 0) ? (w & kValMask) : 0ull);

@@ -43,15 +43,23 @@ struct FusedParams {
   uint32_t* st_touch;
 };
 
-// Shared memory per warp: two staging buffers of kStage entries (a tile's
+// Tiles are finished kDefer iterations after they are computed, so a warp
+// rarely waits on a predecessor that is still being computed. Short tiles are
+// quick (depth 2); a medium tile is one long row (depth 1).
+constexpr int kMaxBufs = 3;  // staging buffers of the deepest variant
+
+// Shared memory per warp: kBufs staging buffers of kStage entries (a tile's
 // finished rows wait there until its offset is known), the per-row nnz of
-// both, and for the medium kernel the warp's hash table.
+// each, and for the medium kernel the warp's hash table. Medium rows with more
+// than kStage outputs stage in the warp's global buffers instead.
 template <int R, bool MEDIUM>
 struct FusedSmem {
-  static constexpr int kStage = MEDIUM ? kSmemSlots * 3 / 4 : 32 * R;
+  static constexpr int kDefer = MEDIUM ? 1 : 2;
+  static constexpr int kBufs = kDefer + 1;
+  static constexpr int kStage = MEDIUM ? 128 : 32 * R;
   static constexpr int kTable = MEDIUM ? kSmemSlots : 0;
-  static constexpr int kWords64 = 2 * kStage + kTable;          // doubles per warp
-  static constexpr int kWords32 = 2 * kStage + kTable + 2 * R;  // u32 per warp
+  static constexpr int kWords64 = kBufs * kStage + kTable;              // doubles per warp
+  static constexpr int kWords32 = kBufs * kStage + kTable + kBufs * R;  // u32 per warp
   static constexpr size_t bytes(int warps) {
     return size_t(warps) * (kWords64 * sizeof(double) + kWords32 * sizeof(uint32_t));
   }
@@ -65,6 +73,8 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
   using SM = FusedSmem<R, MEDIUM>;
   constexpr int EMAX = MEDIUM ? int(kMediumLimit / 32) : 1;
   constexpr int kStage = SM::kStage;
+  constexpr int kBufs = SM::kBufs;
+  constexpr int kDefer = SM::kDefer;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -73,25 +83,30 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
   double* s_val = reinterpret_cast<double*>(smem_raw) + size_t(warp) * SM::kWords64;
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem_raw + size_t(WARPS) * SM::kWords64 * 8) +
                     size_t(warp) * SM::kWords32;
-  uint32_t* s_hdr = s_col + 2 * kStage + SM::kTable;
-  Table<kSmemSlots, false> st{s_col + 2 * kStage, s_val + 2 * kStage};
+  uint32_t* s_hdr = s_col + kBufs * kStage + SM::kTable;
+  Table<kSmemSlots, false> st{s_col + kBufs * kStage, s_val + kBufs * kStage};
   Table<kGlobalSlots, true> gt{nullptr, nullptr};
   uint32_t* g_scol = nullptr;
   double* g_sval = nullptr;
   if constexpr (MEDIUM) {
     gt.keys = p.g_keys + gwarp * kGlobalSlots;
     gt.vals = p.g_vals + gwarp * kGlobalSlots;
-    g_scol = p.g_scol + gwarp * 2 * kMediumLimit;
-    g_sval = p.g_sval + gwarp * 2 * kMediumLimit;
+    g_scol = p.g_scol + gwarp * kMaxBufs * kMediumLimit;
+    g_sval = p.g_sval + gwarp * kMaxBufs * kMediumLimit;
     st.clear();
   }
   const uint64_t rows = p.A.rows;
 
-  // the tile waiting for its offset (finished one iteration later)
-  bool pend = false;
-  uint64_t pd_tile = 0, pd_agg = 0;
-  uint32_t pd_staged = 0;
-  bool pd_global = false;
+  // tiles waiting for their offsets: p0 (oldest) and p1, finished kDefer
+  // iterations after they were computed
+  struct Pending {
+    uint64_t tile, agg;
+    uint32_t staged;
+    int buf;
+    bool global;
+  };
+  Pending p0{}, p1{};
+  int npend = 0;
   int buf = 0;
 
   auto finish = [&](uint64_t tile, uint64_t agg, uint32_t staged, bool global, int b) {
@@ -165,18 +180,20 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
       if (cls[0] == kRowMedium) {
         const uint64_t hi = lo[0] + na[0];
         uint32_t touches = 0, cnt;
+        bool use_gt = false;  // row overflowed the shared table
         if (medium_accumulate<decltype(st), STATS>(p.A, p.B, lo[0], hi, st, kSmemSlots * 3 / 4,
                                                     touches)) {
           cnt = st.template compact<STATS>(smin[0], smax[0]);
         } else {
           st.clear();
           touches = 0;
-          global = true;
+          use_gt = true;
           medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo[0], hi, gt, kGlobalSlots, touches);
           cnt = gt.template compact<STATS>(smin[0], smax[0]);
         }
         nnz[0] = cnt;
         staged = cnt;
+        global = cnt > uint32_t(kStage);  // too big for the shared stage
         int E = 1;
         while (uint32_t(E) * 32u < cnt) E <<= 1;
         K mk[EMAX];
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
         for (int e = 0; e < EMAX; ++e) {
           const uint32_t idx = uint32_t(e) * 32u + lane;
           uint32_t kcol = kEmptyKey;
-          if (e < E && idx < cnt) kcol = global ? gt.ldk(idx) : st.ldk(idx);
+          if (e < E && idx < cnt) kcol = use_gt ? gt.ldk(idx) : st.ldk(idx);
           mk[e] = (e < E && idx < cnt) ? ((K(kcol) << kPosBits) | K(idx)) : ~K(0);
         }
         bitonic_sort_dyn(mk, E);
@@ -195,17 +212,18 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
           if (e < E && idx < cnt) {
             const uint32_t pos = uint32_t(mk[e]) & uint32_t(kGlobalSlots - 1);
             const uint32_t col = uint32_t(mk[e] >> kPosBits);
+            const double val = use_gt ? gt.ldv(pos) : st.ldv(pos);
             if (global) {
               __stcg(g_scol + buf * kMediumLimit + idx, col);
-              __stcg(g_sval + buf * kMediumLimit + idx, gt.ldv(pos));
+              __stcg(g_sval + buf * kMediumLimit + idx, val);
             } else {
               s_col[buf * kStage + idx] = col;
-              s_val[buf * kStage + idx] = st.ldv(pos);
+              s_val[buf * kStage + idx] = val;
             }
           }
         }
         __syncwarp();
-        if (global) gt.clear();
+        if (use_gt) gt.clear();
         else st.clear();
         if (STATS) {
 #pragma unroll
@@ -232,16 +250,27 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
     __syncwarp();
     publish_aggregate(p.tstat, p.gstat, p.gcount, tile, agg, p.ntiles, p.epoch);
 
-    // ---- finish the previous tile: its predecessors published long ago ----
-    if (pend) finish(pd_tile, pd_agg, pd_staged, pd_global, buf ^ 1);
-    pend = true;
-    pd_tile = tile;
-    pd_agg = agg;
-    pd_staged = staged;
-    pd_global = global;
-    buf ^= 1;
+    // ---- finish the tile computed kDefer iterations ago ----
+    const Pending cur{tile, agg, staged, buf, global};
+    if (npend == kDefer) {
+      finish(p0.tile, p0.agg, p0.staged, p0.global, p0.buf);
+      if (kDefer == 2) {
+        p0 = p1;
+        p1 = cur;
+      } else {
+        p0 = cur;
+      }
+    } else if (npend == 0) {
+      p0 = cur;
+      ++npend;
+    } else {
+      p1 = cur;
+      ++npend;
+    }
+    buf = buf == kBufs - 1 ? 0 : buf + 1;
   }
-  if (pend) finish(pd_tile, pd_agg, pd_staged, pd_global, buf ^ 1);
+  if (npend > 0) finish(p0.tile, p0.agg, p0.staged, p0.global, p0.buf);
+  if (npend > 1) finish(p1.tile, p1.agg, p1.staged, p1.global, p1.buf);
 }
 
 }  // namespace spmmm

@@ -435,7 +435,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       // own) and two staging buffers for overflowed rows
       const uint64_t warps = uint64_t(grid) * kFusedWarps;
       const size_t per_warp = kGlobalSlots * (sizeof(uint32_t) + sizeof(double)) +
-                              2 * kMediumLimit * (sizeof(uint32_t) + sizeof(double));
+                              kMaxBufs * kMediumLimit * (sizeof(uint32_t) + sizeof(double));
       bool g_grown = false;
       e = ensure(c->gtab, warps * per_warp, c->stream, &g_grown);
       if (e == cudaSuccess && (g_grown || c->gtab_warps < warps)) {
@@ -448,7 +448,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       const uint64_t n = c->gtab_warps;
       fp.g_vals = reinterpret_cast<double*>(g);
       fp.g_sval = reinterpret_cast<double*>(g + n * kGlobalSlots * 8);
-      fp.g_keys = reinterpret_cast<uint32_t*>(g + n * (kGlobalSlots + 2 * kMediumLimit) * 8);
+      fp.g_keys = reinterpret_cast<uint32_t*>(g + n * (kGlobalSlots + kMaxBufs * kMediumLimit) * 8);
       fp.g_scol = fp.g_keys + n * kGlobalSlots;
     }
     tm.begin(3);
