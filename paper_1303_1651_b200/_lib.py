@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspmmm.so")
+LIB_PATH = os.environ.get("SPMMM_LIB_PATH", os.path.join(HERE, "libspmmm.so"))
 CSRC = os.path.join(HERE, "csrc")
 
 # status codes (include/spmmm.h)

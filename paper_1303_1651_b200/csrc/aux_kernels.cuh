@@ -13,6 +13,8 @@ enum Ctrl : int {
   kCtrlError = 3,     // bit flags: 1 A.row_ptr, 2 A.col_idx range, 4 B.row_ptr, 8 row too long
   kCtrlLongRows = 4,  // number of rows listed by k_collect
   kCtrlStageCursor = 5,
+  kCtrlTicket = 6,    // k_fused's dynamic tile counter
+  kCtrlFault = 7,     // k_fused watchdog report
   kCtrlWords = 8
 };
 

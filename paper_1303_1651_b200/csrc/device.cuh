@@ -96,6 +96,15 @@ __device__ __forceinline__ K shfl_xor_key(K k, int m) {
   return __shfl_xor_sync(kFull, k, m);
 }
 
+// compare-exchange half: keep the smaller or the larger key (VIMNMX + predicate)
+__device__ __forceinline__ uint32_t keep_minmax(uint32_t a, uint32_t b, bool take_min) {
+  return take_min ? umin(a, b) : umax(a, b);
+}
+__device__ __forceinline__ unsigned long long keep_minmax(unsigned long long a,
+                                                          unsigned long long b, bool take_min) {
+  return take_min ? ullmin(a, b) : ullmax(a, b);
+}
+
 // Bitonic sort of E*32 keys held E per lane (element index e*32 + lane),
 // ascending. Distances >= 32 are in-register exchanges, shorter ones are
 // lane shuffles. N >= E is the register array capacity.
@@ -116,10 +125,8 @@ __device__ __forceinline__ void bitonic_sort(K (&key)[N]) {
             const int e2 = e | je;
             const bool up = ((e << 5) & k) == 0;
             const K a = key[e], b = key[e2];
-            const K lo = a < b ? a : b;
-            const K hi = a < b ? b : a;
-            key[e] = up ? lo : hi;
-            key[e2] = up ? hi : lo;
+            key[e] = keep_minmax(a, b, up);
+            key[e2] = keep_minmax(a, b, !up);
           }
         }
       } else {
@@ -129,9 +136,7 @@ __device__ __forceinline__ void bitonic_sort(K (&key)[N]) {
           const uint32_t i = uint32_t(e) * 32u + lane;
           const bool up = (i & uint32_t(k)) == 0;
           const bool lower = (lane & uint32_t(j)) == 0;
-          const K mn = key[e] < p ? key[e] : p;
-          const K mx = key[e] < p ? p : key[e];
-          key[e] = (lower == up) ? mn : mx;
+          key[e] = keep_minmax(key[e], p, lower == up);
         }
       }
     }
@@ -150,12 +155,7 @@ __device__ __forceinline__ void bitonic32_multi(K (&key)[R]) {
       const bool up = (lane & uint32_t(k)) == 0;
       const bool lower = (lane & uint32_t(j)) == 0;
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const K p = shfl_xor_key(key[i], j);
-        const K mn = key[i] < p ? key[i] : p;
-        const K mx = key[i] < p ? p : key[i];
-        key[i] = (lower == up) ? mn : mx;
-      }
+      for (int i = 0; i < R; ++i) key[i] = keep_minmax(key[i], shfl_xor_key(key[i], j), lower == up);
     }
   }
 }
@@ -172,20 +172,40 @@ __device__ __forceinline__ void bitonic_sort_dyn(K (&key)[N], int E) {
 }
 
 // ---------------------------------------------------------------------------
-// Two-level decoupled look-back (single-pass exclusive scan of tile nnz).
+// Hierarchical decoupled look-back (single-pass exclusive scan of tile nnz).
 //
 // Status word: [63:62] flag (0 invalid, 1 aggregate, 2 inclusive prefix),
 // [61:46] epoch (per call, so the arrays never need clearing), [45:0] value.
-// Level 1: one word per tile. Level 2: one word per group of 32 tiles,
-// holding the group's aggregate or its inclusive prefix. With thousands of
-// warp tiles in flight a flat look-back would walk a whole wave of tiles;
-// with groups it reads at most its own group's tiles plus a few group words.
-// A walker that meets a group word nobody has written yet builds it from
-// the group's 32 tile words (benign race: every writer stores a correct value).
+// Level 0 has one word per tile, level l one word per 32^l tiles (the item's
+// aggregate, or its inclusive prefix). Thousands of tiles are in flight, so
+// the nearest published prefix is usually a whole "wave" of tiles back; with
+// three levels a look-back reads at most one chunk of 32 siblings per level.
+// An item word is written by the last of its 32 children to publish (per-item
+// acq_rel counter) and upgraded to a prefix by the last tile it covers.
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 46) - 1;
-constexpr int kGroupShift = 5;
+constexpr int kLevels = 3;
+
+struct LookbackState {
+  uint64_t* stat[kLevels];   // status words per level
+  unsigned long long* count[kLevels];  // [1..] per item: children << 46 | their sum (zeroed per call)
+  uint64_t n[kLevels];       // items per level
+  uint32_t epoch;
+  unsigned long long* fault;  // watchdog report (ctrl word), 0 = none
+};
+
+// Watchdog: a wait that outlives ~2^20 back-off rounds (about a second) is a
+// bug, not a slow predecessor. Record where it happened and stop waiting so
+// the host reports an error instead of hanging the process.
+constexpr int kSpinLimit = 1 << 20;
+__device__ __forceinline__ bool watchdog(const LookbackState& lb, int spins, uint32_t site,
+                                         uint64_t tile) {
+  if (spins < kSpinLimit) return false;
+  if (lane_id() == 0)
+    atomicCAS(lb.fault, 0ull, (1ull << 63) | (uint64_t(site) << 48) | (tile & ((1ull << 48) - 1)));
+  return true;
+}
 
 __device__ __forceinline__ uint32_t status_flag(uint64_t w, uint32_t epoch) {
   return ((w >> 46) & 0xffffu) == (epoch & 0xffffu) ? uint32_t(w >> 62) : 0u;
@@ -195,104 +215,107 @@ __device__ __forceinline__ uint64_t status_word(uint64_t flag, uint32_t epoch, u
   return flag | (uint64_t(epoch & 0xffffu) << 46) | v;
 }
 
-// The 32 tile words of group g -> the group's word (its inclusive prefix if
-// some tile already has one, else its aggregate). Warp-collective; every
-// tile word must be published.
-__device__ __forceinline__ uint64_t group_word(const uint64_t* tstat, uint64_t g, uint32_t epoch) {
-  const uint32_t lane = lane_id();
-  const uint64_t tw = ld_relaxed(&tstat[(g << kGroupShift) + lane]);
-  const uint32_t tpm = __ballot_sync(kFull, status_flag(tw, epoch) == 2);
-  const uint32_t first = tpm ? 31u - __clz(tpm) : 0u;
-  const uint64_t v = warp_sum64(lane >= first ? (tw & kValMask) : 0ull);
-  return status_word(tpm ? kFlagPrefix : kFlagAgg, epoch, v);
+__device__ __forceinline__ void backoff(int& spins) {
+  __nanosleep(spins < 5 ? (32u << spins) : 1024u);
+  ++spins;
 }
 
-// Publish a tile's aggregate (tile 0 publishes its prefix). The last tile of
-// a group to publish (per-group counter) also publishes the group's word, so
-// walkers never have to assemble it. Warp-collective.
-__device__ __forceinline__ void publish_aggregate(uint64_t* tstat, uint64_t* gstat,
-                                                  uint32_t* gcount, uint64_t tile, uint64_t agg,
-                                                  uint64_t ntiles, uint32_t epoch) {
-  const uint32_t lane = lane_id();
-  const uint64_t g = tile >> kGroupShift;
-  const bool full_group = ((g + 1) << kGroupShift) <= ntiles;
-  uint32_t old = 0;
-  if (lane == 0) {
-    st_relaxed(&tstat[tile], status_word(tile == 0 ? kFlagPrefix : kFlagAgg, epoch, agg));
-    if (full_group) {
-      // acq_rel: our word is released before it is counted, and the 31 words
-      // counted before us are visible if we are the last
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                   : "=r"(old) : "l"(gcount + g) : "memory");
-    }
-  }
-  old = __shfl_sync(kFull, old, 0);
-  if (full_group && old == 31) {
-    const uint64_t gw = group_word(tstat, g, epoch);
-    if (lane == 0) st_relaxed(&gstat[g], gw);
+// Publishing a tile: store its word, then add (1 << 46 | aggregate) to the
+// enclosing level-1 item's counter. The counter carries the data itself, so
+// the child whose add completes the item (count reaches 32) gets the item's
+// sum from the atomic's return value and publishes the item word — no fences,
+// no re-reading of the children. Higher levels cascade the same way.
+constexpr unsigned long long kCountOne = 1ull << 46;
+
+__device__ __forceinline__ void publish_aggregate(const LookbackState& lb, uint64_t tile,
+                                                  uint64_t agg) {
+  if (lane_id() != 0) return;
+  st_relaxed(&lb.stat[0][tile], status_word(tile == 0 ? kFlagPrefix : kFlagAgg, lb.epoch, agg));
+  uint64_t sum = agg;
+#pragma unroll
+  for (int l = 1; l < kLevels; ++l) {
+    const uint64_t item = tile >> (5 * l);
+    if (((item + 1) << (5 * l)) > lb.n[0]) return;  // incomplete item: never looked up
+    const unsigned long long old = atomicAdd(lb.count[l] + item, kCountOne | sum);
+    if ((old >> 46) != 31) return;
+    sum += old & kValMask;  // the whole item
+    st_relaxed(&lb.stat[l][item], status_word(kFlagAgg, lb.epoch, sum));
   }
 }
 
-// Warp-collective. The tile's aggregate must already be published. Returns
-// its exclusive prefix and publishes the inclusive one (and the group's, for
-// the last tile of a group).
-__device__ __forceinline__ uint64_t lookback(uint64_t* tstat, uint64_t* gstat, uint64_t tile,
-                                             uint64_t agg, uint32_t epoch) {
+// Warp-collective. The tile's aggregate must be published. Returns the
+// exclusive prefix; publishes the inclusive prefix of the tile and of every
+// item the tile closes.
+__device__ __forceinline__ uint64_t lookback(const LookbackState& lb, uint64_t tile,
+                                             uint64_t agg) {
   const uint32_t lane = lane_id();
-  const uint64_t g = tile >> kGroupShift;
-  const uint32_t q = uint32_t(tile & 31u);
+  const uint32_t epoch = lb.epoch;
   uint64_t excl = 0;
   bool done = tile == 0;
-  // ---- level 1: earlier tiles of the same group ----
-  if (!done && q > 0) {
-    const bool in = lane < q;
-    int spins = 0;
-    while (true) {
-      uint64_t w = 0;
-      uint32_t flag = 0;
-      if (in) {
-        w = ld_relaxed(&tstat[(g << kGroupShift) + lane]);
-        flag = status_flag(w, epoch);
+#pragma unroll
+  for (int l = 0; l < kLevels && !done; ++l) {
+    const uint64_t idx = tile >> (5 * l);
+    const uint64_t* st = lb.stat[l];
+    if (l < kLevels - 1) {
+      // earlier siblings inside the enclosing level-(l+1) item
+      const uint32_t q = uint32_t(idx & 31u);
+      if (q == 0) continue;
+      const uint64_t base = idx - q;
+      const bool in = lane < q;
+      int spins = 0;
+      while (true) {
+        uint64_t w = 0;
+        uint32_t f = 0;
+        if (in) {
+          w = ld_relaxed(&st[base + lane]);
+          f = status_flag(w, epoch);
+        }
+        const uint32_t pm = __ballot_sync(kFull, in && f == 2);
+        const uint32_t first = pm ? 31u - __clz(pm) : 0u;  // nearest prefix
+        const uint32_t need = ((1u << q) - 1u) & ~((1u << first) - 1u);
+        if ((__ballot_sync(kFull, in && f == 0) & need) && !watchdog(lb, spins, 2 + l, tile)) {
+          backoff(spins);
+          continue;
+        }
+        excl += warp_sum64((in && lane >= first) ? (w & kValMask) : 0ull);
+        done = pm != 0;
+        break;
       }
-      const uint32_t pm = __ballot_sync(kFull, in && flag == 2);
-      const uint32_t first = pm ? 31u - __clz(pm) : 0u;  // nearest prefix
-      const uint32_t need = ((1u << q) - 1u) & ~((1u << first) - 1u);
-      if (__ballot_sync(kFull, in && flag == 0) & need) {
-        __nanosleep(32u << (spins < 5 ? spins++ : 5));
-        continue;
+    } else {
+      // top level: walk back until a prefix (or the start)
+      int64_t gb = int64_t(idx) - 1;
+      int spins = 0;
+      while (gb >= 0) {
+        const int64_t gi = gb - int64_t(lane);
+        uint64_t w = 0;
+        uint32_t f = 2;  // before item 0: an implicit prefix of 0
+        if (gi >= 0) {
+          w = ld_relaxed(&st[gi]);
+          f = status_flag(w, epoch);
+        }
+        const uint32_t pm = __ballot_sync(kFull, f == 2);
+        const uint32_t lim = pm ? uint32_t(__ffs(pm) - 1) : 31u;
+        const uint32_t window = lim == 31 ? kFull : ((2u << lim) - 1u);
+        if ((__ballot_sync(kFull, f == 0) & window) && !watchdog(lb, spins, 8, tile)) {
+          backoff(spins);
+          continue;
+        }
+        excl += warp_sum64((lane <= lim && gi >= 0) ? (w & kValMask) : 0ull);
+        if (pm) break;
+        gb -= 32;
       }
-      excl = warp_sum64((in && lane >= first) ? (w & kValMask) : 0ull);
-      done = pm != 0;
-      break;
-    }
-  }
-  // ---- level 2: earlier groups ----
-  if (!done && g > 0) {
-    int64_t gb = int64_t(g) - 1;
-    int spins = 0;
-    while (true) {
-      const int64_t gi = gb - int64_t(lane);
-      uint64_t w = 0;
-      uint32_t flag = 2;  // before group 0: an implicit prefix of 0
-      if (gi >= 0) {
-        w = ld_relaxed(&gstat[gi]);
-        flag = status_flag(w, epoch);
-      }
-      const uint32_t pm = __ballot_sync(kFull, flag == 2);
-      const uint32_t lim = pm ? uint32_t(__ffs(pm) - 1) : 31u;
-      const uint32_t window = lim == 31 ? kFull : ((2u << lim) - 1u);
-      if (__ballot_sync(kFull, flag == 0) & window) {
-        __nanosleep(32u << (spins < 5 ? spins++ : 5));
-        continue;
-      }
-      excl += warp_sum64((lane <= lim && gi >= 0) ? (w & kValMask) : 0ull);
-      if (pm) break;
-      gb -= 32;
+      done = true;
     }
   }
   if (lane == 0) {
-    if (tile != 0) st_relaxed(&tstat[tile], status_word(kFlagPrefix, epoch, excl + agg));
-    if (q == 31) st_relaxed(&gstat[g], status_word(kFlagPrefix, epoch, excl + agg));
+    const uint64_t incl = excl + agg;
+    if (tile != 0) st_relaxed(&lb.stat[0][tile], status_word(kFlagPrefix, epoch, incl));
+#pragma unroll
+    for (int l = 1; l < kLevels; ++l) {
+      const uint64_t span = 1ull << (5 * l);
+      if (((tile + 1) & (span - 1)) == 0)
+        st_relaxed(&lb.stat[l][tile >> (5 * l)], status_word(kFlagPrefix, epoch, incl));
+    }
   }
   return excl;
 }

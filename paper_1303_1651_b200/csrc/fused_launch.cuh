@@ -10,7 +10,10 @@
 namespace spmmm {
 
 constexpr int kFusedWarps = 8;
-constexpr int kShortRowsPerTile = 4;  // rows per warp tile without medium rows
+#ifndef SPMMM_SHORT_ROWS
+#define SPMMM_SHORT_ROWS 8
+#endif
+constexpr int kShortRowsPerTile = SPMMM_SHORT_ROWS;  // rows per warp tile without medium rows
 
 struct FusedLaunchEnv {
   int device;

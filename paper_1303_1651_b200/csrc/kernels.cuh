@@ -28,11 +28,9 @@ struct FusedParams {
   uint64_t* c_rp;
   uint64_t* c_ci;
   double* c_v;
-  uint64_t* tstat;   // one status word per tile
-  uint64_t* gstat;   // one status word per group of 32 tiles
-  uint32_t* gcount;  // tiles of each group that published (zeroed per call)
+  LookbackState lb;  // hierarchical status words (device.cuh)
+  unsigned long long* ticket;  // next free tile (zeroed per call)
   uint64_t ntiles;
-  uint32_t epoch;
   uint32_t medium_limit;
   uint32_t* g_keys;  // [#warps][kGlobalSlots] overflow tables (medium kernel)
   double* g_vals;
@@ -43,30 +41,35 @@ struct FusedParams {
   uint32_t* st_touch;
 };
 
-// Tiles are finished kDefer iterations after they are computed, so a warp
-// rarely waits on a predecessor that is still being computed. Short tiles are
-// quick (depth 2); a medium tile is one long row (depth 1).
-constexpr int kMaxBufs = 3;  // staging buffers of the deepest variant
+// Warps take tiles dynamically, a batch of kBatch consecutive tiles per
+// atomic, so faster SMs simply process more tiles. A warp computes its whole
+// batch, then finishes (look-back + write) its previous batch: a tile is
+// always computed right after it is acquired, so no chain of waits forms and
+// the previous batch's predecessors are already published.
 
-// Shared memory per warp: kBufs staging buffers of kStage entries (a tile's
-// finished rows wait there until its offset is known), the per-row nnz of
-// each, and for the medium kernel the warp's hash table. Medium rows with more
-// than kStage outputs stage in the warp's global buffers instead.
+constexpr int kMaxBufs = 4;  // staging buffers of the largest variant
+
+// Shared memory per warp: kBufs = 2 batches x kBatch tiles of staging
+// (a tile's finished rows wait there until its offset is known), the per-row
+// nnz of each, and for the medium kernel the warp's hash table. Medium rows
+// with more than kStage outputs stage in the warp's global buffers instead.
 template <int R, bool MEDIUM>
 struct FusedSmem {
-  static constexpr int kDefer = MEDIUM ? 1 : 2;
-  static constexpr int kBufs = kDefer + 1;
+  static constexpr int kBatch = MEDIUM ? 2 : 1;  // tiles per ticket
+  static constexpr int kBufs = 2 * kBatch;
   static constexpr int kStage = MEDIUM ? 128 : 32 * R;
   static constexpr int kTable = MEDIUM ? kSmemSlots : 0;
-  static constexpr int kWords64 = kBufs * kStage + kTable;              // doubles per warp
-  static constexpr int kWords32 = kBufs * kStage + kTable + kBufs * R;  // u32 per warp
+  // doubles per warp: staging values, table values, per buffer (tile, agg)
+  static constexpr int kWords64 = kBufs * kStage + kTable + 2 * kBufs;
+  // u32 per warp: staging columns, table keys, per buffer R row nnz + (staged, global)
+  static constexpr int kWords32 = kBufs * kStage + kTable + kBufs * R + 2 * kBufs;
   static constexpr size_t bytes(int warps) {
     return size_t(warps) * (kWords64 * sizeof(double) + kWords32 * sizeof(uint32_t));
   }
 };
 
 template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const FusedParams p) {
+__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : (R <= 2 ? 6 : 4)) k_fused(const FusedParams p) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
@@ -74,16 +77,17 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
   constexpr int EMAX = MEDIUM ? int(kMediumLimit / 32) : 1;
   constexpr int kStage = SM::kStage;
   constexpr int kBufs = SM::kBufs;
-  constexpr int kDefer = SM::kDefer;
+  constexpr int kBatch = SM::kBatch;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint64_t gwarp = uint64_t(blockIdx.x) * WARPS + warp;
-  const uint64_t nwarps = uint64_t(gridDim.x) * WARPS;
   double* s_val = reinterpret_cast<double*>(smem_raw) + size_t(warp) * SM::kWords64;
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem_raw + size_t(WARPS) * SM::kWords64 * 8) +
                     size_t(warp) * SM::kWords32;
   uint32_t* s_hdr = s_col + kBufs * kStage + SM::kTable;
+  uint32_t* s_meta32 = s_hdr + kBufs * R;                                  // [buf][staged, global]
+  uint64_t* s_meta64 = reinterpret_cast<uint64_t*>(s_val + kBufs * kStage + SM::kTable);  // [buf][tile, agg]
   Table<kSmemSlots, false> st{s_col + kBufs * kStage, s_val + kBufs * kStage};
   Table<kGlobalSlots, true> gt{nullptr, nullptr};
   uint32_t* g_scol = nullptr;
@@ -97,20 +101,15 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
   }
   const uint64_t rows = p.A.rows;
 
-  // tiles waiting for their offsets: p0 (oldest) and p1, finished kDefer
-  // iterations after they were computed
-  struct Pending {
-    uint64_t tile, agg;
-    uint32_t staged;
-    int buf;
-    bool global;
-  };
-  Pending p0{}, p1{};
-  int npend = 0;
-  int buf = 0;
+  // the previous batch waits for its offsets; its metadata lives in s_meta*
+  int nprev = 0;
+  int half = 0;  // which half of the staging buffers the current batch fills
 
-  auto finish = [&](uint64_t tile, uint64_t agg, uint32_t staged, bool global, int b) {
-    const uint64_t excl = lookback(p.tstat, p.gstat, tile, agg, p.epoch);
+  auto finish = [&](int b) {
+    const uint64_t tile = s_meta64[2 * b], agg = s_meta64[2 * b + 1];
+    const uint32_t staged = s_meta32[2 * b];
+    const bool global = s_meta32[2 * b + 1] != 0;
+    const uint64_t excl = lookback(p.lb, tile, agg);
     const uint64_t r0 = tile * R;
     if (lane < uint32_t(R) && r0 + lane < rows) {
       uint64_t s = 0;
@@ -133,7 +132,19 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
     __syncwarp();
   };
 
-  for (uint64_t tile = gwarp; tile < p.ntiles; tile += nwarps) {
+  // batch tickets are fetched one batch ahead (the atomic's latency hides
+  // behind a whole batch of work)
+  unsigned long long next_base = 0;
+  if (lane == 0) next_base = atomicAdd(p.ticket, (unsigned long long)kBatch);
+  while (true) {
+    const unsigned long long base = __shfl_sync(kFull, next_base, 0);
+    if (base >= p.ntiles) break;
+    if (lane == 0) next_base = atomicAdd(p.ticket, (unsigned long long)kBatch);
+    const int ncur = int(p.ntiles - base < uint64_t(kBatch) ? p.ntiles - base : kBatch);
+#pragma unroll 1
+    for (int bj = 0; bj < ncur; ++bj) {
+    const uint64_t tile = base + bj;
+    const int buf = half * kBatch + bj;
     const uint64_t r0 = tile * R;
     // ---- row bounds and classes of the tile ----
     uint64_t rpv = 0;
@@ -162,16 +173,40 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
     uint32_t staged = 0;
     bool global = false;
     if (any_short) {
-      ShortOut so[R];
-      short_rows<R, WIDE, STATS>(p.A, p.B, lo, na, on, so, nnz, smin, smax, stouch);
+      // rows go through short_rows in lockstep groups of kLock (register budget)
+      constexpr int kLock = R < 4 ? R : 4;
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        if (!on[i]) nnz[i] = 0;
-        if (on[i] && so[i].keep) {
-          s_col[buf * kStage + staged + so[i].rank] = so[i].col;
-          s_val[buf * kStage + staged + so[i].rank] = so[i].val;
+      for (int h = 0; h < R / kLock; ++h) {
+        uint64_t hlo[kLock];
+        uint32_t hna[kLock], hnnz[kLock], hmin[kLock], hmax[kLock], htouch[kLock];
+        bool hon[kLock];
+        bool hany = false;
+#pragma unroll
+        for (int i = 0; i < kLock; ++i) {
+          hlo[i] = lo[h * kLock + i];
+          hna[i] = na[h * kLock + i];
+          hon[i] = on[h * kLock + i];
+          hany |= hon[i];
         }
-        staged += nnz[i];
+        if (!hany) continue;
+        ShortOut so[kLock];
+        short_rows<kLock, WIDE, STATS>(p.A, p.B, hlo, hna, hon, so, hnnz, hmin, hmax, htouch);
+#pragma unroll
+        for (int i = 0; i < kLock; ++i) {
+          const int r = h * kLock + i;
+          if (!on[r]) continue;
+          nnz[r] = hnnz[i];
+          if (STATS) {
+            smin[r] = hmin[i];
+            smax[r] = hmax[i];
+            stouch[r] = htouch[i];
+          }
+          if (so[i].keep) {
+            s_col[buf * kStage + staged + so[i].rank] = so[i].col;
+            s_val[buf * kStage + staged + so[i].rank] = so[i].val;
+          }
+          staged += nnz[r];
+        }
       }
     }
 
@@ -248,29 +283,24 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : 4) k_fused(const Fuse
       }
     }
     __syncwarp();
-    publish_aggregate(p.tstat, p.gstat, p.gcount, tile, agg, p.ntiles, p.epoch);
+    publish_aggregate(p.lb, tile, agg);
 
-    // ---- finish the tile computed kDefer iterations ago ----
-    const Pending cur{tile, agg, staged, buf, global};
-    if (npend == kDefer) {
-      finish(p0.tile, p0.agg, p0.staged, p0.global, p0.buf);
-      if (kDefer == 2) {
-        p0 = p1;
-        p1 = cur;
-      } else {
-        p0 = cur;
-      }
-    } else if (npend == 0) {
-      p0 = cur;
-      ++npend;
-    } else {
-      p1 = cur;
-      ++npend;
+    if (lane == 0) {
+      s_meta64[2 * buf] = tile;
+      s_meta64[2 * buf + 1] = agg;
+      s_meta32[2 * buf] = staged;
+      s_meta32[2 * buf + 1] = global ? 1u : 0u;
     }
-    buf = buf == kBufs - 1 ? 0 : buf + 1;
+    __syncwarp();
+    }  // tiles of the batch
+    // ---- finish the previous batch ----
+#pragma unroll 1
+    for (int j = 0; j < nprev; ++j) finish((half ^ 1) * kBatch + j);
+    nprev = ncur;
+    half ^= 1;
   }
-  if (npend > 0) finish(p0.tile, p0.agg, p0.staged, p0.global, p0.buf);
-  if (npend > 1) finish(p1.tile, p1.agg, p1.staged, p1.global, p1.buf);
+#pragma unroll 1
+  for (int j = 0; j < nprev; ++j) finish((half ^ 1) * kBatch + j);
 }
 
 }  // namespace spmmm

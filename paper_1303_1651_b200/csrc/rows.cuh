@@ -55,11 +55,17 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
       len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1) - bs[i]);
     }
   }
+  // widest A row of the tile bounds the scan and search depth (warp-uniform)
+  uint32_t na_max = 1;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (on[i] && na[i] > na_max) na_max = na[i];
   uint32_t incl[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) incl[i] = len[i];
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
+    if (uint32_t(d) >= na_max) break;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const uint32_t t = __shfl_up_sync(kFull, incl[i], d);
@@ -71,12 +77,14 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     excl[i] = incl[i] - len[i];
-    tot[i] = __shfl_sync(kFull, incl[i], 31);
+    tot[i] = __shfl_sync(kFull, incl[i], (na[i] - 1) & 31u);
+    if (lane >= na[i]) excl[i] = tot[i];  // beyond the row: never owns a product
     src[i] = 0;
   }
   // entry owning product q = lane: the largest i with excl_i <= lane
 #pragma unroll
   for (int st = 16; st > 0; st >>= 1) {
+    if (uint32_t(st) >= na_max) continue;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const uint32_t ex = __shfl_sync(kFull, excl[i], src[i] + st);
@@ -108,30 +116,34 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
   bitonic32_multi<R>(key);
   double v[R], acc[R];
   bool head[R];
-  uint32_t touches[R];
+  uint32_t seg[R], touches[R];
+  uint32_t max_seg = 0;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     col[i] = uint32_t(key[i] >> 5);
     v[i] = __shfl_sync(kFull, p[i], uint32_t(key[i]) & 31u);
     const uint32_t prev = __shfl_up_sync(kFull, col[i], 1);
     head[i] = lane < tot[i] && (lane == 0 || prev != col[i]);
+    // segment = this head's run of equal columns: up to the next head (or tot)
+    const uint32_t hm = __ballot_sync(kFull, head[i]);
+    const uint32_t above = hm & ~((2u << lane) - 1u);
+    const uint32_t nxt = above ? uint32_t(__ffs(above) - 1) : tot[i];
+    seg[i] = head[i] ? nxt - lane : 0u;
+    max_seg = seg[i] > max_seg ? seg[i] : max_seg;
     acc[i] = v[i];
     touches[i] = 1;
   }
-  for (int d = 1; d < 32; ++d) {
-    bool any = false;
+  max_seg = __reduce_max_sync(kFull, max_seg);
+  // left fold of each segment in lane (= reference k) order
+  for (uint32_t d = 1; d < max_seg; ++d) {
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const uint32_t c = __shfl_down_sync(kFull, col[i], d);
       const double t = __shfl_down_sync(kFull, v[i], d);
-      const bool cond = head[i] && (lane + uint32_t(d) < tot[i]) && c == col[i];
-      if (cond) {
+      if (d < seg[i]) {
         if (STATS && acc[i] == 0.0) ++touches[i];  // re-touch after a transient zero
         acc[i] = __dadd_rn(acc[i], t);
       }
-      any |= cond;
     }
-    if (!__any_sync(kFull, any)) break;
   }
 #pragma unroll
   for (int i = 0; i < R; ++i) {

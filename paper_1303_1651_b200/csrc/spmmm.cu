@@ -388,10 +388,15 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
 
   if (rows) {
     const uint64_t ntiles = (rows + rows_per_tile - 1) / rows_per_tile;
-    const uint64_t ngroups = (ntiles + 31) / 32;
+    // look-back levels: words per level, then counters of levels 1..
+    uint64_t nl[kLevels];
+    nl[0] = ntiles;
+    for (int l = 1; l < kLevels; ++l) nl[l] = (nl[l - 1] + 31) / 32;
+    uint64_t words = 0, counters = 0;
+    for (int l = 0; l < kLevels; ++l) words += nl[l];
+    for (int l = 1; l < kLevels; ++l) counters += nl[l];
     bool grown = false;
-    e = ensure(c->status, (ntiles + ngroups) * sizeof(uint64_t) + ngroups * sizeof(uint32_t),
-               c->stream, &grown);
+    e = ensure(c->status, (words + counters) * sizeof(uint64_t), c->stream, &grown);
     if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "status: %s", cudaGetErrorString(e)));
     if (grown || c->epoch >= 0xffffu) {
       e = cudaMemsetAsync(c->status.p, 0, c->status.cap, c->stream);
@@ -399,11 +404,26 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       c->epoch = 0;
     }
     c->epoch += 1;
-    uint32_t* gcount = reinterpret_cast<uint32_t*>(static_cast<uint64_t*>(c->status.p) + ntiles +
-                                                   ngroups);
-    e = cudaMemsetAsync(gcount, 0, ngroups * sizeof(uint32_t), c->stream);
-    if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
     FusedParams fp;
+    {
+      uint64_t* w = static_cast<uint64_t*>(c->status.p);
+      unsigned long long* cnt = reinterpret_cast<unsigned long long*>(w + words);
+      e = cudaMemsetAsync(cnt, 0, counters * sizeof(unsigned long long), c->stream);
+      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+      fp.lb.count[0] = nullptr;
+      for (int l = 0; l < kLevels; ++l) {
+        fp.lb.stat[l] = w;
+        fp.lb.n[l] = nl[l];
+        w += nl[l];
+        if (l > 0) {
+          fp.lb.count[l] = cnt;
+          cnt += nl[l];
+        }
+      }
+      fp.lb.epoch = c->epoch;
+      fp.lb.fault = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault;
+    }
+    fp.ticket = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlTicket;
     fp.A = A;
     fp.B = B;
     fp.prod = static_cast<const uint32_t*>(c->prod.p);
@@ -412,11 +432,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.c_rp = p->rp;
     fp.c_ci = p->ci;
     fp.c_v = p->v;
-    fp.tstat = static_cast<uint64_t*>(c->status.p);
-    fp.gstat = static_cast<uint64_t*>(c->status.p) + ntiles;
-    fp.gcount = gcount;
     fp.ntiles = ntiles;
-    fp.epoch = c->epoch;
     fp.medium_limit = medium_limit;
     fp.g_keys = nullptr;
     fp.g_vals = nullptr;
@@ -473,11 +489,19 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   }
   release(stage_ci, c->stream);
   release(stage_v, c->stream);
-  e = cudaMemcpyAsync(c->h_ctrl + kCtrlWords - 1, p->rp + rows, sizeof(uint64_t),
-                      cudaMemcpyDeviceToHost, c->stream);
+  e = cudaMemcpyAsync(c->h_ctrl + kCtrlFault, static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault,
+                      sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->h_ctrl + kCtrlTotal, p->rp + rows, sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
-  p->nnz = c->h_ctrl[kCtrlWords - 1];
+  if (c->h_ctrl[kCtrlFault]) {
+    const unsigned long long f = c->h_ctrl[kCtrlFault];
+    return cleanup(fail(SPMMM_ERR_CUDA, "k_fused look-back watchdog: site %llu tile %llu",
+                        (f >> 48) & 0x7fff, f & ((1ull << 48) - 1)));
+  }
+  p->nnz = c->h_ctrl[kCtrlTotal];
   if (tm.on) {
     for (int k = 0; k < kNumKernels; ++k) {
       if (!c->ev_used[k]) continue;
