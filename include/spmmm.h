@@ -132,6 +132,15 @@ int spmmm_last_timings(spmmm_context* ctx, const char** names, double* ms, int c
 /* Number of kernels the last spmmm_multiply launched. */
 int spmmm_last_launch_count(spmmm_context* ctx, int* count);
 
+/* Page-locked host buffers from a process-wide pool (freed blocks are kept
+ * and reused by size). Downloading C into pinned memory runs at PCIe speed
+ * instead of the pageable-copy rate; the Python drop-in returns CsrMatrix
+ * arrays backed by these buffers. */
+int spmmm_host_alloc(uint64_t bytes, void** ptr);
+int spmmm_host_free(void* ptr);
+/* Bytes currently held by the pool (in use + cached). */
+int spmmm_host_pool_bytes(uint64_t* in_use, uint64_t* cached);
+
 #ifdef __cplusplus
 }
 #endif

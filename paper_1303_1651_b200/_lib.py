@@ -41,6 +41,7 @@ EXPORTS = (
     "spmmm_product_download", "spmmm_product_copy_device", "spmmm_product_row_stats",
     "spmmm_product_destroy", "spmmm_estimate_nnz", "spmmm_row_products_prefix",
     "spmmm_last_timings", "spmmm_last_launch_count",
+    "spmmm_host_alloc", "spmmm_host_free", "spmmm_host_pool_bytes",
     "spmmm_splitmix64", "spmmm_gen_fd_size", "spmmm_gen_fd", "spmmm_gen_fd3_size",
     "spmmm_gen_fd3", "spmmm_gen_random_k", "spmmm_gen_zipf",
 )
@@ -99,6 +100,9 @@ def _declare(lib):
         "spmmm_last_timings": (i, [vp, ctypes.POINTER(ctypes.c_char_p),
                                    ctypes.POINTER(ctypes.c_double), i, ctypes.POINTER(i)]),
         "spmmm_last_launch_count": (i, [vp, ctypes.POINTER(i)]),
+        "spmmm_host_alloc": (i, [c_u64, pp]),
+        "spmmm_host_free": (i, [vp]),
+        "spmmm_host_pool_bytes": (i, [p_u64, p_u64]),
         "spmmm_splitmix64": (i, [c_u64, c_u64, vp]),
         "spmmm_gen_fd_size": (i, [c_u64, p_u64, p_u64]),
         "spmmm_gen_fd": (i, [c_u64, vp, vp, vp]),
@@ -214,6 +218,20 @@ class Context:
         return n.value
 
 
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """numpy array of n elements in page-locked memory from the library's
+    pool; the block returns to the pool when the array (and its views) die."""
+    import weakref
+
+    dtype = np.dtype(dtype)
+    nbytes = max(int(n) * dtype.itemsize, 1)
+    ptr = ctypes.c_void_p()
+    check(lib().spmmm_host_alloc(nbytes, ctypes.byref(ptr)), "spmmm_host_alloc")
+    buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, lib().spmmm_host_free, ctypes.c_void_p(ptr.value))
+    return np.frombuffer(buf, dtype=dtype, count=int(n))
+
+
 class Product:
     """Device-resident C returned by spmmm_multiply."""
 
@@ -226,10 +244,11 @@ class Product:
         self.rows, self.cols, self.nnz, self.multiplications = (
             rows.value, cols.value, nnz.value, mults.value)
 
-    def download(self):
-        rp = np.empty(self.rows + 1, np.uint64)
-        ci = np.empty(self.nnz, np.uint64)
-        v = np.empty(self.nnz, np.float64)
+    def download(self, pinned: bool = True):
+        alloc = pinned_empty if pinned else np.empty
+        rp = alloc(self.rows + 1, np.uint64)
+        ci = alloc(self.nnz, np.uint64)
+        v = alloc(self.nnz, np.float64)
         check(lib().spmmm_product_download(self._h, rp.ctypes.data,
                                            ci.ctypes.data if self.nnz else None,
                                            v.ctypes.data if self.nnz else None), "download")

@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -758,6 +759,102 @@ int spmmm_last_timings(spmmm_context* c, const char** names, double* ms, int cap
 int spmmm_last_launch_count(spmmm_context* c, int* count) {
   if (!c || !count) return fail(SPMMM_ERR_INVALID, "NULL argument");
   *count = c->last_launches;
+  return SPMMM_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================
+// Pinned host pool (process-wide): size-bucketed free lists of cudaHostAlloc
+// blocks. Pinning is expensive (page locking), so blocks are recycled.
+// =============================================================================
+namespace {
+
+struct HostPool {
+  std::mutex mu;
+  std::multimap<uint64_t, void*> free_blocks;  // capacity -> block
+  std::map<void*, uint64_t> live;              // block -> capacity
+  uint64_t in_use = 0, cached = 0;
+  static constexpr uint64_t kCacheLimit = 64ull << 30;
+
+  static uint64_t bucket(uint64_t bytes) {
+    // round up to 1/8 steps of the next power of two to bound waste
+    if (bytes <= 4096) return 4096;
+    uint64_t p = 1;
+    while (p < bytes) p <<= 1;
+    const uint64_t step = p / 8;
+    return (bytes + step - 1) / step * step;
+  }
+};
+
+HostPool& host_pool() {
+  static HostPool* pool = new HostPool;  // leaked on purpose: lives until exit
+  return *pool;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spmmm_host_alloc(uint64_t bytes, void** ptr) {
+  if (!ptr) return fail(SPMMM_ERR_INVALID, "ptr is NULL");
+  HostPool& hp = host_pool();
+  const uint64_t cap = HostPool::bucket(bytes ? bytes : 1);
+  {
+    std::lock_guard<std::mutex> lock(hp.mu);
+    auto it = hp.free_blocks.lower_bound(cap);
+    if (it != hp.free_blocks.end() && it->first <= cap + cap / 4) {
+      *ptr = it->second;
+      hp.live[it->second] = it->first;
+      hp.cached -= it->first;
+      hp.in_use += it->first;
+      hp.free_blocks.erase(it);
+      return SPMMM_OK;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, cap, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    // release the cache and retry once
+    std::lock_guard<std::mutex> lock(hp.mu);
+    for (auto& kv : hp.free_blocks) cudaFreeHost(kv.second);
+    hp.free_blocks.clear();
+    hp.cached = 0;
+    e = cudaHostAlloc(&p, cap, cudaHostAllocPortable);
+    if (e != cudaSuccess)
+      return fail(SPMMM_ERR_OOM, "cudaHostAlloc(%llu): %s", (unsigned long long)cap,
+                  cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lock(hp.mu);
+  hp.live[p] = cap;
+  hp.in_use += cap;
+  *ptr = p;
+  return SPMMM_OK;
+}
+
+int spmmm_host_free(void* ptr) {
+  if (!ptr) return SPMMM_OK;
+  HostPool& hp = host_pool();
+  std::lock_guard<std::mutex> lock(hp.mu);
+  auto it = hp.live.find(ptr);
+  if (it == hp.live.end()) return fail(SPMMM_ERR_INVALID, "pointer not from spmmm_host_alloc");
+  const uint64_t cap = it->second;
+  hp.live.erase(it);
+  hp.in_use -= cap;
+  if (hp.cached + cap > HostPool::kCacheLimit) {
+    cudaFreeHost(ptr);
+  } else {
+    hp.free_blocks.emplace(cap, ptr);
+    hp.cached += cap;
+  }
+  return SPMMM_OK;
+}
+
+int spmmm_host_pool_bytes(uint64_t* in_use, uint64_t* cached) {
+  HostPool& hp = host_pool();
+  std::lock_guard<std::mutex> lock(hp.mu);
+  if (in_use) *in_use = hp.in_use;
+  if (cached) *cached = hp.cached;
   return SPMMM_OK;
 }
 
