@@ -145,7 +145,10 @@ def multiply_rowmajor(a, b, *, row_choices: bool = False, threads: int = 1) -> O
     if rc != 0:
         raise RuntimeError(f"oracle failed with status {rc}")
     n = int(nnz.value)
-    return OracleResult(a.rows, b.cols, out_rp, out_ci[:n].copy(), out_v[:n].copy(),
+    # views into the capacity-sized buffers, as the reference's own
+    # CsrBuilder.finish() returns (formats.py:189-196); untouched pages of the
+    # reservation are never faulted in
+    return OracleResult(a.rows, b.cols, out_rp, out_ci[:n], out_v[:n],
                         int(mults.value), choice)
 
 

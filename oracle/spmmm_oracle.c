@@ -32,10 +32,24 @@
  * Pinned against the reference by tests/test_oracle.py (golden fixtures written by
  * tests/golden/make_golden.py, which imports the reference package itself).
  */
+#define _GNU_SOURCE
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <sys/mman.h>
+
+/* Large private buffers: 2 MiB aligned and hinted for transparent huge pages,
+ * so first-touch page faults do not dominate the multi-threaded baseline. */
+static void* big_alloc(size_t bytes) {
+  const size_t align = (size_t)2 << 20;
+  if (bytes < align) return malloc(bytes ? bytes : 1);
+  void* p = NULL;
+  bytes = (bytes + align - 1) / align * align;
+  if (posix_memalign(&p, align, bytes)) return NULL;
+  madvise(p, bytes, MADV_HUGEPAGE);
+  return p;
+}
 
 #define ORACLE_OK 0
 #define ORACLE_ERR_DIM 1
@@ -106,7 +120,8 @@ static uint64_t combined_rows(const ocsr* a, const ocsr* b, uint64_t r0, uint64_
                               uint64_t* out_rp, uint64_t* out_ci, double* out_v, uint64_t cap,
                               int8_t* choice) {
   const uint64_t length = b->cols;
-  double* dense = (double*)calloc(length ? length : 1, sizeof(double)); /* kernels.py:78 */
+  /* kernels.py:78; calloc keeps untouched columns as lazily zeroed pages */
+  double* dense = (double*)calloc(length ? length : 1, sizeof(double));
   uint64_t tcap = 64, tlen = 0;
   uint64_t* touched = (uint64_t*)malloc(tcap * sizeof(uint64_t));
   if (!dense || !touched) { free(dense); free(touched); return UINT64_MAX; }
@@ -201,22 +216,54 @@ int oracle_multiply_rowmajor(uint64_t a_rows, uint64_t a_cols, const uint64_t* a
   return ORACLE_OK;
 }
 
-/* ---- row-parallel variant (same bytes; the multi-core CPU baseline) ---- */
+/* ---- row-parallel variant (same bytes; the multi-core CPU baseline) ----
+ * Three parallel phases: per-row product counts, the product of each of P
+ * product-balanced row blocks into private buffers, then the concatenation
+ * (each thread copies its own block). Rows are independent, so the output is
+ * byte-identical to the serial product. */
 
 typedef struct {
   const ocsr* a;
   const ocsr* b;
   uint64_t r0, r1, cap;
-  uint64_t* rp;
+  uint64_t* prod; /* phase 0 output (rows) */
+  uint64_t* rp;   /* phase 1: private row_ptr (r1-r0+1) */
   uint64_t* ci;
   double* v;
   uint64_t n;
+  /* phase 2 */
+  uint64_t base;
+  uint64_t* out_rp;
+  uint64_t* out_ci;
+  double* out_v;
+  int phase;
 } ojob;
 
 static void* run_job(void* p) {
   ojob* j = (ojob*)p;
-  j->n = combined_rows(j->a, j->b, j->r0, j->r1, j->rp, j->ci, j->v, j->cap, NULL);
+  if (j->phase == 0) {
+    for (uint64_t r = j->r0; r < j->r1; ++r) {
+      uint64_t s = 0;
+      for (uint64_t e = j->a->rp[r]; e < j->a->rp[r + 1]; ++e)
+        s += j->b->rp[j->a->ci[e] + 1] - j->b->rp[j->a->ci[e]];
+      j->prod[r] = s;
+    }
+  } else if (j->phase == 1) {
+    j->n = combined_rows(j->a, j->b, j->r0, j->r1, j->rp, j->ci, j->v, j->cap, NULL);
+  } else {
+    for (uint64_t i = 0; i < j->r1 - j->r0; ++i) j->out_rp[j->r0 + i + 1] = j->base + j->rp[i + 1];
+    memcpy(j->out_ci + j->base, j->ci, j->n * sizeof(uint64_t));
+    memcpy(j->out_v + j->base, j->v, j->n * sizeof(double));
+  }
   return NULL;
+}
+
+static void run_phase(ojob* jobs, pthread_t* th, int n, int phase) {
+  for (int t = 0; t < n; ++t) {
+    jobs[t].phase = phase;
+    pthread_create(&th[t], NULL, run_job, &jobs[t]);
+  }
+  for (int t = 0; t < n; ++t) pthread_join(th[t], NULL);
 }
 
 int oracle_multiply_rowmajor_mt(int nthreads, uint64_t a_rows, uint64_t a_cols,
@@ -229,49 +276,50 @@ int oracle_multiply_rowmajor_mt(int nthreads, uint64_t a_rows, uint64_t a_cols,
   if ((uint64_t)nthreads > a_rows) nthreads = a_rows ? (int)a_rows : 1;
   ocsr a = {a_rows, a_cols, a_rp, a_ci, a_v};
   ocsr b = {b_rows, b_cols, b_rp, b_ci, b_v};
-  /* product-balanced row blocks */
-  uint64_t* pref = (uint64_t*)malloc((a_rows + 1) * sizeof(uint64_t));
+  uint64_t* prod = (uint64_t*)malloc((a_rows + 1) * sizeof(uint64_t));
   ojob* jobs = (ojob*)calloc((size_t)nthreads, sizeof(ojob));
   pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
-  if (!pref || !jobs || !th) { free(pref); free(jobs); free(th); return ORACLE_ERR_NOMEM; }
-  pref[0] = 0;
-  for (uint64_t r = 0; r < a_rows; ++r) {
-    uint64_t p = 0;
-    for (uint64_t e = a_rp[r]; e < a_rp[r + 1]; ++e) p += b_rp[a_ci[e] + 1] - b_rp[a_ci[e]];
-    pref[r + 1] = pref[r] + p;
+  if (!prod || !jobs || !th) { free(prod); free(jobs); free(th); return ORACLE_ERR_NOMEM; }
+  /* phase 0: per-row product counts over equal row ranges */
+  for (int t = 0; t < nthreads; ++t) {
+    jobs[t].a = &a; jobs[t].b = &b; jobs[t].prod = prod;
+    jobs[t].r0 = a_rows * (uint64_t)t / (uint64_t)nthreads;
+    jobs[t].r1 = a_rows * (uint64_t)(t + 1) / (uint64_t)nthreads;
   }
-  const uint64_t total = pref[a_rows];
-  uint64_t r = 0;
+  run_phase(jobs, th, nthreads, 0);
+  uint64_t total = 0;
+  for (uint64_t r = 0; r < a_rows; ++r) total += prod[r];
+  /* product-balanced blocks */
   int rc = ORACLE_OK;
+  uint64_t r = 0, acc = 0;
   for (int t = 0; t < nthreads; ++t) {
     const uint64_t target = (t + 1 == nthreads) ? total : total / nthreads * (t + 1);
-    uint64_t r1 = r;
-    while (r1 < a_rows && pref[r1 + 1] <= target) ++r1;
-    if (t + 1 == nthreads) r1 = a_rows;
-    jobs[t].a = &a; jobs[t].b = &b; jobs[t].r0 = r; jobs[t].r1 = r1;
-    jobs[t].cap = pref[r1] - pref[r];
+    uint64_t r1 = r, blk = 0;
+    while (r1 < a_rows && acc + prod[r1] <= target) { acc += prod[r1]; blk += prod[r1]; ++r1; }
+    if (t + 1 == nthreads) while (r1 < a_rows) { blk += prod[r1]; ++r1; }
+    jobs[t].r0 = r; jobs[t].r1 = r1; jobs[t].cap = blk;
     jobs[t].rp = (uint64_t*)malloc((r1 - r + 1) * sizeof(uint64_t));
-    jobs[t].ci = (uint64_t*)malloc((jobs[t].cap ? jobs[t].cap : 1) * sizeof(uint64_t));
-    jobs[t].v = (double*)malloc((jobs[t].cap ? jobs[t].cap : 1) * sizeof(double));
+    jobs[t].ci = (uint64_t*)big_alloc((blk ? blk : 1) * sizeof(uint64_t));
+    jobs[t].v = (double*)big_alloc((blk ? blk : 1) * sizeof(double));
     if (!jobs[t].rp || !jobs[t].ci || !jobs[t].v) rc = ORACLE_ERR_NOMEM;
     r = r1;
   }
   if (rc == ORACLE_OK) {
-    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, run_job, &jobs[t]);
-    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    run_phase(jobs, th, nthreads, 1);
     uint64_t base = 0;
     out_rp[0] = 0;
-    for (int t = 0; t < nthreads && rc == ORACLE_OK; ++t) {
+    for (int t = 0; t < nthreads; ++t) {
       if (jobs[t].n == UINT64_MAX || base + jobs[t].n > cap) { rc = ORACLE_ERR_CAPACITY; break; }
-      for (uint64_t i = 0; i < jobs[t].r1 - jobs[t].r0; ++i)
-        out_rp[jobs[t].r0 + i + 1] = base + jobs[t].rp[i + 1];
-      memcpy(out_ci + base, jobs[t].ci, jobs[t].n * sizeof(uint64_t));
-      memcpy(out_v + base, jobs[t].v, jobs[t].n * sizeof(double));
+      jobs[t].base = base;
+      jobs[t].out_rp = out_rp; jobs[t].out_ci = out_ci; jobs[t].out_v = out_v;
       base += jobs[t].n;
     }
-    if (nnz) *nnz = base;
+    if (rc == ORACLE_OK) {
+      run_phase(jobs, th, nthreads, 2);
+      if (nnz) *nnz = base;
+    }
   }
   for (int t = 0; t < nthreads; ++t) { free(jobs[t].rp); free(jobs[t].ci); free(jobs[t].v); }
-  free(pref); free(jobs); free(th);
+  free(prod); free(jobs); free(th);
   return rc;
 }
