@@ -55,7 +55,7 @@ constexpr int kMaxBufs = 4;  // staging buffers of the largest variant
 // with more than kStage outputs stage in the warp's global buffers instead.
 template <int R, bool MEDIUM>
 struct FusedSmem {
-  static constexpr int kBatch = MEDIUM ? 2 : 1;  // tiles per ticket
+  static constexpr int kBatch = 1;  // tiles per ticket
   static constexpr int kBufs = 2 * kBatch;
   static constexpr int kStage = MEDIUM ? 128 : 32 * R;
   static constexpr int kTable = MEDIUM ? kSmemSlots : 0;
@@ -69,12 +69,12 @@ struct FusedSmem {
 };
 
 template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : (R <= 2 ? 6 : 4)) k_fused(const FusedParams p) {
+__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_fused(const FusedParams p) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   using SM = FusedSmem<R, MEDIUM>;
-  constexpr int EMAX = MEDIUM ? int(kMediumLimit / 32) : 1;
+  constexpr int EMAX = MEDIUM ? kSmemSlots / 32 : 1;  // register sort up to 256 keys
   constexpr int kStage = SM::kStage;
   constexpr int kBufs = SM::kBufs;
   constexpr int kBatch = SM::kBatch;
@@ -224,39 +224,48 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 3 : (R <= 2 ? 6 : 4)) k_f
           touches = 0;
           use_gt = true;
           medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo[0], hi, gt, kGlobalSlots, touches);
-          cnt = gt.template compact<STATS>(smin[0], smax[0]);
+          cnt = 0;
         }
-        nnz[0] = cnt;
-        staged = cnt;
-        global = cnt > uint32_t(kStage);  // too big for the shared stage
-        int E = 1;
-        while (uint32_t(E) * 32u < cnt) E <<= 1;
-        K mk[EMAX];
+        if (use_gt) {
+          // stage in global memory: gather the keys, sort them in registers,
+          // then fetch each value from the (intact) table
+          uint32_t* scol = g_scol + buf * kMediumLimit;
+          double* sval = g_sval + buf * kMediumLimit;
+          cnt = gt.template gather_keys<STATS>(scol, smin[0], smax[0]);
+          sort_keys_global(scol, cnt);
+          for (uint32_t t = lane; t < cnt; t += 32) __stcg(sval + t, gt.lookup(__ldcg(scol + t)));
+          global = true;
+        } else {
+          global = cnt > uint32_t(kStage);  // too big for the shared stage
+          int E = 1;
+          while (uint32_t(E) * 32u < cnt) E <<= 1;
+          K mk[EMAX];
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          const uint32_t idx = uint32_t(e) * 32u + lane;
-          uint32_t kcol = kEmptyKey;
-          if (e < E && idx < cnt) kcol = use_gt ? gt.ldk(idx) : st.ldk(idx);
-          mk[e] = (e < E && idx < cnt) ? ((K(kcol) << kPosBits) | K(idx)) : ~K(0);
-        }
-        bitonic_sort_dyn(mk, E);
-        // sorted (col, value) into this tile's staging buffer
+          for (int e = 0; e < EMAX; ++e) {
+            const uint32_t idx = uint32_t(e) * 32u + lane;
+            mk[e] = (e < E && idx < cnt) ? ((K(st.ldk(idx)) << kPosBits) | K(idx)) : ~K(0);
+          }
+          bitonic_sort_dyn(mk, E);
+          // sorted (col, value) into this tile's staging buffer
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          const uint32_t idx = uint32_t(e) * 32u + lane;
-          if (e < E && idx < cnt) {
-            const uint32_t pos = uint32_t(mk[e]) & uint32_t(kGlobalSlots - 1);
-            const uint32_t col = uint32_t(mk[e] >> kPosBits);
-            const double val = use_gt ? gt.ldv(pos) : st.ldv(pos);
-            if (global) {
-              __stcg(g_scol + buf * kMediumLimit + idx, col);
-              __stcg(g_sval + buf * kMediumLimit + idx, val);
-            } else {
-              s_col[buf * kStage + idx] = col;
-              s_val[buf * kStage + idx] = val;
+          for (int e = 0; e < EMAX; ++e) {
+            const uint32_t idx = uint32_t(e) * 32u + lane;
+            if (e < E && idx < cnt) {
+              const uint32_t pos = uint32_t(mk[e]) & uint32_t(kGlobalSlots - 1);
+              const uint32_t col = uint32_t(mk[e] >> kPosBits);
+              const double val = st.ldv(pos);
+              if (global) {
+                __stcg(g_scol + buf * kMediumLimit + idx, col);
+                __stcg(g_sval + buf * kMediumLimit + idx, val);
+              } else {
+                s_col[buf * kStage + idx] = col;
+                s_val[buf * kStage + idx] = val;
+              }
             }
           }
         }
+        nnz[0] = cnt;
+        staged = cnt;
         __syncwarp();
         if (use_gt) gt.clear();
         else st.clear();

@@ -228,6 +228,38 @@ struct Table {
     for (uint32_t s = lane; s < uint32_t(T); s += 32) stk(s, kEmptyKey);
     __syncwarp();
   }
+  // Copy the occupied nonzero keys to out[0..cnt) (table left intact);
+  // STATS: min/max over every occupied slot.
+  template <bool STATS>
+  __device__ __forceinline__ uint32_t gather_keys(uint32_t* out, uint32_t& smin,
+                                                  uint32_t& smax) const {
+    const uint32_t lane = lane_id();
+    uint32_t cnt = 0, mn = kEmptyKey, mx = 0;
+    for (uint32_t s0 = 0; s0 < uint32_t(T); s0 += 32) {
+      const uint32_t k = ldk(s0 + lane);
+      const bool occ = k != kEmptyKey;
+      const bool keep = occ && (ldv(s0 + lane) != 0.0);
+      if (STATS && occ) {
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+      }
+      const uint32_t m = __ballot_sync(kFull, keep);
+      if (keep) __stcg(out + cnt + __popc(m & lanemask_lt()), k);
+      cnt += __popc(m);
+    }
+    if (STATS) {
+      smin = __reduce_min_sync(kFull, mn);
+      smax = __reduce_max_sync(kFull, mx);
+    }
+    __syncwarp();
+    return cnt;
+  }
+  // value of a key known to be present
+  __device__ __forceinline__ double lookup(uint32_t col) const {
+    uint32_t h = hash(col);
+    while (ldk(h) != col) h = (h + 1) & (T - 1);
+    return ldv(h);
+  }
   // Compact the occupied nonzero slots to the front (in place); returns the
   // count. STATS: min/max over every occupied slot, zero-valued ones included.
   template <bool STATS>
@@ -262,49 +294,117 @@ struct Table {
   }
 };
 
-// One chunk of up to 32 consecutive products of a group of <= 32 A entries,
-// cut at B-row boundaries when possible. The B loads are issued when the
-// chunk is made and consumed when it is applied (register prefetch).
+// Overflowed rows (more distinct columns than the shared table holds):
+// sort up to kMediumLimit column keys staged in global memory, in registers
+// (32 per lane), out of line so the main kernel keeps its small footprint.
+static __device__ __noinline__ void sort_keys_global(uint32_t* keys, uint32_t n) {
+  const uint32_t lane = lane_id();
+  constexpr int N = kMediumLimit / 32;
+  uint32_t k[N];
+  int E = 1;
+  while (uint32_t(E) * 32u < n) E <<= 1;
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    const uint32_t idx = uint32_t(e) * 32u + lane;
+    k[e] = (e < E && idx < n) ? __ldcg(keys + idx) : kEmptyKey;
+  }
+  bitonic_sort_dyn(k, E);
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    const uint32_t idx = uint32_t(e) * 32u + lane;
+    if (e < E && idx < n) __stcg(keys + idx, k[e]);
+  }
+  __syncwarp();
+}
+
+// One chunk of up to 32 consecutive products of a group of <= 32 A entries.
+// The walk keeps a cursor (entry i, offset within its B row). A chunk is
+//  * single: up to 32 products of one B row (distinct columns) — the common
+//    case for long B rows; no search, every lane takes product `off + lane`;
+//  * packed: whole consecutive short B rows up to 32 products, located per
+//    lane by a binary search over the entries' exclusive offsets.
+// The B loads are issued when the chunk is made and consumed when applied.
 struct Chunk {
-  uint32_t cs, ce;
-  bool single;  // all products come from one B row: columns distinct
+  uint32_t n;       // products in the chunk (0: walk finished)
+  bool single;      // all products from one B row: columns distinct
   uint64_t col;
   double bv;
   double a;
+  uint32_t i_next;  // cursor after this chunk
+  uint32_t off_next;
 };
 
-__device__ __forceinline__ Chunk make_chunk(const DevCsr& B, uint32_t cs, uint32_t gtot,
-                                            uint32_t incl, uint32_t excl, uint64_t bs,
-                                            double av) {
+struct Group {  // one group of <= 32 A entries, one entry per lane
+  uint32_t len, incl, excl, nent;
+  uint64_t bs;
+  double av;
+};
+
+__device__ __forceinline__ Chunk make_chunk(const DevCsr& B, const Group& g, uint32_t i,
+                                            uint32_t off) {
   Chunk c;
-  c.cs = cs;
+  c.n = 0;
+  c.single = true;
   c.col = kEmptyKey;
   c.bv = 0.0;
   c.a = 0.0;
-  c.single = true;
-  if (cs >= gtot) {
-    c.ce = cs;
+  const uint32_t lane = lane_id();
+  // skip exhausted / empty entries (warp-uniform)
+  uint32_t li = i < g.nent ? __shfl_sync(kFull, g.len, i & 31u) : 0u;
+  while (i < g.nent && off >= li) {
+    ++i;
+    off = 0;
+    li = i < g.nent ? __shfl_sync(kFull, g.len, i & 31u) : 0u;
+  }
+  if (i >= g.nent) {
+    c.i_next = i;
+    c.off_next = 0;
     return c;
   }
-  const uint32_t lane = lane_id();
+  const uint32_t rem = li - off;
+  const uint32_t nxt = i + 1 < g.nent ? __shfl_sync(kFull, g.len, (i + 1) & 31u) : 64u;
+  if (rem >= 32 || rem + nxt > 32) {
+    // single B row
+    c.n = rem < 32 ? rem : 32;
+    const uint64_t bsrc = __shfl_sync(kFull, g.bs, i & 31u) + off;
+    c.a = __shfl_sync(kFull, g.av, i & 31u);
+    if (lane < c.n) {
+      c.col = ld_idx(B.ci + bsrc + lane);
+      c.bv = ld_val(B.v + bsrc + lane);
+    }
+    off += c.n;
+    if (off >= li) {
+      ++i;
+      off = 0;
+    }
+    c.i_next = i;
+    c.off_next = off;
+    return c;
+  }
+  // packed: from (i, off) through the last entry that still fits in 32
+  c.single = false;
+  const uint32_t cs = __shfl_sync(kFull, g.excl, i & 31u) + off;
   const uint32_t lim = cs + 32;
-  const uint32_t bm = __ballot_sync(kFull, incl > cs && incl <= lim);
-  c.ce = bm ? __shfl_sync(kFull, incl, 31 - __clz(bm)) : (lim < gtot ? lim : gtot);
+  const uint32_t bm = __ballot_sync(kFull, lane < g.nent && g.incl > cs && g.incl <= lim);
+  const uint32_t last = 31 - __clz(bm);  // bm != 0: entry i itself ends within lim
+  const uint32_t ce = __shfl_sync(kFull, g.incl, last);
+  c.n = ce - cs;
   const uint32_t q = cs + lane;
-  int i = 0;
+  int e = int(i);
 #pragma unroll
   for (int st = 16; st > 0; st >>= 1) {
-    const uint32_t ex = __shfl_sync(kFull, excl, i + st);
-    if (ex <= q) i += st;
+    const uint32_t ex = __shfl_sync(kFull, g.excl, (e + st) & 31);
+    if (e + st <= int(last) && ex <= q) e += st;
   }
-  const uint64_t bsrc = __shfl_sync(kFull, bs, i);
-  c.a = __shfl_sync(kFull, av, i);
-  const uint32_t j = q - __shfl_sync(kFull, excl, i);
-  c.single = __shfl_sync(kFull, i, 0) == __shfl_sync(kFull, i, (c.ce - cs - 1) & 31u);
-  if (q < c.ce) {
+  const uint64_t bsrc = __shfl_sync(kFull, g.bs, e);
+  c.a = __shfl_sync(kFull, g.av, e);
+  const uint32_t j = q - __shfl_sync(kFull, g.excl, e);
+  if (lane < c.n) {
     c.col = ld_idx(B.ci + bsrc + j);
     c.bv = ld_val(B.v + bsrc + j);
   }
+  c.i_next = last + 1;
+  c.off_next = 0;
   return c;
 }
 
@@ -313,7 +413,7 @@ template <class Tab, bool STATS>
 __device__ __forceinline__ uint32_t apply_chunk(const Tab& tab, const Chunk& c,
                                                 uint32_t& touches) {
   const uint32_t lane = lane_id();
-  const bool act = c.cs + lane < c.ce;
+  const bool act = lane < c.n;
   const uint32_t col = uint32_t(c.col);
   const double p = __dmul_rn(c.a, c.bv);
   bool fresh = false;
@@ -321,7 +421,7 @@ __device__ __forceinline__ uint32_t apply_chunk(const Tab& tab, const Chunk& c,
     if (act) fresh = tab.template apply<STATS>(col, p, touches);
     __syncwarp();
   } else {
-    // equal columns from different B rows: apply in rounds, lowest q first
+    // equal columns from different B rows: apply in rounds, lowest product first
     const uint32_t am = __ballot_sync(kFull, act);
     const uint32_t peers = __match_any_sync(kFull, act ? col : kEmptyKey) & am;
     const uint32_t rank = __popc(peers & lanemask_lt());
@@ -343,35 +443,36 @@ __device__ __forceinline__ bool medium_accumulate(const DevCsr& A, const DevCsr&
   const uint32_t lane = lane_id();
   uint32_t inserted = 0;
   for (uint64_t abase = lo; abase < hi; abase += 32) {
+    Group g;
+    g.nent = uint32_t(hi - abase < 32 ? hi - abase : 32);
     const uint64_t e = abase + lane;
-    uint32_t len = 0;
-    uint64_t bs = 0;
-    double av = 0.0;
-    if (e < hi) {
+    g.len = 0;
+    g.bs = 0;
+    g.av = 0.0;
+    if (lane < g.nent) {
       const uint64_t k = ld_idx(A.ci + e);
-      av = ld_val(A.v + e);
-      bs = ld_idx(B.rp + k);
-      len = uint32_t(ld_idx(B.rp + k + 1) - bs);
+      g.av = ld_val(A.v + e);
+      g.bs = ld_idx(B.rp + k);
+      g.len = uint32_t(ld_idx(B.rp + k + 1) - g.bs);
     }
-    const uint32_t incl = warp_incl_scan(len);
-    const uint32_t excl = incl - len;
-    const uint32_t gtot = __shfl_sync(kFull, incl, 31);
+    g.incl = warp_incl_scan(g.len);
+    g.excl = g.incl - g.len;
     // three chunks in flight
-    Chunk c0 = make_chunk(B, 0, gtot, incl, excl, bs, av);
-    Chunk c1 = make_chunk(B, c0.ce, gtot, incl, excl, bs, av);
-    Chunk c2 = make_chunk(B, c1.ce, gtot, incl, excl, bs, av);
-    while (c0.cs < gtot) {
+    Chunk c0 = make_chunk(B, g, 0, 0);
+    Chunk c1 = make_chunk(B, g, c0.i_next, c0.off_next);
+    Chunk c2 = make_chunk(B, g, c1.i_next, c1.off_next);
+    while (c0.n) {
       inserted += apply_chunk<Tab, STATS>(tab, c0, touches);
       if (inserted > limit) return false;
-      c0 = make_chunk(B, c2.ce, gtot, incl, excl, bs, av);
-      if (c1.cs >= gtot) break;
+      c0 = make_chunk(B, g, c2.i_next, c2.off_next);
+      if (!c1.n) break;
       inserted += apply_chunk<Tab, STATS>(tab, c1, touches);
       if (inserted > limit) return false;
-      c1 = make_chunk(B, c0.ce, gtot, incl, excl, bs, av);
-      if (c2.cs >= gtot) break;
+      c1 = make_chunk(B, g, c0.i_next, c0.off_next);
+      if (!c2.n) break;
       inserted += apply_chunk<Tab, STATS>(tab, c2, touches);
       if (inserted > limit) return false;
-      c2 = make_chunk(B, c1.ce, gtot, incl, excl, bs, av);
+      c2 = make_chunk(B, g, c1.i_next, c1.off_next);
     }
   }
   return true;
