@@ -31,7 +31,26 @@ struct DevCsr {
   const uint64_t* __restrict__ ci;  // nnz
   const double* __restrict__ v;     // nnz
   uint64_t rows, cols, nnz;
+  uint64_t pol;  // L2 cache policy for this operand's loads (0 = default)
 };
+
+// L2 eviction policies (createpolicy): B is re-read across rows and should
+// stay in L2; A (when it is not also B) and C stream through once.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 __device__ __forceinline__ int classify(uint32_t prod, uint64_t na, uint32_t medium_limit) {
   if (prod == 0) return kRowZero;
@@ -53,6 +72,16 @@ __device__ __forceinline__ uint64_t ld_idx(const uint64_t* p) {
   return __ldg(reinterpret_cast<const unsigned long long*>(p));
 }
 __device__ __forceinline__ double ld_val(const double* p) { return __ldg(p); }
+__device__ __forceinline__ uint64_t ld_idx(const uint64_t* p, uint64_t pol) {
+  uint64_t v;
+  asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_val(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 
 // ---- relaxed gpu-scope accesses for the look-back status words ----
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {

@@ -32,6 +32,7 @@ struct FusedParams {
   unsigned long long* ticket;  // next free tile (zeroed per call)
   uint64_t ntiles;
   uint32_t medium_limit;
+  uint32_t a_is_b;  // A and B are the same arrays
   uint32_t* g_keys;  // [#warps][kGlobalSlots] overflow tables (medium kernel)
   double* g_vals;
   uint32_t* g_scol;  // [#warps][2][kMediumLimit] staging of overflowed rows
@@ -69,7 +70,7 @@ struct FusedSmem {
 };
 
 template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_fused(const FusedParams p) {
+__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_fused(const FusedParams p_in) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
@@ -82,6 +83,11 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint64_t gwarp = uint64_t(blockIdx.x) * WARPS + warp;
+  // B rows are re-read across A rows: keep them in L2. A streams once unless
+  // it is B itself (C = A·A: its rows are the B rows of neighbouring rows).
+  FusedParams p = p_in;
+  p.B.pol = policy_evict_last();
+  p.A.pol = p.a_is_b ? p.B.pol : policy_evict_first();
   double* s_val = reinterpret_cast<double*>(smem_raw) + size_t(warp) * SM::kWords64;
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem_raw + size_t(WARPS) * SM::kWords64 * 8) +
                     size_t(warp) * SM::kWords32;
@@ -120,26 +126,28 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
     }
     if (global) {
       for (uint32_t t = lane; t < staged; t += 32) {
-        p.c_ci[excl + t] = __ldcg(g_scol + b * kMediumLimit + t);
-        p.c_v[excl + t] = __ldcg(g_sval + b * kMediumLimit + t);
+        __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + excl + t,
+               (unsigned long long)__ldcg(g_scol + b * kMediumLimit + t));
+        __stcs(p.c_v + excl + t, __ldcg(g_sval + b * kMediumLimit + t));
       }
     } else {
       for (uint32_t t = lane; t < staged; t += 32) {
-        p.c_ci[excl + t] = s_col[b * kStage + t];
-        p.c_v[excl + t] = s_val[b * kStage + t];
+        // C is written once and not re-read here: evict-first
+        __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + excl + t,
+               (unsigned long long)s_col[b * kStage + t]);
+        __stcs(p.c_v + excl + t, s_val[b * kStage + t]);
       }
     }
     __syncwarp();
   };
 
-  // batch tickets are fetched one batch ahead (the atomic's latency hides
-  // behind a whole batch of work)
-  unsigned long long next_base = 0;
-  if (lane == 0) next_base = atomicAdd(p.ticket, (unsigned long long)kBatch);
+  // A tile must be computed right after it is acquired (successors wait on
+  // it), so tickets are taken when needed, never ahead.
   while (true) {
-    const unsigned long long base = __shfl_sync(kFull, next_base, 0);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(p.ticket, (unsigned long long)kBatch);
+    base = __shfl_sync(kFull, base, 0);
     if (base >= p.ntiles) break;
-    if (lane == 0) next_base = atomicAdd(p.ticket, (unsigned long long)kBatch);
     const int ncur = int(p.ntiles - base < uint64_t(kBatch) ? p.ntiles - base : kBatch);
 #pragma unroll 1
     for (int bj = 0; bj < ncur; ++bj) {
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
     // ---- row bounds and classes of the tile ----
     uint64_t rpv = 0;
     uint32_t prv = 0;
-    if (lane <= uint32_t(R) && r0 + lane <= rows) rpv = ld_idx(p.A.rp + r0 + lane);
+    if (lane <= uint32_t(R) && r0 + lane <= rows) rpv = ld_idx(p.A.rp + r0 + lane, p.A.pol);
     if (lane < uint32_t(R) && r0 + lane < rows) prv = p.prod[r0 + lane];
     uint64_t lo[R];
     uint32_t na[R], nnz[R], smin[R], smax[R], stouch[R];

@@ -40,8 +40,8 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
     kk[i] = 0;
     av[i] = 0.0;
     if (on[i] && lane < na[i]) {
-      kk[i] = ld_idx(A.ci + lo[i] + lane);
-      av[i] = ld_val(A.v + lo[i] + lane);
+      kk[i] = ld_idx(A.ci + lo[i] + lane, A.pol);
+      av[i] = ld_val(A.v + lo[i] + lane, A.pol);
     }
   }
   uint64_t bs[R];
@@ -51,8 +51,8 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
     bs[i] = 0;
     len[i] = 0;
     if (on[i] && lane < na[i]) {
-      bs[i] = ld_idx(B.rp + kk[i]);
-      len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1) - bs[i]);
+      bs[i] = ld_idx(B.rp + kk[i], B.pol);
+      len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1, B.pol) - bs[i]);
     }
   }
   // widest A row of the tile bounds the scan and search depth (warp-uniform)
@@ -101,8 +101,8 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
     col[i] = 0;
     p[i] = a;
     if (lane < tot[i]) {
-      col[i] = uint32_t(ld_idx(B.ci + bsrc + j));
-      p[i] = ld_val(B.v + bsrc + j);  // multiplied below, after the loads are in flight
+      col[i] = uint32_t(ld_idx(B.ci + bsrc + j, B.pol));
+      p[i] = ld_val(B.v + bsrc + j, B.pol);  // multiplied below, after the loads are in flight
     }
   }
   K key[R];
@@ -369,8 +369,8 @@ __device__ __forceinline__ Chunk make_chunk(const DevCsr& B, const Group& g, uin
     const uint64_t bsrc = __shfl_sync(kFull, g.bs, i & 31u) + off;
     c.a = __shfl_sync(kFull, g.av, i & 31u);
     if (lane < c.n) {
-      c.col = ld_idx(B.ci + bsrc + lane);
-      c.bv = ld_val(B.v + bsrc + lane);
+      c.col = ld_idx(B.ci + bsrc + lane, B.pol);
+      c.bv = ld_val(B.v + bsrc + lane, B.pol);
     }
     off += c.n;
     if (off >= li) {
@@ -400,8 +400,8 @@ __device__ __forceinline__ Chunk make_chunk(const DevCsr& B, const Group& g, uin
   c.a = __shfl_sync(kFull, g.av, e);
   const uint32_t j = q - __shfl_sync(kFull, g.excl, e);
   if (lane < c.n) {
-    c.col = ld_idx(B.ci + bsrc + j);
-    c.bv = ld_val(B.v + bsrc + j);
+    c.col = ld_idx(B.ci + bsrc + j, B.pol);
+    c.bv = ld_val(B.v + bsrc + j, B.pol);
   }
   c.i_next = last + 1;
   c.off_next = 0;
@@ -450,10 +450,10 @@ __device__ __forceinline__ bool medium_accumulate(const DevCsr& A, const DevCsr&
     g.bs = 0;
     g.av = 0.0;
     if (lane < g.nent) {
-      const uint64_t k = ld_idx(A.ci + e);
-      g.av = ld_val(A.v + e);
-      g.bs = ld_idx(B.rp + k);
-      g.len = uint32_t(ld_idx(B.rp + k + 1) - g.bs);
+      const uint64_t k = ld_idx(A.ci + e, A.pol);
+      g.av = ld_val(A.v + e, A.pol);
+      g.bs = ld_idx(B.rp + k, B.pol);
+      g.len = uint32_t(ld_idx(B.rp + k + 1, B.pol) - g.bs);
     }
     g.incl = warp_incl_scan(g.len);
     g.excl = g.incl - g.len;

@@ -435,6 +435,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.c_v = p->v;
     fp.ntiles = ntiles;
     fp.medium_limit = medium_limit;
+    fp.a_is_b = (A.ci == B.ci && A.v == B.v) ? 1u : 0u;
     fp.g_keys = nullptr;
     fp.g_vals = nullptr;
     fp.g_scol = nullptr;
