@@ -32,27 +32,30 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
                                            uint32_t (&nnz)[R], uint32_t (&smin)[R],
                                            uint32_t (&smax)[R], uint32_t (&stouch)[R]) {
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  // narrow variant: every index and offset fits 32 bits (checked on the host)
+  using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
   const uint32_t lane = lane_id();
-  uint64_t kk[R];
+  Off kk[R];
   double av[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     kk[i] = 0;
     av[i] = 0.0;
     if (on[i] && lane < na[i]) {
-      kk[i] = ld_idx(A.ci + lo[i] + lane, A.pol);
+      kk[i] = Off(ld_idx(A.ci + lo[i] + lane, A.pol));
       av[i] = ld_val(A.v + lo[i] + lane, A.pol);
     }
   }
-  uint64_t bs[R];
+  Off bs[R];
   uint32_t len[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     bs[i] = 0;
     len[i] = 0;
     if (on[i] && lane < na[i]) {
-      bs[i] = ld_idx(B.rp + kk[i], B.pol);
-      len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1, B.pol) - bs[i]);
+      const uint64_t b0 = ld_idx(B.rp + kk[i], B.pol);
+      bs[i] = Off(b0);
+      len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1, B.pol) - b0);
     }
   }
   // widest A row of the tile bounds the scan and search depth (warp-uniform)
@@ -95,14 +98,13 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
   double p[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const uint64_t bsrc = __shfl_sync(kFull, bs[i], src[i]);
+    const Off bsrc = __shfl_sync(kFull, bs[i], src[i]) + (lane - __shfl_sync(kFull, excl[i], src[i]));
     const double a = __shfl_sync(kFull, av[i], src[i]);
-    const uint32_t j = lane - __shfl_sync(kFull, excl[i], src[i]);
     col[i] = 0;
     p[i] = a;
     if (lane < tot[i]) {
-      col[i] = uint32_t(ld_idx(B.ci + bsrc + j, B.pol));
-      p[i] = ld_val(B.v + bsrc + j, B.pol);  // multiplied below, after the loads are in flight
+      col[i] = uint32_t(ld_idx(B.ci + bsrc, B.pol));
+      p[i] = ld_val(B.v + bsrc, B.pol);  // multiplied below, after the loads are in flight
     }
   }
   K key[R];

@@ -341,7 +341,9 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   const bool medium = need_table;
   const uint32_t medium_limit = medium ? kMediumLimit : 0u;
   const int pos_bits = medium ? kPosBits : 5;
-  const bool wide = B.cols > (1ull << (32 - pos_bits));
+  // narrow (32-bit keys and offsets) unless columns, entries or rows outgrow it
+  const bool wide = B.cols > (1ull << (32 - pos_bits)) || B.nnz >= (1ull << 32) ||
+                    A.nnz >= (1ull << 32) || B.rows >= (1ull << 32);
   const int rows_per_tile = medium ? 1 : kShortRowsPerTile;
 
   auto* p = new (std::nothrow) spmmm_product;
