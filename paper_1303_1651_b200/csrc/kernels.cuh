@@ -147,91 +147,84 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(p.ticket, (unsigned long long)kBatch);
     base = __shfl_sync(kFull, base, 0);
-    if (base >= p.ntiles) break;
-    const int ncur = int(p.ntiles - base < uint64_t(kBatch) ? p.ntiles - base : kBatch);
+    const bool have = base < p.ntiles;  // else: only finish the last batch
+    const int ncur = have ? int(p.ntiles - base < uint64_t(kBatch) ? p.ntiles - base : kBatch) : 0;
 #pragma unroll 1
     for (int bj = 0; bj < ncur; ++bj) {
     const uint64_t tile = base + bj;
     const int buf = half * kBatch + bj;
     const uint64_t r0 = tile * R;
-    // ---- row bounds and classes of the tile ----
+    // ---- row bounds and classes of the tile: lane i owns row r0 + i ----
     uint64_t rpv = 0;
-    uint32_t prv = 0;
+    uint32_t my_cls = kRowZero, my_na = 0;
     if (lane <= uint32_t(R) && r0 + lane <= rows) rpv = ld_idx(p.A.rp + r0 + lane, p.A.pol);
-    if (lane < uint32_t(R) && r0 + lane < rows) prv = p.prod[r0 + lane];
-    uint64_t lo[R];
-    uint32_t na[R], nnz[R], smin[R], smax[R], stouch[R];
-    int cls[R];
-    bool on[R];
-    bool any_short = false;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      lo[i] = __shfl_sync(kFull, rpv, i);
-      const uint64_t hi = __shfl_sync(kFull, rpv, i + 1);
-      const uint32_t pr = __shfl_sync(kFull, prv, i);
-      cls[i] = (r0 + i < rows) ? classify(pr, hi - lo[i], p.medium_limit) : kRowZero;
-      na[i] = uint32_t(hi - lo[i]);
-      on[i] = cls[i] == kRowShort;
-      any_short |= on[i];
-      nnz[i] = 0;
-      smin[i] = kEmptyKey;
-      smax[i] = 0;
-      stouch[i] = 0;
+    const uint64_t rpn = __shfl_down_sync(kFull, rpv, 1);
+    if (lane < uint32_t(R) && r0 + lane < rows) {
+      my_na = uint32_t(rpn - rpv);
+      my_cls = uint32_t(classify(p.prod[r0 + lane], rpn - rpv, p.medium_limit));
     }
+    // per-row results, lane i = row i
+    uint32_t my_nnz = 0, my_min = kEmptyKey, my_max = 0, my_touch = 0;
     uint32_t staged = 0;
     bool global = false;
-    if (any_short) {
-      // rows go through short_rows in lockstep groups of kLock (register budget)
+    if (__ballot_sync(kFull, my_cls == kRowShort)) {
+      // short rows go through short_rows in lockstep groups of kLock; the
+      // groups run in a loop (one copy of the code: instruction cache)
       constexpr int kLock = R < 4 ? R : 4;
-#pragma unroll
+#pragma unroll 1
       for (int h = 0; h < R / kLock; ++h) {
         uint64_t hlo[kLock];
         uint32_t hna[kLock], hnnz[kLock], hmin[kLock], hmax[kLock], htouch[kLock];
         bool hon[kLock];
-        bool hany = false;
 #pragma unroll
         for (int i = 0; i < kLock; ++i) {
-          hlo[i] = lo[h * kLock + i];
-          hna[i] = na[h * kLock + i];
-          hon[i] = on[h * kLock + i];
-          hany |= hon[i];
+          hlo[i] = __shfl_sync(kFull, rpv, h * kLock + i);
+          hna[i] = __shfl_sync(kFull, my_na, h * kLock + i);
+          hon[i] = __shfl_sync(kFull, my_cls, h * kLock + i) == kRowShort;
         }
-        if (!hany) continue;
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < kLock; ++i) any |= hon[i];
+        if (!any) continue;
         ShortOut so[kLock];
         short_rows<kLock, WIDE, STATS>(p.A, p.B, hlo, hna, hon, so, hnnz, hmin, hmax, htouch);
 #pragma unroll
         for (int i = 0; i < kLock; ++i) {
-          const int r = h * kLock + i;
-          if (!on[r]) continue;
-          nnz[r] = hnnz[i];
-          if (STATS) {
-            smin[r] = hmin[i];
-            smax[r] = hmax[i];
-            stouch[r] = htouch[i];
+          if (!hon[i]) continue;
+          if (lane == uint32_t(h * kLock + i)) {
+            my_nnz = hnnz[i];
+            if (STATS) {
+              my_min = hmin[i];
+              my_max = hmax[i];
+              my_touch = htouch[i];
+            }
           }
           if (so[i].keep) {
             s_col[buf * kStage + staged + so[i].rank] = so[i].col;
             s_val[buf * kStage + staged + so[i].rank] = so[i].val;
           }
-          staged += nnz[r];
+          staged += hnnz[i];
         }
       }
     }
 
     // ---- medium / long row (R == 1 in the medium kernel) ----
     if constexpr (MEDIUM) {
-      if (cls[0] == kRowMedium) {
-        const uint64_t hi = lo[0] + na[0];
+      const int cls0 = int(__shfl_sync(kFull, my_cls, 0));
+      const uint64_t lo0 = __shfl_sync(kFull, rpv, 0);
+      uint32_t smin0 = kEmptyKey, smax0 = 0;
+      if (cls0 == kRowMedium) {
+        const uint64_t hi = __shfl_sync(kFull, rpn, 0);
         uint32_t touches = 0, cnt;
         bool use_gt = false;  // row overflowed the shared table
-        if (medium_accumulate<decltype(st), STATS>(p.A, p.B, lo[0], hi, st, kSmemSlots * 3 / 4,
+        if (medium_accumulate<decltype(st), STATS>(p.A, p.B, lo0, hi, st, kSmemSlots * 3 / 4,
                                                     touches)) {
-          cnt = st.template compact<STATS>(smin[0], smax[0]);
+          cnt = st.template compact<STATS>(smin0, smax0);
         } else {
           st.clear();
           touches = 0;
           use_gt = true;
-          medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo[0], hi, gt, kGlobalSlots, touches);
+          medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo0, hi, gt, kGlobalSlots, touches);
           cnt = 0;
         }
         if (use_gt) {
@@ -239,7 +232,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
           // then fetch each value from the (intact) table
           uint32_t* scol = g_scol + buf * kMediumLimit;
           double* sval = g_sval + buf * kMediumLimit;
-          cnt = gt.template gather_keys<STATS>(scol, smin[0], smax[0]);
+          cnt = gt.template gather_keys<STATS>(scol, smin0, smax0);
           sort_keys_global(scol, cnt);
           for (uint32_t t = lane; t < cnt; t += 32) __stcg(sval + t, gt.lookup(__ldcg(scol + t)));
           global = true;
@@ -272,33 +265,37 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
             }
           }
         }
-        nnz[0] = cnt;
         staged = cnt;
+        if (lane == 0) {
+          my_nnz = cnt;
+          my_min = smin0;
+          my_max = smax0;
+        }
         __syncwarp();
         if (use_gt) gt.clear();
         else st.clear();
         if (STATS) {
 #pragma unroll
           for (int d = 16; d > 0; d >>= 1) touches += __shfl_xor_sync(kFull, touches, d);
-          stouch[0] = touches;
+          if (lane == 0) my_touch = touches;
         }
-      } else if (cls[0] == kRowLong) {
-        nnz[0] = p.l_nnz[p.lmap[r0]];  // copied into place by k_copy_long
+      } else if (cls0 == kRowLong) {
+        if (lane == 0) my_nnz = p.l_nnz[p.lmap[r0]];  // copied into place by k_copy_long
       }
     }
 
     // ---- per-row stats, tile header, aggregate ----
-    uint64_t agg = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      agg += nnz[i];
-      if (lane == uint32_t(i)) s_hdr[buf * R + i] = nnz[i];
-      if (STATS && lane == 0 && r0 + i < rows && cls[i] != kRowLong) {
-        p.st_min[r0 + i] = smin[i];
-        p.st_max[r0 + i] = smax[i];
-        p.st_touch[r0 + i] = stouch[i];
+    if (lane < uint32_t(R)) {
+      s_hdr[buf * R + lane] = my_nnz;
+      if (STATS && r0 + lane < rows && my_cls != kRowLong) {
+        p.st_min[r0 + lane] = my_min;
+        p.st_max[r0 + lane] = my_max;
+        p.st_touch[r0 + lane] = my_touch;
       }
     }
+    uint64_t agg = my_nnz;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) agg += __shfl_xor_sync(kFull, agg, d);
     __syncwarp();
     publish_aggregate(p.lb, tile, agg);
 
@@ -313,11 +310,10 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
     // ---- finish the previous batch ----
 #pragma unroll 1
     for (int j = 0; j < nprev; ++j) finish((half ^ 1) * kBatch + j);
+    if (!have) break;
     nprev = ncur;
     half ^= 1;
   }
-#pragma unroll 1
-  for (int j = 0; j < nprev; ++j) finish((half ^ 1) * kBatch + j);
 }
 
 }  // namespace spmmm
