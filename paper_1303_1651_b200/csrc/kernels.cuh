@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
         if (uint32_t(j) <= lane) s += s_hdr[b * R + j];
       p.c_rp[r0 + lane + 1] = excl + s;
     }
-    if (global) {
+    if (MEDIUM && global) {
       for (uint32_t t = lane; t < staged; t += 32) {
         __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + excl + t,
                (unsigned long long)__ldcg(g_scol + b * kMediumLimit + t));
@@ -171,8 +171,10 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
       // short rows go through short_rows in lockstep groups of kLock; the
       // groups run in a loop (one copy of the code: instruction cache)
       constexpr int kLock = R < 4 ? R : 4;
+      int ngroups = R / kLock;
+      asm volatile("" : "+r"(ngroups));  // opaque: keep one copy of the group body
 #pragma unroll 1
-      for (int h = 0; h < R / kLock; ++h) {
+      for (int h = 0; h < ngroups; ++h) {
         uint64_t hlo[kLock];
         uint32_t hna[kLock], hnnz[kLock], hmin[kLock], hmax[kLock], htouch[kLock];
         bool hon[kLock];
