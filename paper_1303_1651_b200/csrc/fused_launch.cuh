@@ -10,6 +10,9 @@
 namespace spmmm {
 
 constexpr int kFusedWarps = 8;
+#ifndef SPMMM_SHORT_BLOCKS
+#define SPMMM_SHORT_BLOCKS 4  // resident blocks per SM the short variant is compiled for
+#endif
 #ifndef SPMMM_SHORT_ROWS
 #define SPMMM_SHORT_ROWS 8
 #endif

@@ -18,6 +18,10 @@
 
 #include "rows.cuh"
 
+#ifndef SPMMM_SHORT_BLOCKS
+#define SPMMM_SHORT_BLOCKS 4
+#endif
+
 namespace spmmm {
 
 struct FusedParams {
@@ -70,7 +74,7 @@ struct FusedSmem {
 };
 
 template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
-__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_fused(const FusedParams p_in) {
+__global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k_fused(const FusedParams p_in) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
@@ -170,7 +174,10 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : (R <= 2 ? 6 : 4)) k_f
     if (__ballot_sync(kFull, my_cls == kRowShort)) {
       // short rows go through short_rows in lockstep groups of kLock; the
       // groups run in a loop (one copy of the code: instruction cache)
-      constexpr int kLock = R < 4 ? R : 4;
+#ifndef SPMMM_LOCK
+#define SPMMM_LOCK 4
+#endif
+      constexpr int kLock = R < SPMMM_LOCK ? R : SPMMM_LOCK;
       int ngroups = R / kLock;
       asm volatile("" : "+r"(ngroups));  // opaque: keep one copy of the group body
 #pragma unroll 1
