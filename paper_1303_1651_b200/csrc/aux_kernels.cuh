@@ -15,22 +15,36 @@ enum Ctrl : int {
   kCtrlStageCursor = 5,
   kCtrlTicket = 6,    // k_fused's dynamic tile counter
   kCtrlFault = 7,     // k_fused watchdog report
-  kCtrlWords = 8
+  kCtrlNonShort = 8,  // rows that are not short (> 32 products or > 32 A entries)
+  kCtrlWords = 16
 };
 
 // ---------------------------------------------------------------------------
-// K1: per-row product counts. formats.py:276-289 per row.
+// K1: per-row product counts. formats.py:276-289 per row. A warp takes 32
+// consecutive rows (one per lane); rows with many A entries are summed by the
+// whole warp so a 4096-entry row does not stall its 31 neighbours.
 __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
                                                unsigned long long* __restrict__ ctrl) {
-  uint64_t tot = 0, mx = 0;
+  const uint32_t lane = lane_id();
+  uint64_t tot = 0, mx = 0, nonshort = 0;
   uint32_t need = 0, err = 0;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < A.rows; r += stride) {
-    const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
+  const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t gw = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr uint64_t kSerial = 64;  // rows up to this many entries: one thread
+  for (uint64_t base = gw * 32; base < A.rows; base += nwarps * 32) {
+    const uint64_t r = base + lane;
+    uint64_t lo = 0, hi = 0;
+    if (r < A.rows) {
+      lo = ld_idx(A.rp + r);
+      hi = ld_idx(A.rp + r + 1);
+      if (hi < lo || hi > A.nnz) {
+        err |= 1u;
+        hi = lo;
+      }
+    }
     uint64_t p = 0;
-    if (hi < lo || hi > A.nnz) {
-      err |= 1u;
-    } else {
+    const bool serial = hi - lo <= kSerial;
+    if (serial) {
       for (uint64_t e = lo; e < hi; ++e) {
         const uint64_t k = ld_idx(A.ci + e);
         if (k >= B.rows) { err |= 2u; continue; }
@@ -39,22 +53,46 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
         p += b1 - b0;
       }
     }
-    if (p > 0x7fffffffull) err |= 8u;
-    prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
-    tot += p;
-    mx = p > mx ? p : mx;
-    if (p > 32 || (p > 0 && hi - lo > 32)) need = 1;
+    // long A rows: the whole warp, one row at a time
+    uint32_t big = __ballot_sync(kFull, !serial);
+    while (big) {
+      const uint32_t src = __ffs(big) - 1;
+      big &= big - 1;
+      const uint64_t blo = __shfl_sync(kFull, lo, src), bhi = __shfl_sync(kFull, hi, src);
+      uint64_t s = 0;
+      for (uint64_t e = blo + lane; e < bhi; e += 32) {
+        const uint64_t k = ld_idx(A.ci + e);
+        if (k >= B.rows) { err |= 2u; continue; }
+        const uint64_t b0 = ld_idx(B.rp + k), b1 = ld_idx(B.rp + k + 1);
+        if (b1 < b0 || b1 > B.nnz) { err |= 4u; continue; }
+        s += b1 - b0;
+      }
+      s = warp_sum64(s);
+      if (lane == src) p = s;
+    }
+    if (r < A.rows) {
+      if (p > 0x7fffffffull) err |= 8u;
+      prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
+      tot += p;
+      mx = p > mx ? p : mx;
+      if (p > 32 || (p > 0 && hi - lo > 32)) {
+        need = 1;
+        ++nonshort;
+      }
+    }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     tot += __shfl_xor_sync(kFull, tot, d);
+    nonshort += __shfl_xor_sync(kFull, nonshort, d);
     const uint64_t o = __shfl_xor_sync(kFull, mx, d);
     mx = o > mx ? o : mx;
     need |= __shfl_xor_sync(kFull, need, d);
     err |= __shfl_xor_sync(kFull, err, d);
   }
-  if (lane_id() == 0) {
+  if (lane == 0) {
     if (tot) atomicAdd(ctrl + kCtrlTotal, (unsigned long long)tot);
+    if (nonshort) atomicAdd(ctrl + kCtrlNonShort, (unsigned long long)nonshort);
     if (mx) atomicMax(ctrl + kCtrlMaxProd, (unsigned long long)mx);
     if (need) atomicOr(ctrl + kCtrlNeedTable, 1ull);
     if (err) atomicOr(ctrl + kCtrlError, (unsigned long long)err);
@@ -120,6 +158,7 @@ struct LongParams {
   uint32_t* ws_bits;   // [grid][words]
   uint64_t ws_slots;   // power of two >= 2 * max products of a long row
   uint64_t ws_words;   // ceil(cols / 32)
+  uint32_t min_prod;   // listed rows with fewer products belong to k_rows
   uint32_t* st_min;
   uint32_t* st_max;
   uint32_t* st_touch;
@@ -179,8 +218,9 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
 
   for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
     const uint32_t r = p.list[li];
-    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
     const uint32_t prod = p.prod[r];
+    if (prod <= p.min_prod) continue;  // block-uniform
+    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
     uint32_t tsize = 64;
     while (uint64_t(tsize) < 2ull * prod && uint64_t(tsize) < p.ws_slots) tsize <<= 1;
     const uint32_t mask = tsize - 1;

@@ -128,7 +128,26 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
         if (uint32_t(j) <= lane) s += s_hdr[b * R + j];
       p.c_rp[r0 + lane + 1] = excl + s;
     }
-    if (MEDIUM && global) {
+    const uint32_t ext = MEDIUM ? 0u : s_meta32[2 * b + 1];  // short variant: external rows
+    if (!MEDIUM && ext) {
+      // the tile mixes staged short rows with rows computed before k_fused
+      // (copied into their slots by k_copy_long): place each short row alone
+      uint64_t dst = excl;
+      uint32_t src = 0;
+#pragma unroll 1
+      for (int j = 0; j < R; ++j) {
+        const uint32_t n = s_hdr[b * R + j];
+        if (!((ext >> j) & 1u)) {
+          for (uint32_t t = lane; t < n; t += 32) {
+            __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + dst + t,
+                   (unsigned long long)s_col[b * kStage + src + t]);
+            __stcs(p.c_v + dst + t, s_val[b * kStage + src + t]);
+          }
+          src += n;
+        }
+        dst += n;
+      }
+    } else if (MEDIUM && global) {
       for (uint32_t t = lane; t < staged; t += 32) {
         __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + excl + t,
                (unsigned long long)__ldcg(g_scol + b * kMediumLimit + t));
@@ -167,8 +186,11 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       my_na = uint32_t(rpn - rpv);
       my_cls = uint32_t(classify(p.prod[r0 + lane], rpn - rpv, p.medium_limit));
     }
-    // per-row results, lane i = row i
+    // per-row results, lane i = row i; rows computed before this kernel
+    // (long rows, and in split mode every non-short row) only report nnz
     uint32_t my_nnz = 0, my_min = kEmptyKey, my_max = 0, my_touch = 0;
+    if (!MEDIUM && my_cls == kRowLong) my_nnz = p.l_nnz[p.lmap[r0 + lane]];
+    const uint32_t ext_mask = MEDIUM ? 0u : __ballot_sync(kFull, my_cls == kRowLong);
     uint32_t staged = 0;
     bool global = false;
     if (__ballot_sync(kFull, my_cls == kRowShort)) {
@@ -312,7 +334,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       s_meta64[2 * buf] = tile;
       s_meta64[2 * buf + 1] = agg;
       s_meta32[2 * buf] = staged;
-      s_meta32[2 * buf + 1] = global ? 1u : 0u;
+      s_meta32[2 * buf + 1] = MEDIUM ? (global ? 1u : 0u) : ext_mask;
     }
     __syncwarp();
     }  // tiles of the batch
@@ -322,6 +344,112 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     if (!have) break;
     nprev = ncur;
     half ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_rows: split mode. When non-short rows are a minority and vary a lot in
+// cost (skewed matrices such as C5), inlining them in k_fused would make
+// every later tile wait on the slowest one in its look-back. Instead they are
+// computed here first — one warp per row (<= kMediumLimit products), the
+// medium path's shared table with the global overflow table — and staged with
+// their nnz; k_fused then treats them like long rows.
+struct RowsParams {
+  DevCsr A, B;
+  const uint32_t* prod;
+  const uint32_t* list;
+  const unsigned long long* n_list;
+  unsigned long long* cursor;  // staging allocator
+  uint64_t* l_off;
+  uint32_t* l_nnz;
+  uint64_t* l_ci;
+  double* l_v;
+  uint32_t* g_keys;  // per warp [kGlobalSlots] overflow table
+  double* g_vals;
+  uint32_t* g_scol;  // per warp [kMaxBufs * kMediumLimit] sort scratch
+  uint32_t* st_min;
+  uint32_t* st_max;
+  uint32_t* st_touch;
+};
+
+constexpr int kRowsWarps = 8;
+
+template <bool WIDE, bool STATS>
+__global__ void __launch_bounds__(kRowsWarps * 32, 4) k_rows(const RowsParams p_in) {
+  using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  constexpr int EMAX = kSmemSlots / 32;
+  __shared__ uint32_t s_keys[kRowsWarps][kSmemSlots];
+  __shared__ double s_vals[kRowsWarps][kSmemSlots];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint64_t gwarp = uint64_t(blockIdx.x) * kRowsWarps + warp;
+  const uint64_t nwarps = uint64_t(gridDim.x) * kRowsWarps;
+  RowsParams p = p_in;
+  p.B.pol = policy_evict_last();
+  p.A.pol = policy_evict_first();
+  Table<kSmemSlots, false> st{s_keys[warp], s_vals[warp]};
+  Table<kGlobalSlots, true> gt{p.g_keys + gwarp * kGlobalSlots, p.g_vals + gwarp * kGlobalSlots};
+  uint32_t* scratch = p.g_scol + gwarp * kMaxBufs * kMediumLimit;
+  st.clear();
+  const uint64_t n = *p.n_list;
+  for (uint64_t li = gwarp; li < n; li += nwarps) {
+    const uint32_t r = p.list[li];
+    if (p.prod[r] > kMediumLimit) continue;  // k_long's
+    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
+    uint32_t touches = 0, cnt = 0, smin = kEmptyKey, smax = 0;
+    unsigned long long off = 0;
+    if (medium_accumulate<decltype(st), STATS>(p.A, p.B, lo, hi, st, kSmemSlots * 3 / 4,
+                                                touches)) {
+      cnt = st.template compact<STATS>(smin, smax);
+      if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)cnt);
+      off = __shfl_sync(kFull, off, 0);
+      int E = 1;
+      while (uint32_t(E) * 32u < cnt) E <<= 1;
+      K mk[EMAX];
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e) {
+        const uint32_t idx = uint32_t(e) * 32u + lane;
+        mk[e] = (e < E && idx < cnt) ? ((K(st.ldk(idx)) << kPosBits) | K(idx)) : ~K(0);
+      }
+      bitonic_sort_dyn(mk, E);
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e) {
+        const uint32_t idx = uint32_t(e) * 32u + lane;
+        if (e < E && idx < cnt) {
+          p.l_ci[off + idx] = uint64_t(mk[e] >> kPosBits);
+          p.l_v[off + idx] = st.ldv(uint32_t(mk[e]) & uint32_t(kGlobalSlots - 1));
+        }
+      }
+      __syncwarp();
+      st.clear();
+    } else {
+      st.clear();
+      touches = 0;
+      medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo, hi, gt, kGlobalSlots, touches);
+      cnt = gt.template gather_keys<STATS>(scratch, smin, smax);
+      sort_keys_global(scratch, cnt);
+      if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)cnt);
+      off = __shfl_sync(kFull, off, 0);
+      for (uint32_t t = lane; t < cnt; t += 32) {
+        const uint32_t col = __ldcg(scratch + t);
+        p.l_ci[off + t] = col;
+        p.l_v[off + t] = gt.lookup(col);
+      }
+      __syncwarp();
+      gt.clear();
+    }
+    if (STATS) {
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) touches += __shfl_xor_sync(kFull, touches, d);
+    }
+    if (lane == 0) {
+      p.l_off[li] = off;
+      p.l_nnz[li] = cnt;
+      if (STATS) {
+        p.st_min[r] = smin;
+        p.st_max[r] = smax;
+        p.st_touch[r] = touches;
+      }
+    }
   }
 }
 

@@ -79,8 +79,9 @@ void release(DevBuf& b, cudaStream_t s) {
   b.cap = 0;
 }
 
-const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long"};
-constexpr int kNumKernels = 5;
+const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
+                                    "k_rows"};
+constexpr int kNumKernels = 6;
 
 }  // namespace
 
@@ -223,10 +224,41 @@ int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bo
   return SPMMM_OK;
 }
 
+// ---- per-warp global overflow tables and sort/staging scratch ------------------
+
+struct GtabView {
+  uint32_t* keys;
+  double* vals;
+  uint32_t* scol;
+  double* sval;
+};
+
+int ensure_gtab(spmmm_context* c, uint64_t warps, GtabView* v) {
+  const size_t per_warp = kGlobalSlots * (sizeof(uint32_t) + sizeof(double)) +
+                          kMaxBufs * kMediumLimit * (sizeof(uint32_t) + sizeof(double));
+  bool grown = false;
+  CUDA_TRY(ensure(c->gtab, warps * per_warp, c->stream, &grown));
+  if (grown || c->gtab_warps < warps) {
+    CUDA_TRY(cudaMemsetAsync(c->gtab.p, 0xff, c->gtab.cap, c->stream));  // keys empty
+    c->gtab_warps = c->gtab.cap / per_warp;
+  }
+  char* g = static_cast<char*>(c->gtab.p);
+  const uint64_t n = c->gtab_warps;
+  v->vals = reinterpret_cast<double*>(g);
+  v->sval = reinterpret_cast<double*>(g + n * kGlobalSlots * 8);
+  v->keys = reinterpret_cast<uint32_t*>(g + n * (kGlobalSlots + kMaxBufs * kMediumLimit) * 8);
+  v->scol = v->keys + n * kGlobalSlots;
+  return SPMMM_OK;
+}
+
 // ---- the long-row path ------------------------------------------------------
 
+// Rows computed before k_fused: the long rows (> kMediumLimit products, k_long)
+// and, in split mode, every other non-short row (k_rows). They are listed by
+// k_collect (rows of class long for `list_limit`), staged with their nnz, and
+// copied into place by k_copy_long after k_fused.
 int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_prod,
-             uint32_t medium_limit, uint64_t total, bool stats, spmmm_product* p,
+             uint32_t list_limit, bool split, uint64_t total, bool stats, spmmm_product* p,
              DevBuf& stage_ci, DevBuf& stage_v, Timer& tm) {
   const uint64_t rows = A.rows;
   CUDA_TRY(ensure(c->lmap, rows * sizeof(uint32_t), c->stream));
@@ -235,6 +267,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   CUDA_TRY(ensure(c->l_nnz, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
+  const bool any_long = max_prod > kMediumLimit;
   // workspace: one table (>= 2x the distinct columns a row can have) and one
   // column bitmap per resident block
   uint64_t distinct = std::min<uint64_t>(max_prod, std::max<uint64_t>(B.cols, 1));
@@ -245,7 +278,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   int grid = 2 * c->sms;
   const uint64_t budget = 8ull << 30;  // cap the workspace at 8 GiB
   while (grid > 1 && uint64_t(grid) * per_block > budget) grid /= 2;
-  if (slots != c->ws_slots || words != c->ws_words || grid != c->ws_grid) {
+  if (any_long && (slots != c->ws_slots || words != c->ws_words || grid != c->ws_grid)) {
     release(c->ws, c->stream);
     CUDA_TRY(ensure(c->ws, size_t(grid) * per_block, c->stream));
     char* base = static_cast<char*>(c->ws.p);
@@ -262,16 +295,53 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(1);
     k_collect<<<unsigned(blocks), 256, 0, c->stream>>>(
-        A, static_cast<const uint32_t*>(c->prod.p), medium_limit,
+        A, static_cast<const uint32_t*>(c->prod.p), list_limit,
         static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p),
         static_cast<unsigned long long*>(c->ctrl.p));
     CUDA_TRY(cudaGetLastError());
     tm.end(1);
     ++c->last_launches;
   }
+  if (split) {
+    const unsigned grid_rows = unsigned(c->sms) * 4;
+    GtabView gv;
+    int rc = ensure_gtab(c, uint64_t(grid_rows) * kRowsWarps, &gv);
+    if (rc) return rc;
+    RowsParams rp;
+    rp.A = A;
+    rp.B = B;
+    rp.prod = static_cast<const uint32_t*>(c->prod.p);
+    rp.list = static_cast<const uint32_t*>(c->list.p);
+    rp.n_list = static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlLongRows;
+    rp.cursor = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlStageCursor;
+    rp.l_off = static_cast<uint64_t*>(c->l_off.p);
+    rp.l_nnz = static_cast<uint32_t*>(c->l_nnz.p);
+    rp.l_ci = static_cast<uint64_t*>(stage_ci.p);
+    rp.l_v = static_cast<double*>(stage_v.p);
+    rp.g_keys = gv.keys;
+    rp.g_vals = gv.vals;
+    rp.g_scol = gv.scol;
+    rp.st_min = p->st;
+    rp.st_max = p->st ? p->st + rows : nullptr;
+    rp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+    const bool wide = B.cols > (1ull << (32 - kPosBits)) || B.nnz >= (1ull << 32);
+    tm.begin(5);
+    if (wide) {
+      if (stats) k_rows<true, true><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
+      else k_rows<true, false><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
+    } else {
+      if (stats) k_rows<false, true><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
+      else k_rows<false, false><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
+    }
+    CUDA_TRY(cudaGetLastError());
+    tm.end(5);
+    ++c->last_launches;
+  }
+  if (!any_long) return SPMMM_OK;
   LongParams lp;
   lp.A = A;
   lp.B = B;
+  lp.min_prod = kMediumLimit;
   lp.prod = static_cast<const uint32_t*>(c->prod.p);
   lp.list = static_cast<const uint32_t*>(c->list.p);
   lp.ctrl = static_cast<unsigned long long*>(c->ctrl.p);
@@ -338,7 +408,14 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
 
   // Medium kernel (per-warp tables) only when some row needs it; rows past
   // kMediumLimit products are computed by k_long before the fused pass.
-  const bool medium = need_table;
+  // Kernel shape. Without non-short rows: the short variant. When non-short
+  // rows are a minority (skewed matrices) they vary a lot in cost, so they are
+  // computed up front (split mode: k_rows / k_long) and the short variant
+  // runs with them as pre-computed rows. Otherwise (most rows medium, e.g.
+  // C4) medium rows are computed inline by the medium variant.
+  const uint64_t nonshort = c->h_ctrl[kCtrlNonShort];
+  const bool split = need_table && nonshort * 4 <= rows;
+  const bool medium = need_table && !split;
   const uint32_t medium_limit = medium ? kMediumLimit : 0u;
   const int pos_bits = medium ? kPosBits : 5;
   // narrow (32-bit keys and offsets) unless columns, entries or rows outgrow it
@@ -383,9 +460,9 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     release(stage_v, c->stream);
     return cleanup(code);
   };
-  const bool has_long = medium && max_prod > medium_limit;
+  const bool has_long = split || (medium && max_prod > medium_limit);
   if (rows && has_long) {
-    rc = run_long(c, A, B, max_prod, medium_limit, total, stats, p, stage_ci, stage_v, tm);
+    rc = run_long(c, A, B, max_prod, medium_limit, split, total, stats, p, stage_ci, stage_v, tm);
     if (rc) return fail_staged(rc);
   }
 
@@ -451,25 +528,13 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     const unsigned grid = unsigned(std::min<uint64_t>(
         (ntiles + kFusedWarps - 1) / kFusedWarps, uint64_t(occ) * uint64_t(c->sms)));
     if (medium) {
-      // per warp: an overflow table (all keys empty; each warp restores its
-      // own) and two staging buffers for overflowed rows
-      const uint64_t warps = uint64_t(grid) * kFusedWarps;
-      const size_t per_warp = kGlobalSlots * (sizeof(uint32_t) + sizeof(double)) +
-                              kMaxBufs * kMediumLimit * (sizeof(uint32_t) + sizeof(double));
-      bool g_grown = false;
-      e = ensure(c->gtab, warps * per_warp, c->stream, &g_grown);
-      if (e == cudaSuccess && (g_grown || c->gtab_warps < warps)) {
-        e = cudaMemsetAsync(c->gtab.p, 0xff, c->gtab.cap, c->stream);
-        c->gtab_warps = c->gtab.cap / per_warp;
-      }
-      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "overflow tables: %s",
-                                                    cudaGetErrorString(e)));
-      char* g = static_cast<char*>(c->gtab.p);
-      const uint64_t n = c->gtab_warps;
-      fp.g_vals = reinterpret_cast<double*>(g);
-      fp.g_sval = reinterpret_cast<double*>(g + n * kGlobalSlots * 8);
-      fp.g_keys = reinterpret_cast<uint32_t*>(g + n * (kGlobalSlots + kMaxBufs * kMediumLimit) * 8);
-      fp.g_scol = fp.g_keys + n * kGlobalSlots;
+      GtabView gv;
+      rc = ensure_gtab(c, uint64_t(grid) * kFusedWarps, &gv);
+      if (rc) return fail_staged(rc);
+      fp.g_keys = gv.keys;
+      fp.g_vals = gv.vals;
+      fp.g_scol = gv.scol;
+      fp.g_sval = gv.sval;
     }
     tm.begin(3);
     rc = fused_call(c, medium, 1, fp, wide, stats, grid, nullptr);
