@@ -202,11 +202,14 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* scratc
 template <bool STATS>
 __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
   constexpr int NT = kLongThreads;
+  constexpr int kDupSlots = 4 * NT;  // per-chunk duplicate detector
+  constexpr int kBatch = 8;          // bitmap words loaded per batch
   __shared__ uint32_t s_excl[NT + 1];
   __shared__ uint64_t s_bs[NT];
   __shared__ double s_av[NT];
   __shared__ uint32_t s_scan[NT / 32 + 1];
-  __shared__ uint32_t s_min, s_max, s_touch;
+  __shared__ uint32_t s_dup[kDupSlots];
+  __shared__ uint32_t s_min, s_max, s_touch, s_zero;
   __shared__ unsigned long long s_off;
 
   const uint32_t tid = threadIdx.x;
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
   uint32_t* owner = p.ws_owner + uint64_t(blockIdx.x) * p.ws_slots;
   uint32_t* bits = p.ws_bits + uint64_t(blockIdx.x) * p.ws_words;
   const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
+  for (uint32_t s = tid; s < uint32_t(kDupSlots); s += NT) s_dup[s] = kEmptyKey;
 
   for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
     const uint32_t r = p.list[li];
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
     uint32_t tsize = 64;
     while (uint64_t(tsize) < 2ull * prod && uint64_t(tsize) < p.ws_slots) tsize <<= 1;
     const uint32_t mask = tsize - 1;
-    if (tid == 0) { s_min = kEmptyKey; s_max = 0; s_touch = 0; }
+    if (tid == 0) { s_min = kEmptyKey; s_max = 0; s_touch = 0; s_zero = 0; }
     __syncthreads();
     uint32_t touches = 0;
     uint32_t seq_base = 0;
@@ -249,8 +253,9 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
       for (uint32_t cb = 0; cb < total; cb += NT) {
         const uint32_t q = cb + tid;
         const bool act = q < total;
-        uint32_t col = 0, slot = 0;
+        uint32_t col = 0, slot = 0, dslot = kEmptyKey;
         double pv = 0.0;
+        bool dup = false;
         if (act) {
           // largest i with s_excl[i] <= q
           int i = 0;
@@ -277,64 +282,88 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
             h = (h + 1) & mask;
           }
           slot = h;
+          // does another product of this chunk hit the same column?
+          uint32_t d = long_hash(col, kDupSlots - 1);
+          while (true) {
+            const uint32_t old = atomicCAS(s_dup + d, kEmptyKey, col);
+            if (old == kEmptyKey) { dslot = d; break; }  // ours to reset
+            if (old == col) { dup = true; break; }
+            d = (d + 1) & (kDupSlots - 1);
+          }
         }
-        const uint32_t seq = seq_base + q;
-        bool pending = act;
-        while (__syncthreads_or(pending)) {
-          if (pending) atomicMin(owner + slot, seq);
-          __syncthreads();
-          if (pending && atomicAdd(owner + slot, 0u) == seq) {
+        if (!__syncthreads_or(dup)) {
+          // all columns of the chunk distinct: every product adds directly
+          if (act) {
             const double cur = __ldcg(vals + slot);
             if (STATS && cur == 0.0) ++touches;
             __stcg(vals + slot, __dadd_rn(cur, pv));
-            atomicExch(owner + slot, kEmptyKey);
-            pending = false;
           }
-          __syncthreads();
+        } else {
+          // equal columns: rounds, lowest product index first (left fold order)
+          const uint32_t seq = seq_base + q;
+          bool pending = act;
+          while (__syncthreads_or(pending)) {
+            if (pending) atomicMin(owner + slot, seq);
+            __syncthreads();
+            if (pending && atomicAdd(owner + slot, 0u) == seq) {
+              const double cur = __ldcg(vals + slot);
+              if (STATS && cur == 0.0) ++touches;
+              __stcg(vals + slot, __dadd_rn(cur, pv));
+              atomicExch(owner + slot, kEmptyKey);
+              pending = false;
+            }
+            __syncthreads();
+          }
         }
+        // reset the duplicate detector for the next chunk (inserters only)
+        if (dslot != kEmptyKey) s_dup[dslot] = kEmptyKey;
+        __syncthreads();
       }
       seq_base += total;
       __syncthreads();
     }
-    // ---- ordered extraction over the bitmap, dropping exact zeros ----
+    // ---- ordered extraction over the bitmap ----
     const uint32_t cmin = s_min, cmax = s_max;
-    uint32_t nz_total = 0;
-    uint32_t mine = 0, w_begin = 0, w_end = 0;
+    uint32_t w_begin = 0, w_end = 0, mine = 0;
     if (cmin <= cmax) {
       const uint32_t w0 = cmin >> 5, w1 = cmax >> 5;
-      const uint32_t nw = w1 - w0 + 1;
-      const uint32_t per = (nw + NT - 1) / NT;
+      const uint32_t per = (w1 - w0 + 1 + NT - 1) / NT;
       w_begin = w0 + tid * per;
       w_end = w_begin + per;
       if (w_begin > w1 + 1) w_begin = w1 + 1;
       if (w_end > w1 + 1) w_end = w1 + 1;
-      for (uint32_t w = w_begin; w < w_end; ++w) {
-        uint32_t b = __ldcg(bits + w), nzb = 0;
+      for (uint32_t w = w_begin; w < w_end; w += kBatch) {
+        uint32_t wb[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) wb[j] = (w + j < w_end) ? __ldcg(bits + w + j) : 0u;
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) mine += __popc(wb[j]);
+      }
+    }
+    uint32_t n_out;
+    const uint32_t my_base = block_excl_scan<NT>(mine, s_scan, n_out);
+    if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out);
+    __syncthreads();
+    const uint64_t off = s_off;
+    uint64_t pos = off + my_base;
+    bool zero = false;
+    for (uint32_t w = w_begin; w < w_end; w += kBatch) {
+      uint32_t wb[kBatch];
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) wb[j] = (w + j < w_end) ? __ldcg(bits + w + j) : 0u;
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        uint32_t b = wb[j];
         while (b) {
           const uint32_t bit = __ffs(b) - 1;
           b &= b - 1;
-          const uint32_t col = (w << 5) | bit;
-          const uint32_t s = long_probe(keys, col, mask);
-          if (__ldcg(vals + s) != 0.0) nzb |= 1u << bit;
+          const uint32_t col = ((w + j) << 5) | bit;
+          const double v = __ldcg(vals + long_probe(keys, col, mask));
+          zero |= v == 0.0;
+          p.l_ci[pos] = col;
+          p.l_v[pos] = v;
+          ++pos;
         }
-        mine += __popc(nzb);
-        __stcg(bits + w, nzb);
-      }
-    }
-    const uint32_t my_base = block_excl_scan<NT>(mine, s_scan, nz_total);
-    if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)nz_total);
-    __syncthreads();
-    uint64_t pos = s_off + my_base;
-    for (uint32_t w = w_begin; w < w_end; ++w) {
-      uint32_t b = __ldcg(bits + w);
-      while (b) {
-        const uint32_t bit = __ffs(b) - 1;
-        b &= b - 1;
-        const uint32_t col = (w << 5) | bit;
-        const uint32_t s = long_probe(keys, col, mask);
-        p.l_ci[pos] = col;
-        p.l_v[pos] = __ldcg(vals + s);
-        ++pos;
       }
     }
     if (STATS) {
@@ -343,7 +372,31 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
       for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
       if (lane_id() == 0 && t) atomicAdd(&s_touch, t);
     }
-    __syncthreads();
+    uint32_t nz_total = n_out;
+    if (__syncthreads_or(zero)) {
+      // exact cancellations (kernels.py:296-298 drops them): compact in place
+      uint32_t out = 0;
+      for (uint32_t c0 = 0; c0 < n_out; c0 += NT) {
+        const uint32_t i = c0 + tid;
+        uint64_t ci = 0;
+        double v = 0.0;
+        bool keep = false;
+        if (i < n_out) {
+          ci = p.l_ci[off + i];
+          v = p.l_v[off + i];
+          keep = v != 0.0;
+        }
+        uint32_t kept;
+        const uint32_t ex = block_excl_scan<NT>(keep ? 1u : 0u, s_scan, kept);
+        if (keep) {
+          p.l_ci[off + out + ex] = ci;
+          p.l_v[off + out + ex] = v;
+        }
+        out += kept;
+        __syncthreads();
+      }
+      nz_total = out;
+    }
     // restore the workspace for the next row
     for (uint32_t s = tid; s < tsize; s += NT) {
       __stcg(keys + s, kEmptyKey);
@@ -352,7 +405,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
     if (cmin <= cmax)
       for (uint32_t w = (cmin >> 5) + tid; w <= (cmax >> 5); w += NT) __stcg(bits + w, 0u);
     if (tid == 0) {
-      p.l_off[li] = s_off;
+      p.l_off[li] = off;
       p.l_nnz[li] = nz_total;
       if (STATS) {
         p.st_min[r] = cmin;
@@ -363,6 +416,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
     __syncthreads();
   }
 }
+
 
 // Long rows: staged by k_long, placed at their final offsets after k_fused.
 __global__ void __launch_bounds__(256) k_copy_long(const uint32_t* __restrict__ list,
