@@ -16,6 +16,9 @@ enum Ctrl : int {
   kCtrlTicket = 6,    // k_fused's dynamic tile counter
   kCtrlFault = 7,     // k_fused watchdog report
   kCtrlNonShort = 8,  // rows that are not short (> 32 products or > 32 A entries)
+  kCtrlLongTicket = 9,  // k_long's dynamic row counter
+  kCtrlRowsTicket = 10, // k_rows's dynamic row counter
+  kCtrlLongSmemTicket = 11, // k_long_smem's dynamic row counter
   kCtrlWords = 16
 };
 
@@ -155,9 +158,11 @@ struct LongParams {
   uint32_t* ws_keys;   // [grid][slots]
   double* ws_vals;     // [grid][slots]
   uint32_t* ws_owner;  // [grid][slots]
-  uint32_t* ws_bits;   // [grid][words]
+  uint32_t* ws_bits;   // [grid][words + swords]: column bitmap, then its summary
+                       // (bit w of the summary: bitmap word w is nonzero)
   uint64_t ws_slots;   // power of two >= 2 * max products of a long row
   uint64_t ws_words;   // ceil(cols / 32)
+  uint64_t ws_swords;  // ceil(ws_words / 32)
   uint32_t min_prod;   // listed rows with fewer products belong to k_rows
   uint32_t* st_min;
   uint32_t* st_max;
@@ -203,7 +208,6 @@ template <bool STATS>
 __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
   constexpr int NT = kLongThreads;
   constexpr int kDupSlots = 4 * NT;  // per-chunk duplicate detector
-  constexpr int kBatch = 8;          // bitmap words loaded per batch
   __shared__ uint32_t s_excl[NT + 1];
   __shared__ uint64_t s_bs[NT];
   __shared__ double s_av[NT];
@@ -216,11 +220,19 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
   uint32_t* keys = p.ws_keys + uint64_t(blockIdx.x) * p.ws_slots;
   double* vals = p.ws_vals + uint64_t(blockIdx.x) * p.ws_slots;
   uint32_t* owner = p.ws_owner + uint64_t(blockIdx.x) * p.ws_slots;
-  uint32_t* bits = p.ws_bits + uint64_t(blockIdx.x) * p.ws_words;
+  uint32_t* bits = p.ws_bits + uint64_t(blockIdx.x) * (p.ws_words + p.ws_swords);
+  uint32_t* sum = bits + p.ws_words;
   const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
   for (uint32_t s = tid; s < uint32_t(kDupSlots); s += NT) s_dup[s] = kEmptyKey;
 
-  for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
+  // rows are taken dynamically: their costs are heavy-tailed
+  __shared__ uint32_t s_li;
+  while (true) {
+    if (tid == 0) s_li = uint32_t(atomicAdd(p.ctrl + kCtrlLongTicket, 1ull));
+    __syncthreads();
+    const uint32_t li = s_li;
+    __syncthreads();
+    if (li >= n_long) break;
     const uint32_t r = p.list[li];
     const uint32_t prod = p.prod[r];
     if (prod <= p.min_prod) continue;  // block-uniform
@@ -272,7 +284,8 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
             if (k == kEmptyKey) {
               const uint32_t old = atomicCAS(keys + h, kEmptyKey, col);
               if (old == kEmptyKey) {
-                atomicOr(bits + (col >> 5), 1u << (col & 31));
+                if (!(atomicOr(bits + (col >> 5), 1u << (col & 31))))
+                  atomicOr(sum + (col >> 10), 1u << ((col >> 5) & 31));  // word became nonzero
                 atomicMin(&s_min, col);
                 atomicMax(&s_max, col);
                 break;
@@ -322,22 +335,23 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
       seq_base += total;
       __syncthreads();
     }
-    // ---- ordered extraction over the bitmap ----
+    // ---- ordered extraction: summary words -> nonzero bitmap words -> bits ----
     const uint32_t cmin = s_min, cmax = s_max;
-    uint32_t w_begin = 0, w_end = 0, mine = 0;
+    uint32_t s_begin = 0, s_end = 0, mine = 0;
     if (cmin <= cmax) {
-      const uint32_t w0 = cmin >> 5, w1 = cmax >> 5;
-      const uint32_t per = (w1 - w0 + 1 + NT - 1) / NT;
-      w_begin = w0 + tid * per;
-      w_end = w_begin + per;
-      if (w_begin > w1 + 1) w_begin = w1 + 1;
-      if (w_end > w1 + 1) w_end = w1 + 1;
-      for (uint32_t w = w_begin; w < w_end; w += kBatch) {
-        uint32_t wb[kBatch];
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) wb[j] = (w + j < w_end) ? __ldcg(bits + w + j) : 0u;
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) mine += __popc(wb[j]);
+      const uint32_t s0 = cmin >> 10, s1 = cmax >> 10;
+      const uint32_t per = (s1 - s0 + 1 + NT - 1) / NT;
+      s_begin = s0 + tid * per;
+      s_end = s_begin + per;
+      if (s_begin > s1 + 1) s_begin = s1 + 1;
+      if (s_end > s1 + 1) s_end = s1 + 1;
+      for (uint32_t sw = s_begin; sw < s_end; ++sw) {
+        uint32_t sb = __ldcg(sum + sw);
+        while (sb) {
+          const uint32_t j = __ffs(sb) - 1;
+          sb &= sb - 1;
+          mine += __popc(__ldcg(bits + ((sw << 5) | j)));
+        }
       }
     }
     uint32_t n_out;
@@ -347,17 +361,18 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
     const uint64_t off = s_off;
     uint64_t pos = off + my_base;
     bool zero = false;
-    for (uint32_t w = w_begin; w < w_end; w += kBatch) {
-      uint32_t wb[kBatch];
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j) wb[j] = (w + j < w_end) ? __ldcg(bits + w + j) : 0u;
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
-        uint32_t b = wb[j];
+    for (uint32_t sw = s_begin; sw < s_end; ++sw) {
+      uint32_t sb = __ldcg(sum + sw);
+      while (sb) {
+        const uint32_t j = __ffs(sb) - 1;
+        sb &= sb - 1;
+        const uint32_t w = (sw << 5) | j;
+        uint32_t b = __ldcg(bits + w);
+        __stcg(bits + w, 0u);  // restore as we go (the bits are in registers)
         while (b) {
           const uint32_t bit = __ffs(b) - 1;
           b &= b - 1;
-          const uint32_t col = ((w + j) << 5) | bit;
+          const uint32_t col = (w << 5) | bit;
           const double v = __ldcg(vals + long_probe(keys, col, mask));
           zero |= v == 0.0;
           p.l_ci[pos] = col;
@@ -365,6 +380,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
           ++pos;
         }
       }
+      __stcg(sum + sw, 0u);
     }
     if (STATS) {
       uint32_t t = touches;
@@ -402,8 +418,6 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
       __stcg(keys + s, kEmptyKey);
       __stcg(vals + s, 0.0);
     }
-    if (cmin <= cmax)
-      for (uint32_t w = (cmin >> 5) + tid; w <= (cmax >> 5); w += NT) __stcg(bits + w, 0u);
     if (tid == 0) {
       p.l_off[li] = off;
       p.l_nnz[li] = nz_total;
@@ -437,6 +451,217 @@ __global__ void __launch_bounds__(256) k_copy_long(const uint32_t* __restrict__ 
       c_ci[dst + t] = l_ci[src + t];
       c_v[dst + t] = l_v[src + t];
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: long rows that fit shared memory (<= kLongSmemProducts products):
+// one 512-thread block per row, everything on chip.
+//  * accumulate: open-addressing table of up to kLongSmemSlots slots in shared
+//    memory (sized per row for <= 3/4 load); products in chunks of 512 in
+//    (k, j) order; equal columns inside a chunk are applied in rounds, lowest
+//    product index first, arbitrated by a small shared table (column, min
+//    index) — the reference's left fold per column (kernels.py:167-174);
+//  * extract: the row's table region is bitonic-sorted in shared memory by
+//    column (empty and exactly-zero slots sort last and are dropped,
+//    kernels.py:296-298), then written out coalesced.
+constexpr uint32_t kLongSmemSlots = 16384;
+constexpr uint32_t kLongSmemProducts = kLongSmemSlots * 3 / 4;
+constexpr int kLongDupSlots = 2048;
+
+__host__ __device__ constexpr size_t long_smem_bytes() {
+  return size_t(kLongSmemSlots) * (sizeof(uint32_t) + sizeof(double)) +
+         size_t(kLongDupSlots) * 2 * sizeof(uint32_t);
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
+  constexpr int NT = kLongThreads;
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* vals = reinterpret_cast<double*>(sm);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(sm + kLongSmemSlots * sizeof(double));
+  uint32_t* dkey = keys + kLongSmemSlots;
+  uint32_t* dmin = dkey + kLongDupSlots;
+  __shared__ uint32_t s_excl[NT + 1];
+  __shared__ uint64_t s_bs[NT];
+  __shared__ double s_av[NT];
+  __shared__ uint32_t s_scan[NT / 32 + 1];
+  __shared__ uint32_t s_li, s_min, s_max, s_touch;
+  __shared__ unsigned long long s_off;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t s = tid; s < kLongSmemSlots; s += NT) keys[s] = kEmptyKey;
+  for (uint32_t s = tid; s < uint32_t(kLongDupSlots); s += NT) {
+    dkey[s] = kEmptyKey;
+    dmin[s] = kEmptyKey;
+  }
+  const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
+  while (true) {
+    if (tid == 0) s_li = uint32_t(atomicAdd(p.ctrl + kCtrlLongSmemTicket, 1ull));
+    __syncthreads();
+    const uint32_t li = s_li;
+    if (li >= n_long) break;
+    const uint32_t r = p.list[li];
+    const uint32_t prod = p.prod[r];
+    if (prod <= p.min_prod || prod > kLongSmemProducts) {
+      __syncthreads();
+      continue;  // another kernel's row
+    }
+    uint32_t tsize = 64;
+    while (tsize * 3 < prod * 4) tsize <<= 1;  // load <= 3/4
+    const uint32_t mask = tsize - 1;
+    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
+    if (tid == 0) { s_min = kEmptyKey; s_max = 0; s_touch = 0; }
+    uint32_t touches = 0, seq_base = 0;
+    __syncthreads();
+    for (uint64_t abase = lo; abase < hi; abase += NT) {
+      const uint64_t e = abase + tid;
+      uint32_t len = 0;
+      uint64_t bs = 0;
+      double av = 0.0;
+      if (e < hi) {
+        const uint64_t k = ld_idx(p.A.ci + e);
+        av = ld_val(p.A.v + e);
+        bs = ld_idx(p.B.rp + k);
+        len = uint32_t(ld_idx(p.B.rp + k + 1) - bs);
+      }
+      uint32_t total;
+      const uint32_t ex = block_excl_scan<NT>(len, s_scan, total);
+      s_excl[tid] = ex;
+      s_bs[tid] = bs;
+      s_av[tid] = av;
+      if (tid == 0) s_excl[NT] = total;
+      __syncthreads();
+      for (uint32_t cb = 0; cb < total; cb += NT) {
+        const uint32_t q = cb + tid;
+        const bool act = q < total;
+        uint32_t col = 0, slot = 0, d = 0;
+        double pv = 0.0;
+        bool fresh = false, dup = false, dins = false;
+        if (act) {
+          int i = 0;
+#pragma unroll
+          for (int st = NT / 2; st > 0; st >>= 1)
+            if (s_excl[i + st] <= q) i += st;
+          const uint64_t src = s_bs[i] + (q - s_excl[i]);
+          col = uint32_t(ld_idx(p.B.ci + src));
+          pv = __dmul_rn(s_av[i], ld_val(p.B.v + src));
+          uint32_t h = long_hash(col, mask);
+          while (true) {
+            const uint32_t k = keys[h];
+            if (k == col) break;
+            if (k == kEmptyKey) {
+              const uint32_t old = atomicCAS(keys + h, kEmptyKey, col);
+              if (old == kEmptyKey) { fresh = true; break; }
+              if (old == col) break;
+            }
+            h = (h + 1) & mask;
+          }
+          slot = h;
+          d = long_hash(col, kLongDupSlots - 1);
+          while (true) {
+            const uint32_t old = atomicCAS(dkey + d, kEmptyKey, col);
+            if (old == kEmptyKey) { dins = true; break; }
+            if (old == col) { dup = true; break; }
+            d = (d + 1) & (kLongDupSlots - 1);
+          }
+          if (fresh) vals[slot] = 0.0;  // new column: dense[x] == 0.0
+        }
+        if (!__syncthreads_or(dup)) {
+          if (act) {
+            const double cur = vals[slot];
+            if (STATS && cur == 0.0) ++touches;
+            vals[slot] = __dadd_rn(cur, pv);
+          }
+        } else {
+          const uint32_t seq = seq_base + q;
+          bool pending = act;
+          while (__syncthreads_or(pending)) {
+            if (pending) atomicMin(dmin + d, seq);
+            __syncthreads();
+            if (pending && dmin[d] == seq) {
+              const double cur = vals[slot];
+              if (STATS && cur == 0.0) ++touches;
+              vals[slot] = __dadd_rn(cur, pv);
+              dmin[d] = kEmptyKey;
+              pending = false;
+            }
+            __syncthreads();
+          }
+        }
+        if (dins) dkey[d] = kEmptyKey;
+        __syncthreads();
+      }
+      seq_base += total;
+      __syncthreads();
+    }
+    // ---- sort the table region by column; empty / zero slots last ----
+    uint32_t mn = kEmptyKey, mx = 0, keep_cnt = 0;
+    for (uint32_t s = tid; s < tsize; s += NT) {
+      const uint32_t k = keys[s];
+      if (k != kEmptyKey) {
+        if (STATS) {
+          mn = k < mn ? k : mn;
+          mx = k > mx ? k : mx;
+        }
+        if (vals[s] != 0.0) ++keep_cnt;
+        else keys[s] = kEmptyKey;  // exact cancellation: dropped (sorts last)
+      }
+    }
+    uint32_t n_out;
+    block_excl_scan<NT>(keep_cnt, s_scan, n_out);
+    for (uint32_t k2 = 2; k2 <= tsize; k2 <<= 1) {
+      for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < tsize; i += NT) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint32_t ka = keys[i], kb = keys[ixj];
+            const bool up = (i & k2) == 0;
+            if ((ka > kb) == up) {
+              keys[i] = kb;
+              keys[ixj] = ka;
+              const double t = vals[i];
+              vals[i] = vals[ixj];
+              vals[ixj] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out);
+    if (STATS) {
+      uint32_t t = touches;
+#pragma unroll
+      for (int dd = 16; dd > 0; dd >>= 1) {
+        t += __shfl_xor_sync(kFull, t, dd);
+        const uint32_t a = __shfl_xor_sync(kFull, mn, dd), b = __shfl_xor_sync(kFull, mx, dd);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+      }
+      if (lane_id() == 0) {
+        if (t) atomicAdd(&s_touch, t);
+        atomicMin(&s_min, mn);
+        atomicMax(&s_max, mx);
+      }
+    }
+    __syncthreads();
+    const uint64_t off = s_off;
+    for (uint32_t t = tid; t < n_out; t += NT) {
+      p.l_ci[off + t] = keys[t];
+      p.l_v[off + t] = vals[t];
+    }
+    __syncthreads();
+    for (uint32_t s = tid; s < tsize; s += NT) keys[s] = kEmptyKey;
+    if (tid == 0) {
+      p.l_off[li] = off;
+      p.l_nnz[li] = n_out;
+      if (STATS) {
+        p.st_min[r] = s_min;
+        p.st_max[r] = s_max;
+        p.st_touch[r] = s_touch;
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -360,6 +360,7 @@ struct RowsParams {
   const uint32_t* list;
   const unsigned long long* n_list;
   unsigned long long* cursor;  // staging allocator
+  unsigned long long* ticket;  // dynamic row counter
   uint64_t* l_off;
   uint32_t* l_nnz;
   uint64_t* l_ci;
@@ -391,7 +392,12 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 4) k_rows(const RowsParams p_
   uint32_t* scratch = p.g_scol + gwarp * kMaxBufs * kMediumLimit;
   st.clear();
   const uint64_t n = *p.n_list;
-  for (uint64_t li = gwarp; li < n; li += nwarps) {
+  (void)nwarps;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.ticket, 1ull);
+    const uint64_t li = __shfl_sync(kFull, t, 0);
+    if (li >= n) break;
     const uint32_t r = p.list[li];
     if (p.prod[r] > kMediumLimit) continue;  // k_long's
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);

@@ -268,17 +268,19 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
   const bool any_long = max_prod > kMediumLimit;
+  const bool any_huge = max_prod > kLongSmemProducts;  // some row needs k_long
   // workspace: one table (>= 2x the distinct columns a row can have) and one
   // column bitmap per resident block
   uint64_t distinct = std::min<uint64_t>(max_prod, std::max<uint64_t>(B.cols, 1));
   uint64_t slots = 64;
   while (slots < 2 * distinct) slots <<= 1;
   const uint64_t words = std::max<uint64_t>((B.cols + 31) / 32, 1);
-  const uint64_t per_block = slots * (4 + 8 + 4) + words * 4;
+  const uint64_t swords = (words + 31) / 32;
+  const uint64_t per_block = slots * (4 + 8 + 4) + (words + swords) * 4;
   int grid = 2 * c->sms;
   const uint64_t budget = 8ull << 30;  // cap the workspace at 8 GiB
   while (grid > 1 && uint64_t(grid) * per_block > budget) grid /= 2;
-  if (any_long && (slots != c->ws_slots || words != c->ws_words || grid != c->ws_grid)) {
+  if (any_huge && (slots != c->ws_slots || words != c->ws_words || grid != c->ws_grid)) {
     release(c->ws, c->stream);
     CUDA_TRY(ensure(c->ws, size_t(grid) * per_block, c->stream));
     char* base = static_cast<char*>(c->ws.p);
@@ -286,7 +288,8 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     CUDA_TRY(cudaMemsetAsync(base, 0xff, n * 4, c->stream));                   // keys
     CUDA_TRY(cudaMemsetAsync(base + n * 4, 0, n * 8, c->stream));             // vals
     CUDA_TRY(cudaMemsetAsync(base + n * 12, 0xff, n * 4, c->stream));         // owner
-    CUDA_TRY(cudaMemsetAsync(base + n * 16, 0, size_t(grid) * words * 4, c->stream));  // bits
+    CUDA_TRY(cudaMemsetAsync(base + n * 16, 0, size_t(grid) * (words + swords) * 4,
+                             c->stream));  // bitmaps + summaries
     c->ws_slots = slots;
     c->ws_words = words;
     c->ws_grid = grid;
@@ -314,6 +317,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     rp.list = static_cast<const uint32_t*>(c->list.p);
     rp.n_list = static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlLongRows;
     rp.cursor = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlStageCursor;
+    rp.ticket = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlRowsTicket;
     rp.l_off = static_cast<uint64_t*>(c->l_off.p);
     rp.l_nnz = static_cast<uint32_t*>(c->l_nnz.p);
     rp.l_ci = static_cast<uint64_t*>(stage_ci.p);
@@ -357,15 +361,35 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   lp.ws_bits = reinterpret_cast<uint32_t*>(base + n * 16);
   lp.ws_slots = c->ws_slots;
   lp.ws_words = c->ws_words;
+  lp.ws_swords = (c->ws_words + 31) / 32;
   lp.st_min = p->st;
   lp.st_max = p->st ? p->st + rows : nullptr;
   lp.st_touch = p->st ? p->st + 2 * rows : nullptr;
   tm.begin(2);
-  if (stats) k_long<true><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
-  else k_long<false><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
-  CUDA_TRY(cudaGetLastError());
+  {
+    const size_t smem = long_smem_bytes();
+    // per device and cheap: set on every call
+    if (stats)
+      CUDA_TRY(cudaFuncSetAttribute(k_long_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)));
+    else
+      CUDA_TRY(cudaFuncSetAttribute(k_long_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)));
+    // rows of (kMediumLimit, kLongSmemProducts] products: on-chip tables
+    if (stats) k_long_smem<true><<<c->sms, kLongThreads, smem, c->stream>>>(lp);
+    else k_long_smem<false><<<c->sms, kLongThreads, smem, c->stream>>>(lp);
+    CUDA_TRY(cudaGetLastError());
+    ++c->last_launches;
+  }
+  if (any_huge) {
+    // rows past kLongSmemProducts: global-memory tables
+    lp.min_prod = kLongSmemProducts;
+    if (stats) k_long<true><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
+    else k_long<false><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
+    CUDA_TRY(cudaGetLastError());
+    ++c->last_launches;
+  }
   tm.end(2);
-  ++c->last_launches;
   return SPMMM_OK;
 }
 

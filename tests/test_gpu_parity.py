@@ -108,6 +108,9 @@ def _rand_csr(rng, rows, cols, per_row_max, values="uniform", min_len=0):
     (4, (60, 2000, 3000, 1500, 6)),      # long rows (k_long)
     (5, (500, 64, 64, 64, 64)),          # collision heavy, dense-ish
     (6, (1000, 3000, 5000, 45, 4)),      # A rows longer than 32, short B rows
+    (7, (40, 2000, 300, 300, 30)),       # on-chip long rows, few columns (dup rounds)
+    (8, (24, 3000, 60000, 2500, 14)),    # rows past the on-chip limit (global tables)
+    (9, (30, 2000, 400, 1500, 40)),      # global tables, heavy duplicates per chunk
 ])
 @pytest.mark.parametrize("values", ["uniform", "quantized"])
 def test_random_vs_oracle(seed, shape, values):
