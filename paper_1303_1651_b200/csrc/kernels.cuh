@@ -351,9 +351,15 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
 // k_rows: split mode. When non-short rows are a minority and vary a lot in
 // cost (skewed matrices such as C5), inlining them in k_fused would make
 // every later tile wait on the slowest one in its look-back. Instead they are
-// computed here first — one warp per row (<= kMediumLimit products), the
-// medium path's shared table with the global overflow table — and staged with
-// their nnz; k_fused then treats them like long rows.
+// computed here first — one warp per row of <= kRowsLimit products — and
+// staged with their nnz; k_fused then treats them like long rows.
+//
+// Per warp: an open-addressing table of kRowsSlots slots in shared memory,
+// used over a per-row power-of-two region sized for <= 3/4 load (so no
+// overflow path exists). After the row: the region's nonzero (column, value)
+// pairs are compacted to its front in place, bitonic-sorted there by column
+// with a loop (small code: I-cache pressure was this kernel's bound), and
+// written out coalesced.
 struct RowsParams {
   DevCsr A, B;
   const uint32_t* prod;
@@ -365,94 +371,149 @@ struct RowsParams {
   uint32_t* l_nnz;
   uint64_t* l_ci;
   double* l_v;
-  uint32_t* g_keys;  // per warp [kGlobalSlots] overflow table
-  double* g_vals;
-  uint32_t* g_scol;  // per warp [kMaxBufs * kMediumLimit] sort scratch
   uint32_t* st_min;
   uint32_t* st_max;
   uint32_t* st_touch;
 };
 
 constexpr int kRowsWarps = 8;
+constexpr uint32_t kRowsSlots = 1024;
+constexpr uint32_t kRowsLimit = kRowsSlots * 3 / 4;  // products; longer rows: k_long_smem
 
-template <bool WIDE, bool STATS>
-__global__ void __launch_bounds__(kRowsWarps * 32, 4) k_rows(const RowsParams p_in) {
-  using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
-  constexpr int EMAX = kSmemSlots / 32;
-  __shared__ uint32_t s_keys[kRowsWarps][kSmemSlots];
-  __shared__ double s_vals[kRowsWarps][kSmemSlots];
+__host__ __device__ constexpr size_t rows_smem_bytes() {
+  return size_t(kRowsWarps) * kRowsSlots * (sizeof(double) + sizeof(uint32_t));
+}
+
+// Table over a runtime power-of-two region (mask), for medium_accumulate.
+struct RegionTable {
+  uint32_t* keys;
+  double* vals;
+  uint32_t mask;
+  uint32_t shift;  // 32 - log2(region)
+  template <bool STATS>
+  __device__ __forceinline__ bool apply(uint32_t col, double p, uint32_t& touches) const {
+    volatile uint32_t* vk = keys;
+    volatile double* vv = vals;
+    uint32_t h = (col * 0x9E3779B1u) >> shift;
+    bool fresh = false;
+    while (true) {
+      const uint32_t k = vk[h];
+      if (k == col) break;
+      if (k == kEmptyKey) {
+        const uint32_t old = atomicCAS(keys + h, kEmptyKey, col);
+        if (old == kEmptyKey) { fresh = true; break; }
+        if (old == col) break;
+      }
+      h = (h + 1) & mask;
+    }
+    const double cur = fresh ? 0.0 : vv[h];  // fresh slot == dense[x] == 0.0
+    if (STATS && cur == 0.0) ++touches;
+    vv[h] = __dadd_rn(cur, p);
+    return fresh;
+  }
+};
+
+template <bool STATS>
+__global__ void __launch_bounds__(kRowsWarps * 32, 2) k_rows(const RowsParams p_in) {
+  extern __shared__ __align__(16) unsigned char rows_sm[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const uint64_t gwarp = uint64_t(blockIdx.x) * kRowsWarps + warp;
-  const uint64_t nwarps = uint64_t(gridDim.x) * kRowsWarps;
+  double* vals = reinterpret_cast<double*>(rows_sm) + warp * kRowsSlots;
+  uint32_t* keys =
+      reinterpret_cast<uint32_t*>(rows_sm + kRowsWarps * kRowsSlots * sizeof(double)) +
+      warp * kRowsSlots;
+  volatile uint32_t* vk = keys;
+  volatile double* vv = vals;
   RowsParams p = p_in;
   p.B.pol = policy_evict_last();
   p.A.pol = policy_evict_first();
-  Table<kSmemSlots, false> st{s_keys[warp], s_vals[warp]};
-  Table<kGlobalSlots, true> gt{p.g_keys + gwarp * kGlobalSlots, p.g_vals + gwarp * kGlobalSlots};
-  uint32_t* scratch = p.g_scol + gwarp * kMaxBufs * kMediumLimit;
-  st.clear();
+  for (uint32_t s = lane; s < kRowsSlots; s += 32) vk[s] = kEmptyKey;
+  __syncwarp();
   const uint64_t n = *p.n_list;
-  (void)nwarps;
+#pragma unroll 1
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(p.ticket, 1ull);
     const uint64_t li = __shfl_sync(kFull, t, 0);
     if (li >= n) break;
     const uint32_t r = p.list[li];
-    if (p.prod[r] > kMediumLimit) continue;  // k_long's
+    const uint32_t prod = p.prod[r];
+    if (prod > kRowsLimit) continue;  // k_long_smem / k_long
+    uint32_t lg = 6;
+    while ((1u << lg) * 3u < prod * 4u) ++lg;  // region: load <= 3/4
+    const uint32_t region = 1u << lg;
+    const RegionTable tab{keys, vals, region - 1, 32 - lg};
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
-    uint32_t touches = 0, cnt = 0, smin = kEmptyKey, smax = 0;
-    unsigned long long off = 0;
-    if (medium_accumulate<decltype(st), STATS>(p.A, p.B, lo, hi, st, kSmemSlots * 3 / 4,
-                                                touches)) {
-      cnt = st.template compact<STATS>(smin, smax);
-      if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)cnt);
-      off = __shfl_sync(kFull, off, 0);
-      int E = 1;
-      while (uint32_t(E) * 32u < cnt) E <<= 1;
-      K mk[EMAX];
-#pragma unroll
-      for (int e = 0; e < EMAX; ++e) {
-        const uint32_t idx = uint32_t(e) * 32u + lane;
-        mk[e] = (e < E && idx < cnt) ? ((K(st.ldk(idx)) << kPosBits) | K(idx)) : ~K(0);
+    uint32_t touches = 0;
+    medium_accumulate<RegionTable, STATS>(p.A, p.B, lo, hi, tab, region, touches);
+    // compact nonzero pairs to the front, in place (each 32-slot window is
+    // read completely before any lane writes; writes never pass the window)
+    uint32_t cnt = 0, mn = kEmptyKey, mx = 0;
+#pragma unroll 1
+    for (uint32_t s0 = 0; s0 < region; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      const uint32_t k = vk[s];
+      const double v = vv[s];
+      const bool occ = k != kEmptyKey;
+      const bool keep = occ && (v != 0.0);  // kernels.py:296 drops exact zeros
+      if (STATS && occ) {
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
       }
-      bitonic_sort_dyn(mk, E);
-#pragma unroll
-      for (int e = 0; e < EMAX; ++e) {
-        const uint32_t idx = uint32_t(e) * 32u + lane;
-        if (e < E && idx < cnt) {
-          p.l_ci[off + idx] = uint64_t(mk[e] >> kPosBits);
-          p.l_v[off + idx] = st.ldv(uint32_t(mk[e]) & uint32_t(kGlobalSlots - 1));
-        }
-      }
+      const uint32_t m = __ballot_sync(kFull, keep);
       __syncwarp();
-      st.clear();
-    } else {
-      st.clear();
-      touches = 0;
-      medium_accumulate<decltype(gt), STATS>(p.A, p.B, lo, hi, gt, kGlobalSlots, touches);
-      cnt = gt.template gather_keys<STATS>(scratch, smin, smax);
-      sort_keys_global(scratch, cnt);
-      if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)cnt);
-      off = __shfl_sync(kFull, off, 0);
-      for (uint32_t t = lane; t < cnt; t += 32) {
-        const uint32_t col = __ldcg(scratch + t);
-        p.l_ci[off + t] = col;
-        p.l_v[off + t] = gt.lookup(col);
-      }
+      vk[s] = kEmptyKey;
       __syncwarp();
-      gt.clear();
+      if (keep) {
+        const uint32_t pos = cnt + __popc(m & lanemask_lt());
+        vk[pos] = k;
+        vv[pos] = v;
+      }
+      cnt += __popc(m);
     }
+    __syncwarp();
+    // bitonic sort of the first pow2 >= cnt pairs (the rest are empty keys)
+    uint32_t np = 1;
+    while (np < cnt) np <<= 1;
+#pragma unroll 1
+    for (uint32_t k2 = 2; k2 <= np; k2 <<= 1) {
+#pragma unroll 1
+      for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+        for (uint32_t t2 = lane; t2 < (np >> 1); t2 += 32) {
+          const uint32_t i = 2 * t2 - (t2 & (j - 1));
+          const uint32_t ka = vk[i], kb = vk[i + j];
+          const bool up = (i & k2) == 0;
+          if ((ka > kb) == up) {
+            vk[i] = kb;
+            vk[i + j] = ka;
+            const double va = vv[i];
+            vv[i] = vv[i + j];
+            vv[i + j] = va;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)cnt);
+    off = __shfl_sync(kFull, off, 0);
+    for (uint32_t t2 = lane; t2 < cnt; t2 += 32) {
+      __stcs(p.l_ci + off + t2, uint64_t(vk[t2]));
+      __stcs(p.l_v + off + t2, vv[t2]);
+      vk[t2] = kEmptyKey;
+    }
+    __syncwarp();
     if (STATS) {
 #pragma unroll
       for (int d = 16; d > 0; d >>= 1) touches += __shfl_xor_sync(kFull, touches, d);
+      mn = __reduce_min_sync(kFull, mn);
+      mx = __reduce_max_sync(kFull, mx);
     }
     if (lane == 0) {
       p.l_off[li] = off;
       p.l_nnz[li] = cnt;
       if (STATS) {
-        p.st_min[r] = smin;
-        p.st_max[r] = smax;
+        p.st_min[r] = mn;
+        p.st_max[r] = mx;
         p.st_touch[r] = touches;
       }
     }

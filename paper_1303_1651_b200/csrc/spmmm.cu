@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -26,6 +28,19 @@
 using namespace spmmm;
 
 namespace {
+
+// SPMMM_TRACE=1: host-side phase timestamps of spmmm_multiply on stderr
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  Trace() : on(std::getenv("SPMMM_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) const {
+    if (!on) return;
+    const double us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[spmmm] %10.1f us  %s\n", us, what);
+  }
+};
 
 thread_local std::string g_error;
 
@@ -80,8 +95,8 @@ void release(DevBuf& b, cudaStream_t s) {
 }
 
 const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
-                                    "k_rows"};
-constexpr int kNumKernels = 6;
+                                    "k_rows", "k_long_smem"};
+constexpr int kNumKernels = 7;
 
 }  // namespace
 
@@ -99,6 +114,9 @@ struct spmmm_context {
   uint64_t status_cap_tiles = 0;
   uint64_t ws_slots = 0, ws_words = 0;
   int ws_grid = 0;
+  DevBuf stage_ci, stage_v;  // staged pre-computed rows (run_long -> k_copy_long)
+  bool long_smem_attr[2] = {false, false};  // k_long_smem opt-in smem set
+  bool rows_attr[2] = {false, false};       // k_rows opt-in smem set
   cudaEvent_t ev[2 * kNumKernels] = {};
   bool ev_used[kNumKernels] = {};
   double last_ms[kNumKernels] = {};
@@ -260,14 +278,16 @@ int ensure_gtab(spmmm_context* c, uint64_t warps, GtabView* v) {
 int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_prod,
              uint32_t list_limit, bool split, uint64_t total, bool stats, spmmm_product* p,
              DevBuf& stage_ci, DevBuf& stage_v, Timer& tm) {
+  const Trace tr;
   const uint64_t rows = A.rows;
   CUDA_TRY(ensure(c->lmap, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->list, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->l_off, rows * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(c->l_nnz, rows * sizeof(uint32_t), c->stream));
+  tr.mark("  run_long: lists");
   CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
-  const bool any_long = max_prod > kMediumLimit;
+  tr.mark("  run_long: buffers");
   const bool any_huge = max_prod > kLongSmemProducts;  // some row needs k_long
   // workspace: one table (>= 2x the distinct columns a row can have) and one
   // column bitmap per resident block
@@ -294,6 +314,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     c->ws_words = words;
     c->ws_grid = grid;
   }
+  tr.mark("  run_long: workspace");
   {
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(1);
@@ -306,10 +327,6 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     ++c->last_launches;
   }
   if (split) {
-    const unsigned grid_rows = unsigned(c->sms) * 4;
-    GtabView gv;
-    int rc = ensure_gtab(c, uint64_t(grid_rows) * kRowsWarps, &gv);
-    if (rc) return rc;
     RowsParams rp;
     rp.A = A;
     rp.B = B;
@@ -322,30 +339,35 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     rp.l_nnz = static_cast<uint32_t*>(c->l_nnz.p);
     rp.l_ci = static_cast<uint64_t*>(stage_ci.p);
     rp.l_v = static_cast<double*>(stage_v.p);
-    rp.g_keys = gv.keys;
-    rp.g_vals = gv.vals;
-    rp.g_scol = gv.scol;
     rp.st_min = p->st;
     rp.st_max = p->st ? p->st + rows : nullptr;
     rp.st_touch = p->st ? p->st + 2 * rows : nullptr;
-    const bool wide = B.cols > (1ull << (32 - kPosBits)) || B.nnz >= (1ull << 32);
-    tm.begin(5);
-    if (wide) {
-      if (stats) k_rows<true, true><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
-      else k_rows<true, false><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
-    } else {
-      if (stats) k_rows<false, true><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
-      else k_rows<false, false><<<grid_rows, kRowsWarps * 32, 0, c->stream>>>(rp);
+    const size_t smem = rows_smem_bytes();
+    if (!c->rows_attr[stats]) {  // once per context (device)
+      if (stats)
+        CUDA_TRY(cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
+      else
+        CUDA_TRY(cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
+      c->rows_attr[stats] = true;
     }
+    const unsigned grid_rows = unsigned(c->sms) * 2;
+    tm.begin(5);
+    if (stats) k_rows<true><<<grid_rows, kRowsWarps * 32, smem, c->stream>>>(rp);
+    else k_rows<false><<<grid_rows, kRowsWarps * 32, smem, c->stream>>>(rp);
     CUDA_TRY(cudaGetLastError());
     tm.end(5);
     ++c->last_launches;
+    tr.mark("  run_long: k_rows launched");
   }
-  if (!any_long) return SPMMM_OK;
+  // split mode: every row past kRowsLimit; else rows past kMediumLimit
+  const uint32_t long_min = split ? kRowsLimit : kMediumLimit;
+  if (max_prod <= long_min) return SPMMM_OK;
   LongParams lp;
   lp.A = A;
   lp.B = B;
-  lp.min_prod = kMediumLimit;
+  lp.min_prod = long_min;
   lp.prod = static_cast<const uint32_t*>(c->prod.p);
   lp.list = static_cast<const uint32_t*>(c->list.p);
   lp.ctrl = static_cast<unsigned long long*>(c->ctrl.p);
@@ -365,31 +387,35 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   lp.st_min = p->st;
   lp.st_max = p->st ? p->st + rows : nullptr;
   lp.st_touch = p->st ? p->st + 2 * rows : nullptr;
-  tm.begin(2);
   {
+    tm.begin(6);
     const size_t smem = long_smem_bytes();
-    // per device and cheap: set on every call
-    if (stats)
-      CUDA_TRY(cudaFuncSetAttribute(k_long_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(smem)));
-    else
-      CUDA_TRY(cudaFuncSetAttribute(k_long_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(smem)));
+    if (!c->long_smem_attr[stats]) {  // once per context (device)
+      if (stats)
+        CUDA_TRY(cudaFuncSetAttribute(k_long_smem<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      else
+        CUDA_TRY(cudaFuncSetAttribute(k_long_smem<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      c->long_smem_attr[stats] = true;
+    }
     // rows of (kMediumLimit, kLongSmemProducts] products: on-chip tables
     if (stats) k_long_smem<true><<<c->sms, kLongThreads, smem, c->stream>>>(lp);
     else k_long_smem<false><<<c->sms, kLongThreads, smem, c->stream>>>(lp);
     CUDA_TRY(cudaGetLastError());
+    tm.end(6);
     ++c->last_launches;
   }
   if (any_huge) {
+    tm.begin(2);
     // rows past kLongSmemProducts: global-memory tables
     lp.min_prod = kLongSmemProducts;
     if (stats) k_long<true><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
     else k_long<false><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
     CUDA_TRY(cudaGetLastError());
+    tm.end(2);
     ++c->last_launches;
   }
-  tm.end(2);
   return SPMMM_OK;
 }
 
@@ -424,8 +450,10 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   if (rc) return rc;
   const uint64_t rows = A.rows;
 
+  const Trace tr;
   rc = run_count(c, A, B, tm);
   if (rc) return rc;
+  tr.mark("count done (host has totals)");
   const uint64_t total = c->h_ctrl[kCtrlTotal];
   const uint64_t max_prod = c->h_ctrl[kCtrlMaxProd];
   const bool need_table = c->h_ctrl[kCtrlNeedTable] != 0;
@@ -477,17 +505,18 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
                         cudaGetErrorString(e)));
   e = cudaMemsetAsync(p->rp, 0, sizeof(uint64_t), c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+  tr.mark("C allocated");
 
-  DevBuf stage_ci, stage_v;
-  auto fail_staged = [&](int code) {
-    release(stage_ci, c->stream);
-    release(stage_v, c->stream);
-    return cleanup(code);
-  };
+  // staging of pre-computed rows: context buffers, grown on demand and kept
+  // (a per-call cudaMallocAsync of this size costs milliseconds of pool work)
+  DevBuf& stage_ci = c->stage_ci;
+  DevBuf& stage_v = c->stage_v;
+  auto fail_staged = [&](int code) { return cleanup(code); };
   const bool has_long = split || (medium && max_prod > medium_limit);
   if (rows && has_long) {
     rc = run_long(c, A, B, max_prod, medium_limit, split, total, stats, p, stage_ci, stage_v, tm);
     if (rc) return fail_staged(rc);
+    tr.mark("long rows launched");
   }
 
   if (rows) {
@@ -580,8 +609,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       ++c->last_launches;
     }
   }
-  release(stage_ci, c->stream);
-  release(stage_v, c->stream);
+  tr.mark("fused + copy launched");
   e = cudaMemcpyAsync(c->h_ctrl + kCtrlFault, static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault,
                       sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess)
@@ -595,6 +623,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
                         (f >> 48) & 0x7fff, f & ((1ull << 48) - 1)));
   }
   p->nnz = c->h_ctrl[kCtrlTotal];
+  tr.mark("done");
   if (tm.on) {
     for (int k = 0; k < kNumKernels; ++k) {
       if (!c->ev_used[k]) continue;
@@ -678,7 +707,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->gtab, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
+                    &c->ws, &c->gtab, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
     release(*b, c->stream);
   cudaStreamSynchronize(c->stream);
   for (int k = 0; k < 2 * kNumKernels; ++k)
