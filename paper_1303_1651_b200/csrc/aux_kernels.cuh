@@ -486,13 +486,17 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
   __shared__ uint64_t s_bs[NT];
   __shared__ double s_av[NT];
   __shared__ uint32_t s_scan[NT / 32 + 1];
-  __shared__ uint32_t s_li, s_min, s_max, s_touch;
+  __shared__ uint32_t s_li, s_min, s_max, s_touch, s_kmin, s_kmax;
   __shared__ unsigned long long s_off;
   const uint32_t tid = threadIdx.x;
   for (uint32_t s = tid; s < kLongSmemSlots; s += NT) keys[s] = kEmptyKey;
   for (uint32_t s = tid; s < uint32_t(kLongDupSlots); s += NT) {
     dkey[s] = kEmptyKey;
     dmin[s] = kEmptyKey;
+  }
+  if (tid == 0) {
+    s_kmin = kEmptyKey;
+    s_kmax = 0;
   }
   const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
   while (true) {
@@ -594,8 +598,9 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
       seq_base += total;
       __syncthreads();
     }
-    // ---- sort the table region by column; empty / zero slots last ----
-    uint32_t mn = kEmptyKey, mx = 0, keep_cnt = 0;
+    // ---- extract in column order ----
+    // P0: drop exact zeros (kernels.py:296-298); count and range of the rest
+    uint32_t mn = kEmptyKey, mx = 0, keep_cnt = 0, kmn = kEmptyKey, kmx = 0;
     for (uint32_t s = tid; s < tsize; s += NT) {
       const uint32_t k = keys[s];
       if (k != kEmptyKey) {
@@ -603,32 +608,144 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
           mn = k < mn ? k : mn;
           mx = k > mx ? k : mx;
         }
-        if (vals[s] != 0.0) ++keep_cnt;
-        else keys[s] = kEmptyKey;  // exact cancellation: dropped (sorts last)
+        if (vals[s] != 0.0) {
+          ++keep_cnt;
+          kmn = k < kmn ? k : kmn;
+          kmx = k > kmx ? k : kmx;
+        } else {
+          keys[s] = kEmptyKey;
+        }
       }
+    }
+    kmn = __reduce_min_sync(kFull, kmn);
+    kmx = __reduce_max_sync(kFull, kmx);
+    if (lane_id() == 0 && kmn != kEmptyKey) {
+      atomicMin(&s_kmin, kmn);
+      atomicMax(&s_kmax, kmx);
     }
     uint32_t n_out;
-    block_excl_scan<NT>(keep_cnt, s_scan, n_out);
-    for (uint32_t k2 = 2; k2 <= tsize; k2 <<= 1) {
-      for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = tid; i < tsize; i += NT) {
-          const uint32_t ixj = i ^ j;
-          if (ixj > i) {
-            const uint32_t ka = keys[i], kb = keys[ixj];
-            const bool up = (i & k2) == 0;
-            if ((ka > kb) == up) {
-              keys[i] = kb;
-              keys[ixj] = ka;
-              const double t = vals[i];
-              vals[i] = vals[ixj];
-              vals[ixj] = t;
-            }
+    block_excl_scan<NT>(keep_cnt, s_scan, n_out);  // (its barriers order the atomics)
+    // P1: bucket histogram. Buckets are column ranges (monotone), about 16
+    // columns each, so every bucket is a small independent sort.
+    uint32_t nb = 2;
+    while (nb * 16 < n_out && nb < uint32_t(kLongDupSlots) / 2) nb <<= 1;
+    const uint32_t kmin = s_kmin, range = s_kmax - kmin;
+    uint32_t sh = 0;
+    while ((range >> sh) >= nb) ++sh;
+    uint32_t* hist = dkey;  // the duplicate table is idle now
+    uint32_t* cursor = dmin;
+    if (n_out) {
+      for (uint32_t b = tid; b < nb; b += NT) hist[b] = 0;
+      __syncthreads();
+      for (uint32_t s = tid; s < tsize; s += NT) {
+        const uint32_t k = keys[s];
+        if (k != kEmptyKey) atomicAdd(hist + ((k - kmin) >> sh), 1u);
+      }
+      __syncthreads();
+      // exclusive bucket offsets (two buckets per thread; nb <= 2 * NT)
+      const uint32_t h0 = 2 * tid < nb ? hist[2 * tid] : 0u;
+      const uint32_t h1 = 2 * tid + 1 < nb ? hist[2 * tid + 1] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<NT>(h0 + h1, s_scan, tot);
+      if (2 * tid < nb) {
+        cursor[2 * tid] = ex;
+        cursor[2 * tid + 1] = ex + h0;
+      }
+      if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out);
+      __syncthreads();
+      const uint64_t off = s_off;
+      // P2: scatter into the staged row by bucket; clears the table
+      for (uint32_t s = tid; s < tsize; s += NT) {
+        const uint32_t k = keys[s];
+        if (k != kEmptyKey) {
+          const uint32_t pos = atomicAdd(cursor + ((k - kmin) >> sh), 1u);
+          __stcg(p.l_ci + off + pos, uint64_t(k));
+          __stcg(p.l_v + off + pos, vals[s]);
+          keys[s] = kEmptyKey;
+        }
+      }
+      __syncthreads();
+      // P3: one warp per bucket of <= 64: register bitonic sort in place
+      const uint32_t lane = lane_id(), warp = tid >> 5;
+      bool big = false;
+      for (uint32_t b = warp; b < nb; b += NT / 32) {
+        const uint32_t sz = hist[b];
+        if (sz == 0) continue;
+        if (sz > 64) {
+          big = true;
+          continue;
+        }
+        const uint64_t base = off + cursor[b] - sz;
+        unsigned long long key[2];
+        double v[2];
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const uint32_t idx = uint32_t(e2) * 32u + lane;
+          key[e2] = ~0ull;
+          v[e2] = 0.0;
+          if (idx < sz) {
+            key[e2] = (__ldcg(p.l_ci + base + idx) << 6) | idx;
+            v[e2] = __ldcg(p.l_v + base + idx);
           }
         }
-        __syncthreads();
+        bitonic_sort<2>(key);
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const uint32_t idx = uint32_t(e2) * 32u + lane;
+          const uint32_t pos = uint32_t(key[e2]) & 63u;
+          const double t0 = __shfl_sync(kFull, v[0], pos & 31u);
+          const double t1 = __shfl_sync(kFull, v[1], pos & 31u);
+          if (idx < sz) {
+            __stcg(p.l_ci + base + idx, key[e2] >> 6);
+            __stcg(p.l_v + base + idx, (pos >> 5) ? t1 : t0);
+          }
+        }
+      }
+      // P4 (clustered columns only): buckets past 64, sorted by the whole
+      // block in the idle table
+      if (__syncthreads_or(big)) {
+        for (uint32_t b = 0; b < nb; ++b) {
+          const uint32_t sz = hist[b];
+          if (sz <= 64) continue;
+          const uint64_t base = off + cursor[b] - sz;
+          uint32_t np = 1;
+          while (np < sz) np <<= 1;
+          for (uint32_t t = tid; t < np; t += NT) {
+            keys[t] = t < sz ? uint32_t(__ldcg(p.l_ci + base + t)) : kEmptyKey;
+            if (t < sz) vals[t] = __ldcg(p.l_v + base + t);
+          }
+          __syncthreads();
+          for (uint32_t k2 = 2; k2 <= np; k2 <<= 1) {
+            for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+              for (uint32_t t = tid; t < (np >> 1); t += NT) {
+                const uint32_t i = 2 * t - (t & (j - 1));
+                const uint32_t ka = keys[i], kb = keys[i + j];
+                if ((ka > kb) == ((i & k2) == 0)) {
+                  keys[i] = kb;
+                  keys[i + j] = ka;
+                  const double tv = vals[i];
+                  vals[i] = vals[i + j];
+                  vals[i + j] = tv;
+                }
+              }
+              __syncthreads();
+            }
+          }
+          for (uint32_t t = tid; t < sz; t += NT) {
+            __stcg(p.l_ci + base + t, uint64_t(keys[t]));
+            __stcg(p.l_v + base + t, vals[t]);
+          }
+          __syncthreads();
+          for (uint32_t t = tid; t < np; t += NT) keys[t] = kEmptyKey;
+          __syncthreads();
+        }
+      }
+      __syncthreads();
+      for (uint32_t b = tid; b < nb; b += NT) {
+        hist[b] = kEmptyKey;
+        cursor[b] = kEmptyKey;
       }
     }
-    if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out);
     if (STATS) {
       uint32_t t = touches;
 #pragma unroll
@@ -645,21 +762,16 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
       }
     }
     __syncthreads();
-    const uint64_t off = s_off;
-    for (uint32_t t = tid; t < n_out; t += NT) {
-      p.l_ci[off + t] = keys[t];
-      p.l_v[off + t] = vals[t];
-    }
-    __syncthreads();
-    for (uint32_t s = tid; s < tsize; s += NT) keys[s] = kEmptyKey;
     if (tid == 0) {
-      p.l_off[li] = off;
+      p.l_off[li] = n_out ? uint64_t(s_off) : 0ull;
       p.l_nnz[li] = n_out;
       if (STATS) {
         p.st_min[r] = s_min;
         p.st_max[r] = s_max;
         p.st_touch[r] = s_touch;
       }
+      s_kmin = kEmptyKey;
+      s_kmax = 0;
     }
     __syncthreads();
   }

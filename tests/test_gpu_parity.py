@@ -137,6 +137,42 @@ def test_wide_column_keys():
         assert_csr_bitwise_equal(c, _oracle_csr(a, b), f"cols={cols}")
 
 
+def _clustered_operands(rng, rows, inner, entries, blen, cols, far):
+    """A rows of `entries` entries over B rows whose columns crowd into
+    [0, 2*inner) except a few far columns: long rows whose output columns are
+    clustered inside a wide range (big column buckets in extraction)."""
+    a_rp = np.arange(rows + 1, dtype=np.uint64) * np.uint64(entries)
+    a_ci = np.concatenate([np.sort(rng.choice(inner, entries, replace=False))
+                           for _ in range(rows)]).astype(np.uint64)
+    a = CsrMatrix(rows, inner, a_rp, a_ci, rng.uniform(-1, 1, a_ci.size))
+    b_ci = []
+    for k in range(inner):
+        c = rng.choice(2 * inner, blen, replace=False)
+        if k % far == 0:
+            c[0] = cols - 1 - k
+        b_ci.append(np.sort(c))
+    b_rp = np.arange(inner + 1, dtype=np.uint64) * np.uint64(blen)
+    b = CsrMatrix(inner, cols, b_rp, np.concatenate(b_ci).astype(np.uint64),
+                  rng.uniform(-1, 1, inner * blen))
+    return a, b
+
+
+@pytest.mark.parametrize("rows,inner,entries,blen", [
+    (12, 3000, 1500, 4),     # on-chip long rows (k_long_smem), clustered buckets
+    (6, 6000, 4000, 5),      # rows past the on-chip limit
+    (40, 2000, 200, 3),      # warp rows (k_rows)
+])
+def test_long_rows_clustered_columns(rows, inner, entries, blen):
+    rng = np.random.default_rng(rows * 7 + blen)
+    a, b = _clustered_operands(rng, rows, inner, entries, blen, 5_000_000, 997)
+    stats = KernelStats()
+    c = multiply_rowmajor(a, b, StrategyKind.COMBINED, stats)
+    ref = oracle.multiply_rowmajor(a, b, row_choices=True)
+    assert_csr_bitwise_equal(c, CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx,
+                                          ref.values), "clustered")
+    assert np.array_equal(_choices_array(stats, rows), ref.row_choices)
+
+
 def test_row_block_views_concatenate_to_full_product():
     """Row blocks of A as zero-copy device views (row_ptr[0] != 0) multiply to
     the matching row blocks of C (kernels.py:323-329: rows are independent)."""
