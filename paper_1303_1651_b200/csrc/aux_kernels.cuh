@@ -1,6 +1,8 @@
 // Count, long-row-listing and long-row kernels (used only by spmmm.cu).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "device.cuh"
 
 namespace spmmm {
@@ -19,7 +21,11 @@ enum Ctrl : int {
   kCtrlLongTicket = 9,  // k_long's dynamic row counter
   kCtrlRowsTicket = 10, // k_rows's dynamic row counter
   kCtrlLongSmemTicket = 11, // k_long_smem's dynamic row counter
-  kCtrlWords = 16
+  kCtrlMidRows = 12,    // sub-list: rows for k_long_smem (one block per row)
+  kCtrlHugeRows = 13,   // sub-list: rows for the cluster variant (8 blocks per row)
+  kCtrlOvfRows = 14,    // sub-list: rows the cluster variant handed to k_long
+  kCtrlHugeTicket = 15, // cluster variant's dynamic row counter
+  kCtrlWords = 24
 };
 
 // ---------------------------------------------------------------------------
@@ -105,8 +111,11 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
 // ---------------------------------------------------------------------------
 // K2: list the long rows (warp-aggregated append; order is irrelevant).
 __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __restrict__ prod,
-                                                 uint32_t medium_limit, uint32_t* __restrict__ list,
+                                                 uint32_t medium_limit, uint32_t mid_min,
+                                                 uint32_t huge_min, uint32_t* __restrict__ list,
                                                  uint32_t* __restrict__ lmap,
+                                                 uint32_t* __restrict__ mid_list,
+                                                 uint32_t* __restrict__ huge_list,
                                                  unsigned long long* __restrict__ ctrl) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -115,9 +124,11 @@ __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __res
   for (uint64_t it = 0; it < span; ++it) {
     const uint64_t r = start + it * stride;
     bool is_long = false;
+    uint32_t pr = 0;
     if (r < A.rows) {
       const uint64_t na = ld_idx(A.rp + r + 1) - ld_idx(A.rp + r);
-      is_long = classify(prod[r], na, medium_limit) == kRowLong;
+      pr = prod[r];
+      is_long = classify(pr, na, medium_limit) == kRowLong;
     }
     const uint32_t m = __ballot_sync(kFull, is_long);
     if (!m) continue;
@@ -128,6 +139,9 @@ __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __res
       const uint32_t idx = base + __popc(m & lanemask_lt());
       list[idx] = uint32_t(r);
       lmap[r] = idx;
+      // rows per computing kernel (few: plain atomics)
+      if (pr > huge_min) huge_list[atomicAdd(ctrl + kCtrlHugeRows, 1ull)] = idx;
+      else if (pr > mid_min) mid_list[atomicAdd(ctrl + kCtrlMidRows, 1ull)] = idx;
     }
   }
 }
@@ -163,7 +177,10 @@ struct LongParams {
   uint64_t ws_slots;   // power of two >= 2 * max products of a long row
   uint64_t ws_words;   // ceil(cols / 32)
   uint64_t ws_swords;  // ceil(ws_words / 32)
-  uint32_t min_prod;   // listed rows with fewer products belong to k_rows
+  const uint32_t* sub;                // this kernel's rows, as indices into list
+  const unsigned long long* n_sub;    // their count
+  unsigned long long* ticket;         // dynamic row counter
+  uint32_t* ovf;                      // cluster variant: rows handed on to k_long
   uint32_t* st_min;
   uint32_t* st_max;
   uint32_t* st_touch;
@@ -222,20 +239,20 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
   uint32_t* owner = p.ws_owner + uint64_t(blockIdx.x) * p.ws_slots;
   uint32_t* bits = p.ws_bits + uint64_t(blockIdx.x) * (p.ws_words + p.ws_swords);
   uint32_t* sum = bits + p.ws_words;
-  const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
+  const uint32_t n_sub = uint32_t(*(volatile const unsigned long long*)p.n_sub);
   for (uint32_t s = tid; s < uint32_t(kDupSlots); s += NT) s_dup[s] = kEmptyKey;
 
   // rows are taken dynamically: their costs are heavy-tailed
   __shared__ uint32_t s_li;
   while (true) {
-    if (tid == 0) s_li = uint32_t(atomicAdd(p.ctrl + kCtrlLongTicket, 1ull));
+    if (tid == 0) s_li = uint32_t(atomicAdd(p.ticket, 1ull));
     __syncthreads();
-    const uint32_t li = s_li;
+    const uint32_t t = s_li;
     __syncthreads();
-    if (li >= n_long) break;
+    if (t >= n_sub) break;
+    const uint32_t li = p.sub[t];
     const uint32_t r = p.list[li];
     const uint32_t prod = p.prod[r];
-    if (prod <= p.min_prod) continue;  // block-uniform
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
     uint32_t tsize = 64;
     while (uint64_t(tsize) < 2ull * prod && uint64_t(tsize) < p.ws_slots) tsize <<= 1;
@@ -474,9 +491,30 @@ __host__ __device__ constexpr size_t long_smem_bytes() {
          size_t(kLongDupSlots) * 2 * sizeof(uint32_t);
 }
 
-template <bool STATS>
+// lower_bound of x in the sorted column run B.ci[lo, hi)
+__device__ __forceinline__ uint64_t col_lower_bound(const uint64_t* ci, uint64_t lo, uint64_t hi,
+                                                    uint64_t x) {
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (ld_idx(ci + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// PARTS == 1: one block per row of (min, kLongSmemProducts] products.
+// PARTS > 1: a thread-block cluster of PARTS blocks per longer row. Block i
+// owns the i-th of PARTS equal column ranges of the row: it walks the whole
+// A row but only the slice of each B row inside its range (binary search),
+// so every column still folds in k order on one block. Counts, offsets and
+// row stats are exchanged through distributed shared memory; the parts are
+// staged back to back in column order. A part whose distinct columns outgrow
+// the table hands the whole row to k_long (global tables).
+template <bool STATS, int PARTS>
 __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
+  namespace cg = cooperative_groups;
   constexpr int NT = kLongThreads;
+  constexpr uint32_t kCap = kLongSmemSlots * 7 / 8;  // PARTS > 1: inserts before hand-off
   extern __shared__ __align__(16) unsigned char sm[];
   double* vals = reinterpret_cast<double*>(sm);
   uint32_t* keys = reinterpret_cast<uint32_t*>(sm + kLongSmemSlots * sizeof(double));
@@ -486,9 +524,13 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
   __shared__ uint64_t s_bs[NT];
   __shared__ double s_av[NT];
   __shared__ uint32_t s_scan[NT / 32 + 1];
-  __shared__ uint32_t s_li, s_min, s_max, s_touch, s_kmin, s_kmax;
+  __shared__ uint32_t s_li, s_tk, s_min, s_max, s_touch, s_kmin, s_kmax, s_cmin, s_cmax;
+  __shared__ uint32_t s_x[2];  // PARTS > 1: this part's nnz, overflow flag
+  __shared__ uint32_t s_ins;
   __shared__ unsigned long long s_off;
   const uint32_t tid = threadIdx.x;
+  uint32_t rank = 0;
+  if constexpr (PARTS > 1) rank = cg::this_cluster().block_rank();
   for (uint32_t s = tid; s < kLongSmemSlots; s += NT) keys[s] = kEmptyKey;
   for (uint32_t s = tid; s < uint32_t(kLongDupSlots); s += NT) {
     dkey[s] = kEmptyKey;
@@ -497,27 +539,61 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
   if (tid == 0) {
     s_kmin = kEmptyKey;
     s_kmax = 0;
+    s_cmin = kEmptyKey;
+    s_cmax = 0;
   }
-  const uint32_t n_long = uint32_t(*(volatile unsigned long long*)(p.ctrl + kCtrlLongRows));
+  const uint32_t n_sub = uint32_t(*(volatile const unsigned long long*)p.n_sub);
   while (true) {
-    if (tid == 0) s_li = uint32_t(atomicAdd(p.ctrl + kCtrlLongSmemTicket, 1ull));
-    __syncthreads();
-    const uint32_t li = s_li;
-    if (li >= n_long) break;
+    if constexpr (PARTS == 1) {
+      if (tid == 0) s_li = uint32_t(atomicAdd(p.ticket, 1ull));
+      __syncthreads();
+    } else {
+      if (rank == 0 && tid == 0) s_tk = uint32_t(atomicAdd(p.ticket, 1ull));
+      cg::this_cluster().sync();
+      if (tid == 0) s_li = *cg::this_cluster().map_shared_rank(&s_tk, 0);
+      __syncthreads();
+    }
+    const uint32_t t_row = s_li;
+    if (t_row >= n_sub) break;
+    const uint32_t li = p.sub[t_row];
     const uint32_t r = p.list[li];
     const uint32_t prod = p.prod[r];
-    if (prod <= p.min_prod || prod > kLongSmemProducts) {
-      __syncthreads();
-      continue;  // another kernel's row
+    uint32_t tsize = kLongSmemSlots;
+    if constexpr (PARTS == 1) {
+      tsize = 64;
+      while (tsize * 3 < prod * 4) tsize <<= 1;  // load <= 3/4
     }
-    uint32_t tsize = 64;
-    while (tsize * 3 < prod * 4) tsize <<= 1;  // load <= 3/4
     const uint32_t mask = tsize - 1;
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
-    if (tid == 0) { s_min = kEmptyKey; s_max = 0; s_touch = 0; }
+    // PARTS > 1: this block's column range [clo, chi)
+    uint64_t clo = 0, chi = ~0ull;
+    if constexpr (PARTS > 1) {
+      uint32_t cmn = kEmptyKey, cmx = 0;
+      for (uint64_t e = lo + tid; e < hi; e += NT) {
+        const uint64_t k = ld_idx(p.A.ci + e);
+        const uint64_t bs = ld_idx(p.B.rp + k), be = ld_idx(p.B.rp + k + 1);
+        if (be > bs) {
+          const uint32_t c0 = uint32_t(ld_idx(p.B.ci + bs)), c1 = uint32_t(ld_idx(p.B.ci + be - 1));
+          cmn = c0 < cmn ? c0 : cmn;
+          cmx = c1 > cmx ? c1 : cmx;
+        }
+      }
+      cmn = __reduce_min_sync(kFull, cmn);
+      cmx = __reduce_max_sync(kFull, cmx);
+      if (lane_id() == 0) {
+        atomicMin(&s_cmin, cmn);
+        atomicMax(&s_cmax, cmx);
+      }
+      __syncthreads();
+      const uint64_t w = uint64_t(s_cmax - s_cmin) / PARTS + 1;
+      clo = s_cmin + rank * w;
+      chi = clo + w;
+    }
+    if (tid == 0) { s_min = kEmptyKey; s_max = 0; s_touch = 0; s_ins = 0; }
     uint32_t touches = 0, seq_base = 0;
+    bool over = false;
     __syncthreads();
-    for (uint64_t abase = lo; abase < hi; abase += NT) {
+    for (uint64_t abase = lo; abase < hi && !over; abase += NT) {
       const uint64_t e = abase + tid;
       uint32_t len = 0;
       uint64_t bs = 0;
@@ -526,7 +602,12 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
         const uint64_t k = ld_idx(p.A.ci + e);
         av = ld_val(p.A.v + e);
         bs = ld_idx(p.B.rp + k);
-        len = uint32_t(ld_idx(p.B.rp + k + 1) - bs);
+        uint64_t be = ld_idx(p.B.rp + k + 1);
+        if constexpr (PARTS > 1) {
+          bs = col_lower_bound(p.B.ci, bs, be, clo);
+          be = col_lower_bound(p.B.ci, bs, be, chi);
+        }
+        len = uint32_t(be - bs);
       }
       uint32_t total;
       const uint32_t ex = block_excl_scan<NT>(len, s_scan, total);
@@ -536,6 +617,13 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
       if (tid == 0) s_excl[NT] = total;
       __syncthreads();
       for (uint32_t cb = 0; cb < total; cb += NT) {
+        if constexpr (PARTS > 1) {
+          // room for a whole chunk of new columns, or hand the row on
+          if (s_ins + NT > kCap) {
+            over = true;
+            break;
+          }
+        }
         const uint32_t q = cb + tid;
         const bool act = q < total;
         uint32_t col = 0, slot = 0, d = 0;
@@ -569,6 +657,9 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
             d = (d + 1) & (kLongDupSlots - 1);
           }
           if (fresh) vals[slot] = 0.0;  // new column: dense[x] == 0.0
+        }
+        if constexpr (PARTS > 1) {
+          if (fresh) atomicAdd(&s_ins, 1u);  // read after the next barrier
         }
         if (!__syncthreads_or(dup)) {
           if (act) {
@@ -608,7 +699,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
           mn = k < mn ? k : mn;
           mx = k > mx ? k : mx;
         }
-        if (vals[s] != 0.0) {
+        if (vals[s] != 0.0 && !over) {
           ++keep_cnt;
           kmn = k < kmn ? k : kmn;
           kmx = k > kmx ? k : kmx;
@@ -623,8 +714,80 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
       atomicMin(&s_kmin, kmn);
       atomicMax(&s_kmax, kmx);
     }
+    if (STATS) {
+      uint32_t t = touches;
+#pragma unroll
+      for (int dd = 16; dd > 0; dd >>= 1) t += __shfl_xor_sync(kFull, t, dd);
+      mn = __reduce_min_sync(kFull, mn);
+      mx = __reduce_max_sync(kFull, mx);
+      if (lane_id() == 0) {
+        if (t) atomicAdd(&s_touch, t);
+        atomicMin(&s_min, mn);
+        atomicMax(&s_max, mx);
+      }
+    }
     uint32_t n_out;
     block_excl_scan<NT>(keep_cnt, s_scan, n_out);  // (its barriers order the atomics)
+    bool handed_on = false;
+    if constexpr (PARTS == 1) {
+      if (tid == 0) {
+        s_off = n_out ? atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out) : 0ull;
+        p.l_off[li] = s_off;
+        p.l_nnz[li] = n_out;
+        if (STATS) {
+          p.st_min[r] = s_min;
+          p.st_max[r] = s_max;
+          p.st_touch[r] = s_touch;
+        }
+      }
+      __syncthreads();
+    } else {
+      cg::cluster_group cluster = cg::this_cluster();
+      if (tid == 0) {  // (`over` is block-uniform)
+        s_x[0] = n_out;
+        s_x[1] = over ? 1u : 0u;
+      }
+      cluster.sync();  // (A) parts' counts, flags and stats are final
+      uint32_t prefix = 0, total = 0, any_over = 0;
+#pragma unroll
+      for (int j = 0; j < PARTS; ++j) {
+        const uint32_t* x = cluster.map_shared_rank(s_x, j);
+        const uint32_t nj = x[0];
+        any_over |= x[1];
+        prefix += uint32_t(j) < rank ? nj : 0u;
+        total += nj;
+      }
+      if (rank == 0 && tid == 0) {
+        if (any_over) {
+          p.ovf[atomicAdd(p.ctrl + kCtrlOvfRows, 1ull)] = li;
+        } else {
+          s_off = total ? atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)total) : 0ull;
+          p.l_off[li] = s_off;
+          p.l_nnz[li] = total;
+          if (STATS) {
+            uint32_t a0 = kEmptyKey, a1 = 0, a2 = 0;
+            for (int j = 0; j < PARTS; ++j) {
+              const uint32_t mj = *cluster.map_shared_rank(&s_min, j);
+              const uint32_t xj = *cluster.map_shared_rank(&s_max, j);
+              a0 = mj < a0 ? mj : a0;
+              a1 = xj > a1 ? xj : a1;
+              a2 += *cluster.map_shared_rank(&s_touch, j);
+            }
+            p.st_min[r] = a0;
+            p.st_max[r] = a1;
+            p.st_touch[r] = a2;
+          }
+        }
+      }
+      cluster.sync();  // (B) the row's staging offset is known
+      if (any_over) {
+        handed_on = true;
+        for (uint32_t s = tid; s < tsize; s += NT) keys[s] = kEmptyKey;
+      } else if (tid == 0) {
+        s_off = *cluster.map_shared_rank(&s_off, 0) + prefix;
+      }
+      __syncthreads();
+    }
     // P1: bucket histogram. Buckets are column ranges (monotone), about 16
     // columns each, so every bucket is a small independent sort.
     uint32_t nb = 2;
@@ -634,7 +797,8 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
     while ((range >> sh) >= nb) ++sh;
     uint32_t* hist = dkey;  // the duplicate table is idle now
     uint32_t* cursor = dmin;
-    if (n_out) {
+    if (n_out && !handed_on) {
+      const uint64_t off = s_off;
       for (uint32_t b = tid; b < nb; b += NT) hist[b] = 0;
       __syncthreads();
       for (uint32_t s = tid; s < tsize; s += NT) {
@@ -651,9 +815,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
         cursor[2 * tid] = ex;
         cursor[2 * tid + 1] = ex + h0;
       }
-      if (tid == 0) s_off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out);
       __syncthreads();
-      const uint64_t off = s_off;
       // P2: scatter into the staged row by bucket; clears the table
       for (uint32_t s = tid; s < tsize; s += NT) {
         const uint32_t k = keys[s];
@@ -746,35 +908,16 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
         cursor[b] = kEmptyKey;
       }
     }
-    if (STATS) {
-      uint32_t t = touches;
-#pragma unroll
-      for (int dd = 16; dd > 0; dd >>= 1) {
-        t += __shfl_xor_sync(kFull, t, dd);
-        const uint32_t a = __shfl_xor_sync(kFull, mn, dd), b = __shfl_xor_sync(kFull, mx, dd);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
-      }
-      if (lane_id() == 0) {
-        if (t) atomicAdd(&s_touch, t);
-        atomicMin(&s_min, mn);
-        atomicMax(&s_max, mx);
-      }
-    }
     __syncthreads();
     if (tid == 0) {
-      p.l_off[li] = n_out ? uint64_t(s_off) : 0ull;
-      p.l_nnz[li] = n_out;
-      if (STATS) {
-        p.st_min[r] = s_min;
-        p.st_max[r] = s_max;
-        p.st_touch[r] = s_touch;
-      }
       s_kmin = kEmptyKey;
       s_kmax = 0;
+      s_cmin = kEmptyKey;
+      s_cmax = 0;
     }
     __syncthreads();
   }
+  if constexpr (PARTS > 1) cg::this_cluster().sync();  // no block leaves while read remotely
 }
 
 }  // namespace spmmm

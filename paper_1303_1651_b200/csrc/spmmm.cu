@@ -95,8 +95,8 @@ void release(DevBuf& b, cudaStream_t s) {
 }
 
 const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
-                                    "k_rows", "k_long_smem"};
-constexpr int kNumKernels = 7;
+                                    "k_rows", "k_long_smem", "k_long_cluster"};
+constexpr int kNumKernels = 8;
 
 }  // namespace
 
@@ -117,6 +117,8 @@ struct spmmm_context {
   DevBuf stage_ci, stage_v;  // staged pre-computed rows (run_long -> k_copy_long)
   bool long_smem_attr[2] = {false, false};  // k_long_smem opt-in smem set
   bool rows_attr[2] = {false, false};       // k_rows opt-in smem set
+  int long_clusters = 0;                     // resident kLongParts-block clusters
+  DevBuf sub;                                // per-kernel row sub-lists
   cudaEvent_t ev[2 * kNumKernels] = {};
   bool ev_used[kNumKernels] = {};
   double last_ms[kNumKernels] = {};
@@ -271,6 +273,47 @@ int ensure_gtab(spmmm_context* c, uint64_t warps, GtabView* v) {
 
 // ---- the long-row path ------------------------------------------------------
 
+constexpr int kLongParts = 8;  // blocks per cluster for rows past kLongSmemProducts
+
+// k_long_smem, one block per row or (cluster) kLongParts blocks per row
+template <bool S>
+int launch_long_smem(spmmm_context* c, const LongParams& lp, bool cluster) {
+  const size_t smem = long_smem_bytes();
+  auto* k1 = k_long_smem<S, 1>;
+  auto* k8 = k_long_smem<S, kLongParts>;
+  if (!c->long_smem_attr[S]) {  // once per context (device)
+    CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CUDA_TRY(cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    c->long_smem_attr[S] = true;
+  }
+  if (!cluster) {
+    k1<<<c->sms, kLongThreads, smem, c->stream>>>(lp);
+    CUDA_TRY(cudaGetLastError());
+    return SPMMM_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kLongParts;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kLongThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (c->long_clusters <= 0) {
+    cfg.gridDim = dim3(kLongParts * 64);
+    int n = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, k8, &cfg));
+    if (n <= 0) return fail(SPMMM_ERR_UNSUPPORTED, "no %d-block cluster fits a GPC", kLongParts);
+    c->long_clusters = n;
+  }
+  cfg.gridDim = dim3(unsigned(kLongParts * c->long_clusters));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k8, lp));
+  return SPMMM_OK;
+}
+
 // Rows computed before k_fused: the long rows (> kMediumLimit products, k_long)
 // and, in split mode, every other non-short row (k_rows). They are listed by
 // k_collect (rows of class long for `list_limit`), staged with their nnz, and
@@ -284,6 +327,12 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   CUDA_TRY(ensure(c->list, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->l_off, rows * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(c->l_nnz, rows * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(c->sub, 3 * rows * sizeof(uint32_t), c->stream));
+  uint32_t* mid_list = static_cast<uint32_t*>(c->sub.p);
+  uint32_t* huge_list = mid_list + rows;
+  uint32_t* ovf_list = mid_list + 2 * rows;
+  // split mode: k_rows takes rows up to kRowsLimit; else k_fused up to kMediumLimit
+  const uint32_t long_min = split ? kRowsLimit : kMediumLimit;
   tr.mark("  run_long: lists");
   CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
@@ -319,8 +368,8 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(1);
     k_collect<<<unsigned(blocks), 256, 0, c->stream>>>(
-        A, static_cast<const uint32_t*>(c->prod.p), list_limit,
-        static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p),
+        A, static_cast<const uint32_t*>(c->prod.p), list_limit, long_min, kLongSmemProducts,
+        static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p), mid_list, huge_list,
         static_cast<unsigned long long*>(c->ctrl.p));
     CUDA_TRY(cudaGetLastError());
     tm.end(1);
@@ -361,13 +410,10 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     ++c->last_launches;
     tr.mark("  run_long: k_rows launched");
   }
-  // split mode: every row past kRowsLimit; else rows past kMediumLimit
-  const uint32_t long_min = split ? kRowsLimit : kMediumLimit;
   if (max_prod <= long_min) return SPMMM_OK;
   LongParams lp;
   lp.A = A;
   lp.B = B;
-  lp.min_prod = long_min;
   lp.prod = static_cast<const uint32_t*>(c->prod.p);
   lp.list = static_cast<const uint32_t*>(c->list.p);
   lp.ctrl = static_cast<unsigned long long*>(c->ctrl.p);
@@ -387,29 +433,32 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   lp.st_min = p->st;
   lp.st_max = p->st ? p->st + rows : nullptr;
   lp.st_touch = p->st ? p->st + 2 * rows : nullptr;
-  {
-    tm.begin(6);
-    const size_t smem = long_smem_bytes();
-    if (!c->long_smem_attr[stats]) {  // once per context (device)
-      if (stats)
-        CUDA_TRY(cudaFuncSetAttribute(k_long_smem<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      else
-        CUDA_TRY(cudaFuncSetAttribute(k_long_smem<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      c->long_smem_attr[stats] = true;
-    }
-    // rows of (kMediumLimit, kLongSmemProducts] products: on-chip tables
-    if (stats) k_long_smem<true><<<c->sms, kLongThreads, smem, c->stream>>>(lp);
-    else k_long_smem<false><<<c->sms, kLongThreads, smem, c->stream>>>(lp);
-    CUDA_TRY(cudaGetLastError());
-    tm.end(6);
-    ++c->last_launches;
-  }
+  unsigned long long* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
+  lp.ovf = ovf_list;
+  // rows of (long_min, kLongSmemProducts] products: a block and on-chip tables
+  lp.sub = mid_list;
+  lp.n_sub = ctrl + kCtrlMidRows;
+  lp.ticket = ctrl + kCtrlLongSmemTicket;
+  tm.begin(6);
+  int rc = stats ? launch_long_smem<true>(c, lp, false) : launch_long_smem<false>(c, lp, false);
+  if (rc) return rc;
+  tm.end(6);
+  ++c->last_launches;
   if (any_huge) {
+    // longer rows: a cluster of blocks per row, one column range each
+    lp.sub = huge_list;
+    lp.n_sub = ctrl + kCtrlHugeRows;
+    lp.ticket = ctrl + kCtrlHugeTicket;
+    tm.begin(7);
+    rc = stats ? launch_long_smem<true>(c, lp, true) : launch_long_smem<false>(c, lp, true);
+    if (rc) return rc;
+    tm.end(7);
+    ++c->last_launches;
+    // rows whose column ranges outgrew the on-chip tables: global tables
+    lp.sub = ovf_list;
+    lp.n_sub = ctrl + kCtrlOvfRows;
+    lp.ticket = ctrl + kCtrlLongTicket;
     tm.begin(2);
-    // rows past kLongSmemProducts: global-memory tables
-    lp.min_prod = kLongSmemProducts;
     if (stats) k_long<true><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
     else k_long<false><<<c->ws_grid, kLongThreads, 0, c->stream>>>(lp);
     CUDA_TRY(cudaGetLastError());
@@ -707,7 +756,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->gtab, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
+                    &c->ws, &c->gtab, &c->sub, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
     release(*b, c->stream);
   cudaStreamSynchronize(c->stream);
   for (int k = 0; k < 2 * kNumKernels; ++k)

@@ -159,7 +159,8 @@ def _clustered_operands(rng, rows, inner, entries, blen, cols, far):
 
 @pytest.mark.parametrize("rows,inner,entries,blen", [
     (12, 3000, 1500, 4),     # on-chip long rows (k_long_smem), clustered buckets
-    (6, 6000, 4000, 5),      # rows past the on-chip limit
+    (6, 6000, 4000, 5),      # rows past the on-chip limit (cluster of column parts)
+    (3, 20000, 4000, 10),    # one part outgrows its table: handed on to k_long
     (40, 2000, 200, 3),      # warp rows (k_rows)
 ])
 def test_long_rows_clustered_columns(rows, inner, entries, blen):
