@@ -25,6 +25,7 @@ enum Ctrl : int {
   kCtrlHugeRows = 13,   // sub-list: rows for the cluster variant (8 blocks per row)
   kCtrlOvfRows = 14,    // sub-list: rows the cluster variant handed to k_long
   kCtrlHugeTicket = 15, // cluster variant's dynamic row counter
+  kCtrlCopyTickets = 16, // k_copy_long: [16] block rows, [17] warp rows
   kCtrlWords = 24
 };
 
@@ -450,23 +451,63 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
 
 
 // Long rows: staged by k_long, placed at their final offsets after k_fused.
-__global__ void __launch_bounds__(256) k_copy_long(const uint32_t* __restrict__ list,
-                                                   const uint64_t* __restrict__ l_off,
-                                                   const uint32_t* __restrict__ l_nnz,
-                                                   const unsigned long long* __restrict__ n_long,
-                                                   const uint64_t* __restrict__ l_ci,
-                                                   const double* __restrict__ l_v,
-                                                   const uint64_t* __restrict__ c_rp,
-                                                   uint64_t* __restrict__ c_ci,
-                                                   double* __restrict__ c_v) {
-  const uint32_t n = uint32_t(*n_long);
-  for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
-    const uint64_t dst = c_rp[list[li]];
-    const uint64_t src = l_off[li];
-    const uint32_t cnt = l_nnz[li];
-    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
-      c_ci[dst + t] = l_ci[src + t];
-      c_v[dst + t] = l_v[src + t];
+struct CopyParams {
+  const uint32_t* list;      // pre-computed rows (k_collect)
+  const uint32_t* prod;
+  const uint32_t* big;       // mid then huge sub-lists (rows = A.rows apart)
+  const unsigned long long* ctrl;
+  unsigned long long* tickets;  // [0] big rows, [1] other rows
+  const uint64_t* l_off;
+  const uint32_t* l_nnz;
+  const uint64_t* l_ci;
+  const double* l_v;
+  const uint64_t* c_rp;
+  uint64_t* c_ci;
+  double* c_v;
+  uint64_t rows;
+  uint32_t long_min;         // rows past it are in the sub-lists
+};
+
+// Copy the staged rows into their slots of C (after k_fused wrote row_ptr).
+// Rows of the sub-lists (long: up to tens of thousands of entries) are copied
+// by whole blocks first; the remaining listed rows (<= long_min products) by
+// one warp each. Both take rows dynamically.
+__global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
+  __shared__ uint32_t s_t;
+  const uint32_t n_mid = uint32_t(p.ctrl[kCtrlMidRows]);
+  const uint32_t n_big = n_mid + uint32_t(p.ctrl[kCtrlHugeRows]);
+  while (true) {
+    if (threadIdx.x == 0) s_t = uint32_t(atomicAdd(p.tickets, 1ull));
+    __syncthreads();
+    const uint32_t t = s_t;
+    __syncthreads();
+    if (t >= n_big) break;
+    const uint32_t li = t < n_mid ? p.big[t] : p.big[p.rows + (t - n_mid)];
+    const uint64_t dst = p.c_rp[p.list[li]];
+    const uint64_t src = p.l_off[li];
+    const uint32_t cnt = p.l_nnz[li];
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + dst + i,
+             (unsigned long long)__ldcs(p.l_ci + src + i));
+      __stcs(p.c_v + dst + i, __ldcs(p.l_v + src + i));
+    }
+  }
+  const uint32_t lane = lane_id();
+  const uint32_t n = uint32_t(p.ctrl[kCtrlLongRows]);
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.tickets + 1, 1ull);
+    const uint32_t li = uint32_t(__shfl_sync(kFull, t, 0));
+    if (li >= n) break;
+    const uint32_t r = p.list[li];
+    if (p.prod[r] > p.long_min) continue;  // copied above
+    const uint64_t dst = p.c_rp[r];
+    const uint64_t src = p.l_off[li];
+    const uint32_t cnt = p.l_nnz[li];
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + dst + i,
+             (unsigned long long)__ldcs(p.l_ci + src + i));
+      __stcs(p.c_v + dst + i, __ldcs(p.l_v + src + i));
     }
   }
 }
@@ -790,9 +831,10 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
     }
     // P1: bucket histogram. Buckets are column ranges (monotone), about 16
     // columns each, so every bucket is a small independent sort.
+    const uint32_t kmin = s_kmin, range = s_kmax - kmin;
     uint32_t nb = 2;
     while (nb * 16 < n_out && nb < uint32_t(kLongDupSlots) / 2) nb <<= 1;
-    const uint32_t kmin = s_kmin, range = s_kmax - kmin;
+    while ((range >> 26) >= nb) nb <<= 1;  // bucket width <= 2^26: 32-bit sort keys
     uint32_t sh = 0;
     while ((range >> sh) >= nb) ++sh;
     uint32_t* hist = dkey;  // the duplicate table is idle now
@@ -838,15 +880,16 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
           continue;
         }
         const uint64_t base = off + cursor[b] - sz;
-        unsigned long long key[2];
+        const uint32_t blo = kmin + (b << sh);  // bucket's first column
+        uint32_t key[2];
         double v[2];
 #pragma unroll
         for (int e2 = 0; e2 < 2; ++e2) {
           const uint32_t idx = uint32_t(e2) * 32u + lane;
-          key[e2] = ~0ull;
+          key[e2] = ~0u;
           v[e2] = 0.0;
           if (idx < sz) {
-            key[e2] = (__ldcg(p.l_ci + base + idx) << 6) | idx;
+            key[e2] = ((uint32_t(__ldcg(p.l_ci + base + idx)) - blo) << 6) | idx;
             v[e2] = __ldcg(p.l_v + base + idx);
           }
         }
@@ -854,11 +897,11 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
 #pragma unroll
         for (int e2 = 0; e2 < 2; ++e2) {
           const uint32_t idx = uint32_t(e2) * 32u + lane;
-          const uint32_t pos = uint32_t(key[e2]) & 63u;
+          const uint32_t pos = key[e2] & 63u;
           const double t0 = __shfl_sync(kFull, v[0], pos & 31u);
           const double t1 = __shfl_sync(kFull, v[1], pos & 31u);
           if (idx < sz) {
-            __stcg(p.l_ci + base + idx, key[e2] >> 6);
+            __stcg(p.l_ci + base + idx, uint64_t(blo + (key[e2] >> 6)));
             __stcg(p.l_v + base + idx, (pos >> 5) ? t1 : t0);
           }
         }

@@ -645,12 +645,22 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     ++c->last_launches;
     if (has_long) {
       tm.begin(4);
-      k_copy_long<<<c->sms * 4, 256, 0, c->stream>>>(
-          static_cast<const uint32_t*>(c->list.p), static_cast<const uint64_t*>(c->l_off.p),
-          static_cast<const uint32_t*>(c->l_nnz.p),
-          static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlLongRows,
-          static_cast<const uint64_t*>(stage_ci.p), static_cast<const double*>(stage_v.p),
-          p->rp, p->ci, p->v);
+      CopyParams cp;
+      cp.list = static_cast<const uint32_t*>(c->list.p);
+      cp.prod = static_cast<const uint32_t*>(c->prod.p);
+      cp.big = static_cast<const uint32_t*>(c->sub.p);
+      cp.ctrl = static_cast<const unsigned long long*>(c->ctrl.p);
+      cp.tickets = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCopyTickets;
+      cp.l_off = static_cast<const uint64_t*>(c->l_off.p);
+      cp.l_nnz = static_cast<const uint32_t*>(c->l_nnz.p);
+      cp.l_ci = static_cast<const uint64_t*>(stage_ci.p);
+      cp.l_v = static_cast<const double*>(stage_v.p);
+      cp.c_rp = p->rp;
+      cp.c_ci = p->ci;
+      cp.c_v = p->v;
+      cp.rows = rows;
+      cp.long_min = split ? kRowsLimit : kMediumLimit;
+      k_copy_long<<<c->sms * 8, 256, 0, c->stream>>>(cp);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "k_copy_long: %s",
                                                     cudaGetErrorString(e)));
