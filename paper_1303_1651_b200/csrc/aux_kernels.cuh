@@ -610,13 +610,31 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
     uint64_t clo = 0, chi = ~0ull;
     if constexpr (PARTS > 1) {
       uint32_t cmn = kEmptyKey, cmx = 0;
-      for (uint64_t e = lo + tid; e < hi; e += NT) {
-        const uint64_t k = ld_idx(p.A.ci + e);
-        const uint64_t bs = ld_idx(p.B.rp + k), be = ld_idx(p.B.rp + k + 1);
-        if (be > bs) {
-          const uint32_t c0 = uint32_t(ld_idx(p.B.ci + bs)), c1 = uint32_t(ld_idx(p.B.ci + be - 1));
-          cmn = c0 < cmn ? c0 : cmn;
-          cmx = c1 > cmx ? c1 : cmx;
+      // four entries per thread per round: the three dependent loads of each
+      // entry overlap across the four
+      for (uint64_t e0 = lo + tid; e0 < hi; e0 += 4 * NT) {
+        uint64_t k[4], bs[4], be[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t e = e0 + uint64_t(u) * NT;
+          k[u] = e < hi ? ld_idx(p.A.ci + e) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          bs[u] = be[u] = 0;
+          if (k[u] != ~0ull) {
+            bs[u] = ld_idx(p.B.rp + k[u]);
+            be[u] = ld_idx(p.B.rp + k[u] + 1);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (be[u] > bs[u]) {
+            const uint32_t c0 = uint32_t(ld_idx(p.B.ci + bs[u]));
+            const uint32_t c1 = uint32_t(ld_idx(p.B.ci + be[u] - 1));
+            cmn = c0 < cmn ? c0 : cmn;
+            cmx = c1 > cmx ? c1 : cmx;
+          }
         }
       }
       cmn = __reduce_min_sync(kFull, cmn);
@@ -645,8 +663,23 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
         bs = ld_idx(p.B.rp + k);
         uint64_t be = ld_idx(p.B.rp + k + 1);
         if constexpr (PARTS > 1) {
-          bs = col_lower_bound(p.B.ci, bs, be, clo);
-          be = col_lower_bound(p.B.ci, bs, be, chi);
+          if (be - bs <= 8) {  // short B row: one round of loads, then count
+            uint32_t c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              c[u] = bs + u < be ? uint32_t(ld_idx(p.B.ci + bs + u)) : kEmptyKey;
+            uint32_t nlo = 0, nhi = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              nlo += (bs + u < be && c[u] < clo) ? 1u : 0u;
+              nhi += (bs + u < be && c[u] < chi) ? 1u : 0u;
+            }
+            be = bs + nhi;
+            bs = bs + nlo;
+          } else {
+            bs = col_lower_bound(p.B.ci, bs, be, clo);
+            be = col_lower_bound(p.B.ci, bs, be, chi);
+          }
         }
         len = uint32_t(be - bs);
       }

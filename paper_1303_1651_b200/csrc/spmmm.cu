@@ -273,7 +273,10 @@ int ensure_gtab(spmmm_context* c, uint64_t warps, GtabView* v) {
 
 // ---- the long-row path ------------------------------------------------------
 
-constexpr int kLongParts = 8;  // blocks per cluster for rows past kLongSmemProducts
+#ifndef SPMMM_LONG_PARTS
+#define SPMMM_LONG_PARTS 4
+#endif
+constexpr int kLongParts = SPMMM_LONG_PARTS;  // blocks per cluster for rows past kLongSmemProducts
 
 // k_long_smem, one block per row or (cluster) kLongParts blocks per row
 template <bool S>
