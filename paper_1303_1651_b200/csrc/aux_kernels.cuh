@@ -926,7 +926,8 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
             v[e2] = __ldcg(p.l_v + base + idx);
           }
         }
-        bitonic_sort<2>(key);
+        if (sz <= 32) bitonic_sort<1>(key);  // the common size (about 16 per bucket)
+        else bitonic_sort<2>(key);
 #pragma unroll
         for (int e2 = 0; e2 < 2; ++e2) {
           const uint32_t idx = uint32_t(e2) * 32u + lane;
