@@ -119,6 +119,10 @@ struct spmmm_context {
   bool rows_attr[2] = {false, false};       // k_rows opt-in smem set
   int long_clusters = 0;                     // resident kLongParts-block clusters
   DevBuf sub;                                // per-kernel row sub-lists
+  // freed product arrays, reused by later products (a fresh cudaMallocAsync
+  // of hundreds of MB can cost tens of milliseconds of pool growth)
+  std::vector<std::pair<void*, size_t>> cache;
+  size_t cache_bytes = 0;
   cudaEvent_t ev[2 * kNumKernels] = {};
   bool ev_used[kNumKernels] = {};
   double last_ms[kNumKernels] = {};
@@ -133,9 +137,60 @@ struct spmmm_product {
   uint64_t* ci = nullptr;
   double* v = nullptr;
   uint32_t* st = nullptr;  // 3 * rows (min, max, touched) when row stats were requested
+  size_t cap[4] = {0, 0, 0, 0};  // allocation sizes of rp, ci, v, st (context cache)
 };
 
 namespace {
+
+// ---- product array cache ----------------------------------------------------
+
+constexpr size_t kCacheLimit = size_t(48) << 30;
+
+// Best fit among cached blocks of [bytes, 2*bytes + 1 MiB], else a new one.
+cudaError_t cache_alloc(spmmm_context* c, size_t bytes, void** out, size_t* cap) {
+  bytes = std::max(bytes, size_t(256));
+  int best = -1;
+  for (int i = 0; i < int(c->cache.size()); ++i) {
+    const size_t s = c->cache[i].second;
+    if (s >= bytes && s <= 2 * bytes + (size_t(1) << 20) &&
+        (best < 0 || s < c->cache[best].second))
+      best = i;
+  }
+  if (best >= 0) {
+    *out = c->cache[best].first;
+    *cap = c->cache[best].second;
+    c->cache_bytes -= *cap;
+    c->cache.erase(c->cache.begin() + best);
+    return cudaSuccess;
+  }
+  *cap = bytes;
+  return cudaMallocAsync(out, bytes, c->stream);
+}
+
+// Return a block (stream-ordered on the context stream, so a later product
+// on the same stream may reuse it at once); the oldest blocks past the limit
+// go back to the pool.
+void cache_free(spmmm_context* c, void* ptr, size_t cap) {
+  if (!ptr) return;
+  c->cache.emplace_back(ptr, cap);
+  c->cache_bytes += cap;
+  while (c->cache_bytes > kCacheLimit && !c->cache.empty()) {
+    cudaFreeAsync(c->cache.front().first, c->stream);
+    c->cache_bytes -= c->cache.front().second;
+    c->cache.erase(c->cache.begin());
+  }
+}
+
+void product_release(spmmm_context* c, spmmm_product* p) {
+  cache_free(c, p->rp, p->cap[0]);
+  cache_free(c, p->ci, p->cap[1]);
+  cache_free(c, p->v, p->cap[2]);
+  cache_free(c, p->st, p->cap[3]);
+  p->rp = nullptr;
+  p->ci = nullptr;
+  p->v = nullptr;
+  p->st = nullptr;
+}
 
 // ---- operand views --------------------------------------------------------
 
@@ -534,23 +589,20 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   p->cols = B.cols;
   p->mults = total;
   auto cleanup = [&](int code) {
-    if (p->rp) cudaFreeAsync(p->rp, c->stream);
-    if (p->ci) cudaFreeAsync(p->ci, c->stream);
-    if (p->v) cudaFreeAsync(p->v, c->stream);
-    if (p->st) cudaFreeAsync(p->st, c->stream);
+    product_release(c, p);
     delete p;
     return code;
   };
   // C storage: one reservation of `total` entries (the reference's own
   // capacity rule: CsrBuilder(..., estimate_nnz(a, b)), kernels.py:314)
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p->rp), (rows + 1) * 8, c->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&p->ci),
-                                            std::max<uint64_t>(total, 1) * 8, c->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&p->v),
-                                            std::max<uint64_t>(total, 1) * 8, c->stream);
+  cudaError_t e = cache_alloc(c, (rows + 1) * 8, reinterpret_cast<void**>(&p->rp), &p->cap[0]);
+  if (e == cudaSuccess)
+    e = cache_alloc(c, std::max<uint64_t>(total, 1) * 8, reinterpret_cast<void**>(&p->ci), &p->cap[1]);
+  if (e == cudaSuccess)
+    e = cache_alloc(c, std::max<uint64_t>(total, 1) * 8, reinterpret_cast<void**>(&p->v), &p->cap[2]);
   if (e == cudaSuccess && stats)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&p->st),
-                        std::max<uint64_t>(rows, 1) * 3 * sizeof(uint32_t), c->stream);
+    e = cache_alloc(c, std::max<uint64_t>(rows, 1) * 3 * sizeof(uint32_t),
+                    reinterpret_cast<void**>(&p->st), &p->cap[3]);
   if (e != cudaSuccess)
     return cleanup(fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
                         "allocating C (%llu entries): %s", (unsigned long long)total,
@@ -769,8 +821,11 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->gtab, &c->sub, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci, &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
+                    &c->ws, &c->gtab, &c->sub, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
+                    &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
     release(*b, c->stream);
+  for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
+  c->cache.clear();
   cudaStreamSynchronize(c->stream);
   for (int k = 0; k < 2 * kNumKernels; ++k)
     if (c->ev[k]) cudaEventDestroy(c->ev[k]);
@@ -867,10 +922,7 @@ int spmmm_product_destroy(spmmm_product* p) {
   spmmm_context* c = p->ctx;
   std::lock_guard<std::mutex> lock(c->mu);
   cudaSetDevice(c->device);
-  if (p->rp) cudaFreeAsync(p->rp, c->stream);
-  if (p->ci) cudaFreeAsync(p->ci, c->stream);
-  if (p->v) cudaFreeAsync(p->v, c->stream);
-  if (p->st) cudaFreeAsync(p->st, c->stream);
+  product_release(c, p);
   delete p;
   return SPMMM_OK;
 }
