@@ -4,6 +4,7 @@
 #include <cooperative_groups.h>
 
 #include "device.cuh"
+#include "rows.cuh"
 
 namespace spmmm {
 
@@ -26,6 +27,7 @@ enum Ctrl : int {
   kCtrlOvfRows = 14,    // sub-list: rows the cluster variant handed to k_long
   kCtrlHugeTicket = 15, // cluster variant's dynamic row counter
   kCtrlCopyTickets = 16, // k_copy_long: [16] block rows, [17] warp rows
+  kCtrlBMaxLen = 18,    // longest B row (entries)
   kCtrlWords = 24
 };
 
@@ -91,8 +93,18 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       }
     }
   }
+  // longest B row (decides the ELL copy of B); malformed rows saturate
+  uint64_t bmax = 0;
+  for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x); r < B.rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t b0 = ld_idx(B.rp + r), b1 = ld_idx(B.rp + r + 1);
+    const uint64_t l = b1 >= b0 ? b1 - b0 : ~0ull;
+    bmax = l > bmax ? l : bmax;
+  }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t ob = __shfl_xor_sync(kFull, bmax, d);
+    bmax = ob > bmax ? ob : bmax;
     tot += __shfl_xor_sync(kFull, tot, d);
     nonshort += __shfl_xor_sync(kFull, nonshort, d);
     const uint64_t o = __shfl_xor_sync(kFull, mx, d);
@@ -102,10 +114,37 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
   }
   if (lane == 0) {
     if (tot) atomicAdd(ctrl + kCtrlTotal, (unsigned long long)tot);
+    if (bmax) atomicMax(ctrl + kCtrlBMaxLen, (unsigned long long)bmax);
     if (nonshort) atomicAdd(ctrl + kCtrlNonShort, (unsigned long long)nonshort);
     if (mx) atomicMax(ctrl + kCtrlMaxProd, (unsigned long long)mx);
     if (need) atomicOr(ctrl + kCtrlNeedTable, 1ull);
     if (err) atomicOr(ctrl + kCtrlError, (unsigned long long)err);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ELL copy of B (rows <= kEllSlots entries): one 64-byte record per row, written
+// with four 16-byte stores (consecutive threads, consecutive records).
+__global__ void __launch_bounds__(256) k_pack_ell(DevCsr B, uint4* __restrict__ ell) {
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < B.rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+    uint32_t c[kEllSlots + 1];
+    double v[kEllSlots];
+#pragma unroll
+    for (int j = 0; j < kEllSlots; ++j) {
+      const bool in = lo + j < hi;
+      c[j] = in ? uint32_t(ld_idx(B.ci + lo + j)) : kEmptyKey;
+      v[j] = in ? ld_val(B.v + lo + j) : 0.0;
+    }
+    c[kEllSlots] = kEmptyKey;
+    auto lo32 = [](double x) { return uint32_t(__double_as_longlong(x)); };
+    auto hi32 = [](double x) { return uint32_t(uint64_t(__double_as_longlong(x)) >> 32); };
+    uint4* rec = ell + r * 4;
+    rec[0] = make_uint4(c[0], c[1], c[2], c[3]);
+    rec[1] = make_uint4(c[4], c[5], lo32(v[0]), hi32(v[0]));
+    rec[2] = make_uint4(lo32(v[1]), hi32(v[1]), lo32(v[2]), hi32(v[2]));
+    rec[3] = make_uint4(lo32(v[3]), hi32(v[3]), lo32(v[4]), hi32(v[4]));
   }
 }
 

@@ -82,6 +82,11 @@ __device__ __forceinline__ double ld_val(const double* p, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 
 // ---- relaxed gpu-scope accesses for the look-back status words ----
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {

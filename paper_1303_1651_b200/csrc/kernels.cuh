@@ -29,6 +29,7 @@ struct FusedParams {
   const uint32_t* prod;
   const uint32_t* lmap;
   const uint32_t* l_nnz;
+  const uint32_t* ell;  // ELL records of B (short variant, B rows <= kEllSlots) or null
   uint64_t* c_rp;
   uint64_t* c_ci;
   double* c_v;
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
         for (int i = 0; i < kLock; ++i) any |= hon[i];
         if (!any) continue;
         ShortOut so[kLock];
-        short_rows<kLock, WIDE, STATS>(p.A, p.B, hlo, hna, hon, so, hnnz, hmin, hmax, htouch);
+        short_rows<kLock, WIDE, STATS, !MEDIUM>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz, hmin, hmax, htouch);
 #pragma unroll
         for (int i = 0; i < kLock; ++i) {
           if (!hon[i]) continue;

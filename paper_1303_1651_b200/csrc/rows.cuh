@@ -25,8 +25,20 @@ struct ShortOut {
   bool keep;
 };
 
-template <int R, bool WIDE, bool STATS>
+// ELL copy of B for matrices whose rows have <= kEllSlots entries: one 64-byte
+// record per B row, u32 col[6] (unused slots 0xffffffff) then f64 val[5].
+// A tile row with <= kEllEntries A entries then maps product (entry e, slot j)
+// to lane 5e + j — lane order is still the reference's (k, j) order — and
+// needs no B.row_ptr loads, no scan and no search: one 64-byte block per
+// referenced B row.
+constexpr int kEllSlots = 5;
+constexpr int kEllWords = 16;   // 64 B per record
+constexpr int kEllValOff = 6;   // values start after 6 column words (byte 24)
+constexpr uint32_t kEllEntries = 32 / kEllSlots;  // 6
+
+template <int R, bool WIDE, bool STATS, bool ELLOK>
 __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
+                                           const uint32_t* __restrict__ ell,
                                            const uint64_t (&lo)[R], const uint32_t (&na)[R],
                                            const bool (&on)[R], ShortOut (&out)[R],
                                            uint32_t (&nnz)[R], uint32_t (&smin)[R],
@@ -35,87 +47,121 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
   // narrow variant: every index and offset fits 32 bits (checked on the host)
   using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
   const uint32_t lane = lane_id();
-  Off kk[R];
-  double av[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    kk[i] = 0;
-    av[i] = 0.0;
-    if (on[i] && lane < na[i]) {
-      kk[i] = Off(ld_idx(A.ci + lo[i] + lane, A.pol));
-      av[i] = ld_val(A.v + lo[i] + lane, A.pol);
-    }
-  }
-  Off bs[R];
-  uint32_t len[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    bs[i] = 0;
-    len[i] = 0;
-    if (on[i] && lane < na[i]) {
-      const uint64_t b0 = ld_idx(B.rp + kk[i], B.pol);
-      bs[i] = Off(b0);
-      len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1, B.pol) - b0);
-    }
-  }
-  // widest A row of the tile bounds the scan and search depth (warp-uniform)
-  uint32_t na_max = 1;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (on[i] && na[i] > na_max) na_max = na[i];
-  uint32_t incl[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) incl[i] = len[i];
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    if (uint32_t(d) >= na_max) break;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint32_t t = __shfl_up_sync(kFull, incl[i], d);
-      if (lane >= uint32_t(d)) incl[i] += t;
-    }
-  }
-  uint32_t excl[R], tot[R];
-  int src[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    excl[i] = incl[i] - len[i];
-    tot[i] = __shfl_sync(kFull, incl[i], (na[i] - 1) & 31u);
-    if (lane >= na[i]) excl[i] = tot[i];  // beyond the row: never owns a product
-    src[i] = 0;
-  }
-  // entry owning product q = lane: the largest i with excl_i <= lane
-#pragma unroll
-  for (int st = 16; st > 0; st >>= 1) {
-    if (uint32_t(st) >= na_max) continue;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint32_t ex = __shfl_sync(kFull, excl[i], src[i] + st);
-      if (ex <= lane) src[i] += st;
-    }
-  }
-  uint32_t col[R];
-  double p[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const Off bsrc = __shfl_sync(kFull, bs[i], src[i]) + (lane - __shfl_sync(kFull, excl[i], src[i]));
-    const double a = __shfl_sync(kFull, av[i], src[i]);
-    col[i] = 0;
-    p[i] = a;
-    if (lane < tot[i]) {
-      col[i] = uint32_t(ld_idx(B.ci + bsrc, B.pol));
-      p[i] = ld_val(B.v + bsrc, B.pol);  // multiplied below, after the loads are in flight
-    }
-  }
   K key[R];
+  double p[R];
+  uint32_t tot[R];
+  bool fast = false;
+  if constexpr (ELLOK) {
+    fast = ell != nullptr;
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const bool valid = lane < tot[i];
-    const double a = __shfl_sync(kFull, av[i], src[i]);
-    p[i] = valid ? __dmul_rn(a, p[i]) : 0.0;
-    key[i] = valid ? ((K(col[i]) << 5) | K(lane)) : ~K(0);
+    for (int i = 0; i < R; ++i) fast &= !on[i] || na[i] <= kEllEntries;
   }
+  if (fast) {
+    const uint32_t e = lane / kEllSlots, j = lane - e * kEllSlots;
+    uint32_t col[R];
+    double bv[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      col[i] = kEmptyKey;
+      p[i] = 0.0;
+      bv[i] = 0.0;
+      if (on[i] && e < na[i]) {
+        const uint64_t k = ld_idx(A.ci + lo[i] + e, A.pol);
+        p[i] = ld_val(A.v + lo[i] + e, A.pol);
+        const uint32_t* rec = ell + k * kEllWords;
+        col[i] = ld_u32(rec + j, B.pol);
+        bv[i] = ld_val(reinterpret_cast<const double*>(rec + kEllValOff) + j, B.pol);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const bool valid = col[i] != kEmptyKey;
+      p[i] = valid ? __dmul_rn(p[i], bv[i]) : 0.0;
+      tot[i] = __popc(__ballot_sync(kFull, valid));
+      key[i] = valid ? ((K(col[i]) << 5) | K(lane)) : ~K(0);
+    }
+  } else {
+    Off kk[R];
+    double av[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      kk[i] = 0;
+      av[i] = 0.0;
+      if (on[i] && lane < na[i]) {
+        kk[i] = Off(ld_idx(A.ci + lo[i] + lane, A.pol));
+        av[i] = ld_val(A.v + lo[i] + lane, A.pol);
+      }
+    }
+    Off bs[R];
+    uint32_t len[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      bs[i] = 0;
+      len[i] = 0;
+      if (on[i] && lane < na[i]) {
+        const uint64_t b0 = ld_idx(B.rp + kk[i], B.pol);
+        bs[i] = Off(b0);
+        len[i] = uint32_t(ld_idx(B.rp + kk[i] + 1, B.pol) - b0);
+      }
+    }
+    // widest A row of the tile bounds the scan and search depth (warp-uniform)
+    uint32_t na_max = 1;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (on[i] && na[i] > na_max) na_max = na[i];
+    uint32_t incl[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) incl[i] = len[i];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      if (uint32_t(d) >= na_max) break;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint32_t t = __shfl_up_sync(kFull, incl[i], d);
+        if (lane >= uint32_t(d)) incl[i] += t;
+      }
+    }
+    uint32_t excl[R];
+    int src[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      excl[i] = incl[i] - len[i];
+      tot[i] = __shfl_sync(kFull, incl[i], (na[i] - 1) & 31u);
+      if (lane >= na[i]) excl[i] = tot[i];  // beyond the row: never owns a product
+      src[i] = 0;
+    }
+    // entry owning product q = lane: the largest i with excl_i <= lane
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      if (uint32_t(st) >= na_max) continue;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint32_t ex = __shfl_sync(kFull, excl[i], src[i] + st);
+        if (ex <= lane) src[i] += st;
+      }
+    }
+    uint32_t col[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const Off bsrc = __shfl_sync(kFull, bs[i], src[i]) + (lane - __shfl_sync(kFull, excl[i], src[i]));
+      const double a = __shfl_sync(kFull, av[i], src[i]);
+      col[i] = 0;
+      p[i] = a;
+      if (lane < tot[i]) {
+        col[i] = uint32_t(ld_idx(B.ci + bsrc, B.pol));
+        p[i] = ld_val(B.v + bsrc, B.pol);  // multiplied below, after the loads are in flight
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const bool valid = lane < tot[i];
+      const double a = __shfl_sync(kFull, av[i], src[i]);
+      p[i] = valid ? __dmul_rn(a, p[i]) : 0.0;
+      key[i] = valid ? ((K(col[i]) << 5) | K(lane)) : ~K(0);
+    }
+  }  // generic path
   bitonic32_multi<R>(key);
+  uint32_t col[R];
   double v[R], acc[R];
   bool head[R];
   uint32_t seg[R], touches[R];

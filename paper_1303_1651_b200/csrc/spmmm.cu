@@ -95,8 +95,8 @@ void release(DevBuf& b, cudaStream_t s) {
 }
 
 const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
-                                    "k_rows", "k_long_smem", "k_long_cluster"};
-constexpr int kNumKernels = 8;
+                                    "k_rows", "k_long_smem", "k_long_cluster", "k_pack_ell"};
+constexpr int kNumKernels = 9;
 
 }  // namespace
 
@@ -119,6 +119,7 @@ struct spmmm_context {
   bool rows_attr[2] = {false, false};       // k_rows opt-in smem set
   int long_clusters = 0;                     // resident kLongParts-block clusters
   DevBuf sub;                                // per-kernel row sub-lists
+  DevBuf ell;                                // ELL records of B (short rows)
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -672,6 +673,22 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.ntiles = ntiles;
     fp.medium_limit = medium_limit;
     fp.a_is_b = (A.ci == B.ci && A.v == B.v) ? 1u : 0u;
+    fp.ell = nullptr;
+    // short variant over a B whose rows all fit an ELL record: pack B once per
+    // call (one 64-byte record per row; a referenced B row is then one block)
+    if (!medium && c->h_ctrl[kCtrlBMaxLen] <= uint64_t(kEllSlots) && B.rows > 0) {
+      e = ensure(c->ell, B.rows * 64, c->stream);
+      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "ell: %s", cudaGetErrorString(e)));
+      const uint64_t blocks = std::min<uint64_t>((B.rows + 255) / 256, uint64_t(c->sms) * 16);
+      tm.begin(8);
+      k_pack_ell<<<unsigned(blocks), 256, 0, c->stream>>>(B, static_cast<uint4*>(c->ell.p));
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "k_pack_ell: %s",
+                                                    cudaGetErrorString(e)));
+      tm.end(8);
+      ++c->last_launches;
+      fp.ell = static_cast<const uint32_t*>(c->ell.p);
+    }
     fp.g_keys = nullptr;
     fp.g_vals = nullptr;
     fp.g_scol = nullptr;
@@ -821,7 +838,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->gtab, &c->sub, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
+                    &c->ws, &c->gtab, &c->sub, &c->ell, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);

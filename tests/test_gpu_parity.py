@@ -111,6 +111,8 @@ def _rand_csr(rng, rows, cols, per_row_max, values="uniform", min_len=0):
     (7, (40, 2000, 300, 300, 30)),       # on-chip long rows, few columns (dup rounds)
     (8, (24, 3000, 60000, 2500, 14)),    # rows past the on-chip limit (global tables)
     (9, (30, 2000, 400, 1500, 40)),      # global tables, heavy duplicates per chunk
+    (10, (2000, 3000, 4000, 32, 1)),     # ELL copy of B, wide A rows (generic short path)
+    (11, (2000, 3000, 4000, 6, 5)),      # ELL fast path, empty and partial B rows
 ])
 @pytest.mark.parametrize("values", ["uniform", "quantized"])
 def test_random_vs_oracle(seed, shape, values):
