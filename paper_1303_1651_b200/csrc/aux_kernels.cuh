@@ -27,7 +27,9 @@ enum Ctrl : int {
   kCtrlOvfRows = 14,    // sub-list: rows the cluster variant handed to k_long
   kCtrlHugeTicket = 15, // cluster variant's dynamic row counter
   kCtrlCopyTickets = 16, // k_copy_long: [16] block rows, [17] warp rows
-  kCtrlBMaxLen = 18,    // longest B row (entries)
+  kCtrlBMaxLen = 18,    // longest B row referenced by A (entries)
+  kCtrlKMinInv = 19,    // ~(smallest column of A), 0 if A has no entries
+  kCtrlKMax1 = 20,      // largest column of A + 1, 0 if none
   kCtrlWords = 24
 };
 
@@ -38,7 +40,7 @@ enum Ctrl : int {
 __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
                                                unsigned long long* __restrict__ ctrl) {
   const uint32_t lane = lane_id();
-  uint64_t tot = 0, mx = 0, nonshort = 0;
+  uint64_t tot = 0, mx = 0, nonshort = 0, bmax = 0, kmin = ~0ull, kmax1 = 0;
   uint32_t need = 0, err = 0;
   const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
   const uint64_t gw = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -57,12 +59,30 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
     uint64_t p = 0;
     const bool serial = hi - lo <= kSerial;
     if (serial) {
-      for (uint64_t e = lo; e < hi; ++e) {
-        const uint64_t k = ld_idx(A.ci + e);
-        if (k >= B.rows) { err |= 2u; continue; }
-        const uint64_t b0 = ld_idx(B.rp + k), b1 = ld_idx(B.rp + k + 1);
-        if (b1 < b0 || b1 > B.nnz) { err |= 4u; continue; }
-        p += b1 - b0;
+      // four entries per round: their two dependent load levels overlap
+      for (uint64_t e0 = lo; e0 < hi; e0 += 4) {
+        uint64_t k[4], b0[4], b1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k[u] = e0 + u < hi ? ld_idx(A.ci + e0 + u) : ~0ull;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          b0[u] = b1[u] = 0;
+          if (k[u] != ~0ull && k[u] < B.rows) {
+            b0[u] = ld_idx(B.rp + k[u]);
+            b1[u] = ld_idx(B.rp + k[u] + 1);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k[u] == ~0ull) continue;
+          if (k[u] >= B.rows) { err |= 2u; continue; }
+          if (b1[u] < b0[u] || b1[u] > B.nnz) { err |= 4u; continue; }
+          const uint64_t l = b1[u] - b0[u];
+          p += l;
+          bmax = l > bmax ? l : bmax;
+          kmin = k[u] < kmin ? k[u] : kmin;
+          kmax1 = k[u] + 1 > kmax1 ? k[u] + 1 : kmax1;
+        }
       }
     }
     // long A rows: the whole warp, one row at a time
@@ -78,6 +98,9 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
         const uint64_t b0 = ld_idx(B.rp + k), b1 = ld_idx(B.rp + k + 1);
         if (b1 < b0 || b1 > B.nnz) { err |= 4u; continue; }
         s += b1 - b0;
+        bmax = b1 - b0 > bmax ? b1 - b0 : bmax;
+        kmin = k < kmin ? k : kmin;
+        kmax1 = k + 1 > kmax1 ? k + 1 : kmax1;
       }
       s = warp_sum64(s);
       if (lane == src) p = s;
@@ -93,18 +116,14 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       }
     }
   }
-  // longest B row (decides the ELL copy of B); malformed rows saturate
-  uint64_t bmax = 0;
-  for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x); r < B.rows;
-       r += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t b0 = ld_idx(B.rp + r), b1 = ld_idx(B.rp + r + 1);
-    const uint64_t l = b1 >= b0 ? b1 - b0 : ~0ull;
-    bmax = l > bmax ? l : bmax;
-  }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     const uint64_t ob = __shfl_xor_sync(kFull, bmax, d);
     bmax = ob > bmax ? ob : bmax;
+    const uint64_t ok0 = __shfl_xor_sync(kFull, kmin, d);
+    kmin = ok0 < kmin ? ok0 : kmin;
+    const uint64_t ok1 = __shfl_xor_sync(kFull, kmax1, d);
+    kmax1 = ok1 > kmax1 ? ok1 : kmax1;
     tot += __shfl_xor_sync(kFull, tot, d);
     nonshort += __shfl_xor_sync(kFull, nonshort, d);
     const uint64_t o = __shfl_xor_sync(kFull, mx, d);
@@ -112,23 +131,75 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
     need |= __shfl_xor_sync(kFull, need, d);
     err |= __shfl_xor_sync(kFull, err, d);
   }
+  // block-level combine, then one set of atomics per block (same-address
+  // atomics from every warp serialise in L2)
+  __shared__ unsigned long long s_red[8][8];
+  const uint32_t warp = threadIdx.x >> 5;
   if (lane == 0) {
-    if (tot) atomicAdd(ctrl + kCtrlTotal, (unsigned long long)tot);
-    if (bmax) atomicMax(ctrl + kCtrlBMaxLen, (unsigned long long)bmax);
-    if (nonshort) atomicAdd(ctrl + kCtrlNonShort, (unsigned long long)nonshort);
-    if (mx) atomicMax(ctrl + kCtrlMaxProd, (unsigned long long)mx);
-    if (need) atomicOr(ctrl + kCtrlNeedTable, 1ull);
-    if (err) atomicOr(ctrl + kCtrlError, (unsigned long long)err);
+    s_red[0][warp] = tot;
+    s_red[1][warp] = nonshort;
+    s_red[2][warp] = mx;
+    s_red[3][warp] = bmax;
+    s_red[4][warp] = ~kmin;
+    s_red[5][warp] = kmax1;
+    s_red[6][warp] = need;
+    s_red[7][warp] = err;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const uint32_t f = threadIdx.x;
+    unsigned long long x = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+      const unsigned long long y = s_red[f][w];
+      x = f < 2 ? x + y : (f < 6 ? (y > x ? y : x) : (x | y));
+    }
+    if (x) {
+      switch (f) {
+        case 0: atomicAdd(ctrl + kCtrlTotal, x); break;
+        case 1: atomicAdd(ctrl + kCtrlNonShort, x); break;
+        case 2: atomicMax(ctrl + kCtrlMaxProd, x); break;
+        case 3: atomicMax(ctrl + kCtrlBMaxLen, x); break;
+        case 4: atomicMax(ctrl + kCtrlKMinInv, x); break;
+        case 5: atomicMax(ctrl + kCtrlKMax1, x); break;
+        case 6: atomicOr(ctrl + kCtrlNeedTable, 1ull); break;
+        default: atomicOr(ctrl + kCtrlError, x); break;
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // ELL copy of B (rows <= kEllSlots entries): one 64-byte record per row, written
 // with four 16-byte stores (consecutive threads, consecutive records).
-__global__ void __launch_bounds__(256) k_pack_ell(DevCsr B, uint4* __restrict__ ell) {
-  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < B.rows;
+// Whether the short variant reads B through ELL records, from k_count's
+// results — evaluated identically by k_pack_ell (device) and the host.
+__host__ __device__ inline bool ell_wanted(const unsigned long long* w, uint64_t rows) {
+  const uint64_t total = w[kCtrlTotal], bmax = w[kCtrlBMaxLen];
+  const uint64_t k0 = ~w[kCtrlKMinInv], k1 = w[kCtrlKMax1];
+  const bool need = w[kCtrlNeedTable] != 0;
+  const bool split = need && w[kCtrlNonShort] * 4 <= rows;
+  if (need && !split) return false;  // medium variant
+  if (bmax > uint64_t(kEllSlots) || k1 <= k0) return false;
+  // worth it when the referenced B rows (>= total / longest) are not much
+  // fewer than the rows the copy spans
+  return 10 * (total / (bmax ? bmax : 1)) >= 7 * (k1 - k0);
+}
+
+// Only the rows A references ([kmin, kmax], from k_count) are packed; rows in
+// between that are longer than a record are truncated and never read. Runs
+// right behind k_count, while the host reads k_count's results back.
+__global__ void __launch_bounds__(256) k_pack_ell(DevCsr B, uint64_t a_rows,
+                                                  const unsigned long long* __restrict__ ctrl,
+                                                  uint4* __restrict__ ell) {
+  if (!ell_wanted(ctrl, a_rows)) return;
+  const uint64_t r0 = ~ctrl[kCtrlKMinInv], r1 = ctrl[kCtrlKMax1];
+  for (uint64_t r = r0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < r1;
        r += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+    // unreferenced rows are not validated by k_count: clamp to the arrays
+    uint64_t hi = ld_idx(B.rp + r + 1);
+    hi = hi < B.nnz ? hi : B.nnz;
+    uint64_t lo = ld_idx(B.rp + r);
+    lo = lo < hi ? lo : hi;
     uint32_t c[kEllSlots + 1];
     double v[kEllSlots];
 #pragma unroll

@@ -125,6 +125,7 @@ struct spmmm_context {
   std::vector<std::pair<void*, size_t>> cache;
   size_t cache_bytes = 0;
   cudaEvent_t ev[2 * kNumKernels] = {};
+  cudaEvent_t ev_count = nullptr;  // k_count's results are on the host
   bool ev_used[kNumKernels] = {};
   double last_ms[kNumKernels] = {};
   int last_count = 0;
@@ -263,8 +264,9 @@ struct Timer {
 
 // ---- the count pass ----------------------------------------------------------
 
-int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm) {
+int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, bool pack = false) {
   CUDA_TRY(ensure(c->prod, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
+  if (pack) CUDA_TRY(ensure(c->ell, std::max<uint64_t>(B.rows, 1) * 64, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
   if (A.rows) {
     const uint64_t blocks = std::min<uint64_t>((A.rows + 255) / 256, uint64_t(c->sms) * 8);
@@ -277,7 +279,17 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm) {
   }
   CUDA_TRY(cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, kCtrlWords * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev_count, c->stream));
+  if (pack && A.rows) {
+    // the ELL copy of B (if k_count's results call for it) overlaps the readback
+    tm.begin(8);
+    k_pack_ell<<<unsigned(c->sms) * 16, 256, 0, c->stream>>>(
+        B, A.rows, static_cast<const unsigned long long*>(c->ctrl.p), static_cast<uint4*>(c->ell.p));
+    CUDA_TRY(cudaGetLastError());
+    tm.end(8);
+    ++c->last_launches;
+  }
+  CUDA_TRY(cudaEventSynchronize(c->ev_count));
   const unsigned long long err = c->h_ctrl[kCtrlError];
   if (err & 1) return fail(SPMMM_ERR_INVALID, "malformed a.row_ptr (decreasing or past nnz)");
   if (err & 2) return fail(SPMMM_ERR_INVALID, "a.col_idx entry >= b.rows");
@@ -559,7 +571,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   const uint64_t rows = A.rows;
 
   const Trace tr;
-  rc = run_count(c, A, B, tm);
+  rc = run_count(c, A, B, tm, true);
   if (rc) return rc;
   tr.mark("count done (host has totals)");
   const uint64_t total = c->h_ctrl[kCtrlTotal];
@@ -676,19 +688,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.ell = nullptr;
     // short variant over a B whose rows all fit an ELL record: pack B once per
     // call (one 64-byte record per row; a referenced B row is then one block)
-    if (!medium && c->h_ctrl[kCtrlBMaxLen] <= uint64_t(kEllSlots) && B.rows > 0) {
-      e = ensure(c->ell, B.rows * 64, c->stream);
-      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "ell: %s", cudaGetErrorString(e)));
-      const uint64_t blocks = std::min<uint64_t>((B.rows + 255) / 256, uint64_t(c->sms) * 16);
-      tm.begin(8);
-      k_pack_ell<<<unsigned(blocks), 256, 0, c->stream>>>(B, static_cast<uint4*>(c->ell.p));
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "k_pack_ell: %s",
-                                                    cudaGetErrorString(e)));
-      tm.end(8);
-      ++c->last_launches;
-      fp.ell = static_cast<const uint32_t*>(c->ell.p);
-    }
+    if (ell_wanted(c->h_ctrl, rows)) fp.ell = static_cast<const uint32_t*>(c->ell.p);
     fp.g_keys = nullptr;
     fp.g_vals = nullptr;
     fp.g_scol = nullptr;
@@ -823,6 +823,7 @@ int spmmm_context_create(int device, void* cuda_stream, spmmm_context** out) {
   }
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_ctrl, kCtrlWords * sizeof(unsigned long long));
   for (int k = 0; k < 2 * kNumKernels && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
   if (e == cudaSuccess) e = ensure(c->ctrl, kCtrlWords * sizeof(unsigned long long), c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
@@ -846,6 +847,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaStreamSynchronize(c->stream);
   for (int k = 0; k < 2 * kNumKernels; ++k)
     if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+  if (c->ev_count) cudaEventDestroy(c->ev_count);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
