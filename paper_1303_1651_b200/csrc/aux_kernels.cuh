@@ -30,6 +30,7 @@ enum Ctrl : int {
   kCtrlBMaxLen = 18,    // longest B row referenced by A (entries)
   kCtrlKMinInv = 19,    // ~(smallest column of A), 0 if A has no entries
   kCtrlKMax1 = 20,      // largest column of A + 1, 0 if none
+  kCtrlNnz = 21,        // nnz(C), written by k_fused's last tile
   kCtrlWords = 24
 };
 
@@ -37,8 +38,14 @@ enum Ctrl : int {
 // K1: per-row product counts. formats.py:276-289 per row. A warp takes 32
 // consecutive rows (one per lane); rows with many A entries are summed by the
 // whole warp so a 4096-entry row does not stall its 31 neighbours.
+// Also zeroes k_fused's look-back counters (`zero`, `nzero` words) on the way.
 __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
-                                               unsigned long long* __restrict__ ctrl) {
+                                               unsigned long long* __restrict__ ctrl,
+                                               unsigned long long* __restrict__ zero,
+                                               uint64_t nzero) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nzero;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    zero[i] = 0;
   const uint32_t lane = lane_id();
   uint64_t tot = 0, mx = 0, nonshort = 0, bmax = 0, kmin = ~0ull, kmax1 = 0;
   uint32_t need = 0, err = 0;

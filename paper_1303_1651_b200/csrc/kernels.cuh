@@ -30,6 +30,7 @@ struct FusedParams {
   const uint32_t* lmap;
   const uint32_t* l_nnz;
   const uint32_t* ell;  // ELL records of B (short variant, B rows <= kEllSlots) or null
+  unsigned long long* nnz_out;  // nnz(C) for the host (ctrl word)
   uint64_t* c_rp;
   uint64_t* c_ci;
   double* c_v;
@@ -128,7 +129,9 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       for (int j = 0; j < R; ++j)
         if (uint32_t(j) <= lane) s += s_hdr[b * R + j];
       p.c_rp[r0 + lane + 1] = excl + s;
+      if (r0 + lane + 1 == rows) *p.nnz_out = excl + s;  // read back by the host
     }
+    if (tile == 0 && lane == 0) p.c_rp[0] = 0;
     const uint32_t ext = MEDIUM ? 0u : s_meta32[2 * b + 1];  // short variant: external rows
     if (!MEDIUM && ext) {
       // the tile mixes staged short rows with rows computed before k_fused

@@ -264,15 +264,43 @@ struct Timer {
 
 // ---- the count pass ----------------------------------------------------------
 
+// Look-back state of k_fused: the level-1.. counters first (zeroed by k_count
+// for the largest layout a call can use: one row per tile), then the status
+// words of every level.
+uint64_t lb_counters_max(uint64_t rows) {
+  uint64_t n = rows, total = 0;
+  for (int l = 1; l < kLevels; ++l) {
+    n = (n + 31) / 32;
+    total += n;
+  }
+  return total;
+}
+
 int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, bool pack = false) {
   CUDA_TRY(ensure(c->prod, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
+  // status: counters + words for one row per tile (the medium layout, the largest)
+  const uint64_t ncnt = pack ? lb_counters_max(A.rows) : 0;
+  if (pack) {
+    bool grown = false;
+    uint64_t words = 0, n = A.rows;
+    for (int l = 0; l < kLevels; ++l) {
+      words += n;
+      n = (n + 31) / 32;
+    }
+    CUDA_TRY(ensure(c->status, (words + ncnt) * sizeof(uint64_t), c->stream, &grown));
+    if (grown || c->epoch >= 0xffffu) {
+      CUDA_TRY(cudaMemsetAsync(c->status.p, 0, c->status.cap, c->stream));
+      c->epoch = 0;
+    }
+  }
   if (pack) CUDA_TRY(ensure(c->ell, std::max<uint64_t>(B.rows, 1) * 64, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
   if (A.rows) {
     const uint64_t blocks = std::min<uint64_t>((A.rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(0);
     k_count<<<unsigned(blocks), 256, 0, c->stream>>>(
-        A, B, static_cast<uint32_t*>(c->prod.p), static_cast<unsigned long long*>(c->ctrl.p));
+        A, B, static_cast<uint32_t*>(c->prod.p), static_cast<unsigned long long*>(c->ctrl.p),
+        static_cast<unsigned long long*>(c->status.p), ncnt);
     CUDA_TRY(cudaGetLastError());
     tm.end(0);
     ++c->last_launches;
@@ -620,8 +648,10 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     return cleanup(fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
                         "allocating C (%llu entries): %s", (unsigned long long)total,
                         cudaGetErrorString(e)));
-  e = cudaMemsetAsync(p->rp, 0, sizeof(uint64_t), c->stream);
-  if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+  if (!rows) {  // otherwise k_fused's first tile writes row_ptr[0]
+    e = cudaMemsetAsync(p->rp, 0, sizeof(uint64_t), c->stream);
+    if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+  }
   tr.mark("C allocated");
 
   // staging of pre-computed rows: context buffers, grown on demand and kept
@@ -642,24 +672,12 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     uint64_t nl[kLevels];
     nl[0] = ntiles;
     for (int l = 1; l < kLevels; ++l) nl[l] = (nl[l - 1] + 31) / 32;
-    uint64_t words = 0, counters = 0;
-    for (int l = 0; l < kLevels; ++l) words += nl[l];
-    for (int l = 1; l < kLevels; ++l) counters += nl[l];
-    bool grown = false;
-    e = ensure(c->status, (words + counters) * sizeof(uint64_t), c->stream, &grown);
-    if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_OOM, "status: %s", cudaGetErrorString(e)));
-    if (grown || c->epoch >= 0xffffu) {
-      e = cudaMemsetAsync(c->status.p, 0, c->status.cap, c->stream);
-      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
-      c->epoch = 0;
-    }
     c->epoch += 1;
     FusedParams fp;
     {
-      uint64_t* w = static_cast<uint64_t*>(c->status.p);
-      unsigned long long* cnt = reinterpret_cast<unsigned long long*>(w + words);
-      e = cudaMemsetAsync(cnt, 0, counters * sizeof(unsigned long long), c->stream);
-      if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e)));
+      // counters at the front (zeroed by k_count), then the status words
+      unsigned long long* cnt = static_cast<unsigned long long*>(c->status.p);
+      uint64_t* w = reinterpret_cast<uint64_t*>(cnt + lb_counters_max(rows));
       fp.lb.count[0] = nullptr;
       for (int l = 0; l < kLevels; ++l) {
         fp.lb.stat[l] = w;
@@ -674,6 +692,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       fp.lb.fault = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault;
     }
     fp.ticket = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlTicket;
+    fp.nnz_out = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlNnz;
     fp.A = A;
     fp.B = B;
     fp.prod = static_cast<const uint32_t*>(c->prod.p);
@@ -741,11 +760,12 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     }
   }
   tr.mark("fused + copy launched");
+  // one read-back: the watchdog word through nnz(C) (rows == 0: nnz is 0)
+  static_assert(kCtrlNnz > kCtrlFault, "ctrl layout");
+  if (!rows) c->h_ctrl[kCtrlNnz] = 0;
   e = cudaMemcpyAsync(c->h_ctrl + kCtrlFault, static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault,
-                      sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(c->h_ctrl + kCtrlTotal, p->rp + rows, sizeof(uint64_t),
-                        cudaMemcpyDeviceToHost, c->stream);
+                      (rows ? kCtrlNnz - kCtrlFault + 1 : 1) * sizeof(uint64_t),
+                      cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
   if (c->h_ctrl[kCtrlFault]) {
@@ -753,7 +773,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     return cleanup(fail(SPMMM_ERR_CUDA, "k_fused look-back watchdog: site %llu tile %llu",
                         (f >> 48) & 0x7fff, f & ((1ull << 48) - 1)));
   }
-  p->nnz = c->h_ctrl[kCtrlTotal];
+  p->nnz = c->h_ctrl[kCtrlNnz];
   tr.mark("done");
   if (tm.on) {
     for (int k = 0; k < kNumKernels; ++k) {
