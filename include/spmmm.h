@@ -126,6 +126,14 @@ int spmmm_estimate_nnz(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* 
 int spmmm_row_products_prefix(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b,
                               uint64_t* out);
 
+/* Storage-order conversion: the product holds the CSR of M^T for the CSR view
+ * M, i.e. the arrays of csr_to_csc(M) (formats.py:302-329); a CSC matrix
+ * passed as the CSR view of its transpose yields csc_to_csr (formats.py:332-357).
+ * Within each output slice the minor indices keep the input's major order (the
+ * reference's stable scatter). Used by multiply_mixed's single conversion
+ * (kernels.py:417-438); the result's device arrays can feed spmmm_multiply. */
+int spmmm_transpose(spmmm_context* ctx, const spmmm_csr* m, spmmm_product** out);
+
 /* Per-kernel timings of the last spmmm_multiply with SPMMM_FLAG_TIMING:
  * names[i] (static strings) and milliseconds ms[i], i < *count (<= cap). */
 int spmmm_last_timings(spmmm_context* ctx, const char** names, double* ms, int cap, int* count);

@@ -165,3 +165,50 @@ def dense_multiply(a_dense, b_dense):
         out += np.multiply.outer(a[:, k], b[k, :])
     mults = int(np.count_nonzero(a, axis=0) @ np.count_nonzero(b, axis=1))
     return out, mults
+
+
+# ---------------------------------------------------------------------------
+# Storage orders (kernels.py:335-363, 417-438; formats.py:292-357).
+
+
+@dataclass
+class _Csr:
+    rows: int
+    cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+
+def transpose(n_major, n_minor, ptr, idx, val):
+    """formats.py:302-329 (csr_to_csc) / 332-357 (csc_to_csr): count per minor
+    index, prefix sum, then a stable scatter of the entries in major order.
+    Returns (ptr, idx, val) of the other storage order (n_minor slices)."""
+    ptr = np.asarray(ptr, np.uint64)
+    idx = np.asarray(idx, np.uint64)
+    val = np.asarray(val, np.float64)
+    counts = np.bincount(idx.astype(np.intp), minlength=n_minor)
+    out_ptr = np.zeros(n_minor + 1, np.uint64)
+    np.cumsum(counts, out=out_ptr[1:])
+    # stable order by minor index == the reference's scatter in major order
+    order = np.argsort(idx, kind="stable")
+    major_of = np.repeat(np.arange(n_major, dtype=np.uint64), np.diff(ptr).astype(np.intp))
+    return out_ptr, major_of[order], val[order]
+
+
+def multiply_colmajor(a_csc, b_csc, *, row_choices: bool = False) -> OracleResult:
+    """kernels.py:335-363: for each column c of B, its entries b[k, c] in
+    ascending k scale column k of A into the accumulator. That is the
+    row-major kernel with B's columns as the 'rows' and A's columns as the
+    scaled slices — kernels.py:344-357 calls the same accumulate with the
+    roles swapped — so it runs on the CSR views of Bᵀ and Aᵀ. Returns the CSC
+    arrays of C (as row_ptr/col_idx of Cᵀ) and per-column choices."""
+    if a_csc.cols != b_csc.rows:
+        raise ValueError(f"dimension mismatch: {a_csc.cols} (cols of a) != {b_csc.rows} (rows of b)")
+    bt = _Csr(b_csc.cols, b_csc.rows, b_csc.col_ptr, b_csc.row_idx, b_csc.values)
+    at = _Csr(a_csc.cols, a_csc.rows, a_csc.col_ptr, a_csc.row_idx, a_csc.values)
+    return multiply_rowmajor(bt, at, row_choices=row_choices)

@@ -5,16 +5,23 @@ Gustavson kernel), running as hand-written sm_100a CUDA in libspmmm.so.
 Public surface (mirrors the reference's names for this path):
     multiply_rowmajor, StrategyKind, KernelStats, combined_select,
     CsrMatrix, estimate_nnz, count_mults, install
+and the storage-order neighbours:
+    multiply_colmajor, multiply_mixed, estimate_nnz_csc, CscMatrix,
+    csr_to_csc, csc_to_csr
 """
 
 from ._lib import build as _build_lib
-from .formats import INDEX_DTYPE, VALUE_DTYPE, CsrMatrix, validate_csr
+from .formats import (INDEX_DTYPE, VALUE_DTYPE, CscMatrix, CsrMatrix, csc_to_csr, csr_to_csc,
+                      validate_csr)
 from .install import install
 from .kernels import (
     KernelStats,
     StrategyKind,
     combined_select,
     estimate_nnz,
+    estimate_nnz_csc,
+    multiply_colmajor,
+    multiply_mixed,
     multiply_rowmajor,
     row_products_prefix,
 )
@@ -29,7 +36,8 @@ def build(verbose: bool = False) -> str:
 
 
 __all__ = [
-    "CsrMatrix", "FlopCount", "INDEX_DTYPE", "KernelStats", "StrategyKind", "VALUE_DTYPE",
+    "CscMatrix", "csc_to_csr", "csr_to_csc", "estimate_nnz_csc", "multiply_colmajor",
+    "multiply_mixed", "CsrMatrix", "FlopCount", "INDEX_DTYPE", "KernelStats", "StrategyKind", "VALUE_DTYPE",
     "build", "bytes_alg", "combined_select", "count_mults", "estimate_nnz",
     "inner_loop_balance", "install", "multiply_rowmajor", "roofline", "row_products_prefix",
     "validate_csr",

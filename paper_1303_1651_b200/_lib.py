@@ -40,6 +40,7 @@ EXPORTS = (
     "spmmm_multiply", "spmmm_product_shape", "spmmm_product_device_arrays",
     "spmmm_product_download", "spmmm_product_copy_device", "spmmm_product_row_stats",
     "spmmm_product_destroy", "spmmm_estimate_nnz", "spmmm_row_products_prefix",
+    "spmmm_transpose",
     "spmmm_last_timings", "spmmm_last_launch_count",
     "spmmm_host_alloc", "spmmm_host_free", "spmmm_host_pool_bytes",
     "spmmm_splitmix64", "spmmm_gen_fd_size", "spmmm_gen_fd", "spmmm_gen_fd3_size",
@@ -97,6 +98,7 @@ def _declare(lib):
         "spmmm_estimate_nnz": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr), p_u64]),
         "spmmm_row_products_prefix": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr),
                                           vp]),
+        "spmmm_transpose": (i, [vp, ctypes.POINTER(SpmmmCsr), pp]),
         "spmmm_last_timings": (i, [vp, ctypes.POINTER(ctypes.c_char_p),
                                    ctypes.POINTER(ctypes.c_double), i, ctypes.POINTER(i)]),
         "spmmm_last_launch_count": (i, [vp, ctypes.POINTER(i)]),
@@ -295,6 +297,20 @@ def multiply_views(ctx: Context, a: SpmmmCsr, b: SpmmmCsr, strategy_id: int,
     check(lib().spmmm_multiply(ctx.handle, ctypes.byref(a), ctypes.byref(b), int(strategy_id),
                                int(flags), ctypes.byref(h)), "spmmm_multiply")
     return Product(ctx, h)
+
+
+def transpose_view(ctx: Context, m: SpmmmCsr) -> Product:
+    """CSR of M^T for the CSR view M (spmmm_transpose): the storage-order
+    conversion of formats.py:302-357, on the device."""
+    h = ctypes.c_void_p()
+    check(lib().spmmm_transpose(ctx.handle, ctypes.byref(m), ctypes.byref(h)), "spmmm_transpose")
+    return Product(ctx, h)
+
+
+def product_view(p: Product) -> SpmmmCsr:
+    """Device CSR view of a product's arrays (valid while `p` is open)."""
+    rp, ci, v = p.device_arrays()
+    return device_view(p.rows, p.cols, p.nnz, rp, ci, v)
 
 
 _default_ctx = None

@@ -23,6 +23,7 @@
 
 #include "../../include/spmmm.h"
 #include "aux_kernels.cuh"
+#include "convert.cuh"
 #include "fused_launch.cuh"
 
 using namespace spmmm;
@@ -120,6 +121,7 @@ struct spmmm_context {
   int long_clusters = 0;                     // resident kLongParts-block clusters
   DevBuf sub;                                // per-kernel row sub-lists
   DevBuf ell;                                // ELL records of B (short rows)
+  DevBuf tr_scratch;                         // storage-order conversion scratch
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -859,7 +861,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->gtab, &c->sub, &c->ell, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
+                    &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
@@ -984,6 +986,79 @@ int spmmm_estimate_nnz(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   rc = run_count(c, A, B, tm);
   if (rc) return rc;
   *out = c->h_ctrl[kCtrlTotal];
+  return SPMMM_OK;
+}
+
+int spmmm_transpose(spmmm_context* c, const spmmm_csr* m, spmmm_product** out) {
+  if (!c || !out) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  *out = nullptr;
+  std::lock_guard<std::mutex> lock(c->mu);
+  int rc = check_view(m, "m");
+  if (rc) return rc;
+  if (m->rows >= 0xffffffffull || m->cols >= 0xffffffffull)
+    return fail(SPMMM_ERR_UNSUPPORTED, "conversion needs rows and cols < 2^32 - 1");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->last_launches = 0;
+  DevCsr M;
+  uint64_t base = 0, end = 0;
+  if (m->memory == SPMMM_MEM_DEVICE) {
+    M = DevCsr{m->row_ptr, m->col_idx, m->values, m->rows, m->cols, m->nnz};
+    CUDA_TRY(cudaMemcpyAsync(c->h_ctrl, m->row_ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->h_ctrl + 1, m->row_ptr + m->rows, sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    base = c->h_ctrl[0];
+    end = c->h_ctrl[1];
+  } else {
+    base = m->row_ptr[0];
+    end = m->row_ptr[m->rows];
+    if (base != 0) return fail(SPMMM_ERR_INVALID, "host row_ptr must start at 0");
+    rc = upload(c, m, c->a_rp, c->a_ci, c->a_v, &M);
+    if (rc) return rc;
+  }
+  if (end < base || end > m->nnz)
+    return fail(SPMMM_ERR_INVALID, "malformed row_ptr (row_ptr[rows] < row_ptr[0] or past nnz)");
+  const uint64_t n = end - base;
+  if (n >= 0xffffffffull) return fail(SPMMM_ERR_UNSUPPORTED, "conversion needs nnz < 2^32 - 1");
+  auto* p = new (std::nothrow) spmmm_product;
+  if (!p) return fail(SPMMM_ERR_OOM, "host allocation failed");
+  p->ctx = c;
+  p->rows = m->cols;
+  p->cols = m->rows;
+  p->nnz = n;
+  p->mults = 0;
+  cudaError_t e = cache_alloc(c, (p->rows + 1) * 8, reinterpret_cast<void**>(&p->rp), &p->cap[0]);
+  if (e == cudaSuccess)
+    e = cache_alloc(c, std::max<uint64_t>(n, 1) * 8, reinterpret_cast<void**>(&p->ci), &p->cap[1]);
+  if (e == cudaSuccess)
+    e = cache_alloc(c, std::max<uint64_t>(n, 1) * 8, reinterpret_cast<void**>(&p->v), &p->cap[2]);
+  const size_t sb = transpose_scratch_bytes(n, m->cols);
+  if (e == cudaSuccess) e = ensure(c->tr_scratch, sb, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream);
+  unsigned long long* err = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlError;
+  if (e == cudaSuccess)
+    e = transpose_csr(M, base, n, p->rp, p->ci, p->v, c->tr_scratch.p, c->tr_scratch.cap, err,
+                      c->sms, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->h_ctrl + kCtrlError, err, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                        c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    product_release(c, p);
+    delete p;
+    return fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA, "transpose: %s",
+                cudaGetErrorString(e));
+  }
+  const unsigned long long f = c->h_ctrl[kCtrlError];
+  if (f) {
+    product_release(c, p);
+    delete p;
+    return fail(SPMMM_ERR_INVALID, (f & 2) ? "malformed row_ptr" : "col_idx entry >= cols");
+  }
+  c->last_launches = 4;
+  *out = p;
   return SPMMM_OK;
 }
 

@@ -68,6 +68,87 @@ class CsrMatrix:
         return out
 
 
+@dataclass(eq=False)
+class CscMatrix:
+    """Column-major mirror of CsrMatrix (formats.py:94-140): `col_ptr`
+    (uint64, cols+1), `row_idx` (uint64, nnz), `values` (float64, nnz),
+    strictly increasing rows per column, arrays frozen on construction."""
+
+    rows: int
+    cols: int
+    col_ptr: np.ndarray
+    row_idx: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        _frozen(self.col_ptr)
+        _frozen(self.row_idx)
+        _frozen(self.values)
+
+    @property
+    def nnz(self) -> int:
+        return len(self.values)
+
+    @classmethod
+    def from_arrays(cls, rows, cols, col_ptr, row_idx, values) -> "CscMatrix":
+        return cls(int(rows), int(cols),
+                   np.asarray(col_ptr, dtype=INDEX_DTYPE).copy(),
+                   np.asarray(row_idx, dtype=INDEX_DTYPE).copy(),
+                   np.asarray(values, dtype=VALUE_DTYPE).copy())
+
+    @classmethod
+    def from_dense(cls, dense) -> "CscMatrix":
+        dense = np.asarray(dense, dtype=VALUE_DTYPE)
+        t = CsrMatrix.from_dense(dense.T)
+        return cls(dense.shape[0], dense.shape[1], t.row_ptr, t.col_idx, t.values)
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.rows, self.cols), dtype=VALUE_DTYPE)
+        if self.nnz:
+            per_col = np.diff(self.col_ptr).astype(np.intp)
+            c = np.repeat(np.arange(self.cols), per_col)
+            out[self.row_idx.astype(np.intp), c] = self.values
+        return out
+
+
+def is_csr(m) -> bool:
+    """Row-major operand: anything with `row_ptr` (the reference's CsrMatrix,
+    ours, or a compatible class); column-major: anything with `col_ptr`."""
+    return hasattr(m, "row_ptr")
+
+
+def csc_arrays(m):
+    """(col_ptr, row_idx, values) of any CSC-like object, contiguous."""
+    return (np.ascontiguousarray(m.col_ptr, dtype=INDEX_DTYPE),
+            np.ascontiguousarray(m.row_idx, dtype=INDEX_DTYPE),
+            np.ascontiguousarray(m.values, dtype=VALUE_DTYPE))
+
+
+def _transpose_arrays(n_major, n_minor, ptr, idx, val):
+    """Device transpose of the compressed (ptr, idx, val) structure with
+    n_major slices over n_minor indices: the arrays of the other storage
+    order, minor indices ascending within each new slice (spmmm_transpose)."""
+    from . import _lib
+    ctx = _lib.default_context()
+    view = _lib.csr_view(n_major, n_minor, ptr, idx, val)
+    with _lib.transpose_view(ctx, view) as p:
+        return p.download()
+
+
+def csr_to_csc(a):
+    """formats.py:302-329 on the GPU (stable: rows ascend within each column)."""
+    rp, ci, v = csr_arrays(a)
+    cp, ri, vv = _transpose_arrays(a.rows, a.cols, rp, ci, v)
+    return CscMatrix(a.rows, a.cols, cp, ri, vv)
+
+
+def csc_to_csr(a):
+    """formats.py:332-357 on the GPU (the mirror of csr_to_csc)."""
+    cp, ri, v = csc_arrays(a)
+    rp, ci, vv = _transpose_arrays(a.cols, a.rows, cp, ri, v)
+    return CsrMatrix(a.rows, a.cols, rp, ci, vv)
+
+
 def csr_arrays(m):
     """(row_ptr, col_idx, values) of any CSR-like object as contiguous
     uint64/uint64/float64 arrays (no copy when already in that layout)."""

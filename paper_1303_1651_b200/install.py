@@ -17,9 +17,13 @@ from __future__ import annotations
 import importlib
 import sys
 
-from .kernels import multiply_rowmajor
+from . import kernels as _k
 
 _TARGETS = ("kernels", "bench", "")
+# the entry points replaced wherever a target module binds them
+_NAMES = {"multiply_rowmajor": _k.multiply_rowmajor,
+          "multiply_colmajor": _k.multiply_colmajor,
+          "multiply_mixed": _k.multiply_mixed}
 
 
 class Installation:
@@ -27,8 +31,8 @@ class Installation:
         self._saved = saved
 
     def uninstall(self):
-        for mod, old in self._saved:
-            mod.multiply_rowmajor = old
+        for mod, name, old in self._saved:
+            setattr(mod, name, old)
         self._saved = []
 
     def __enter__(self):
@@ -39,7 +43,8 @@ class Installation:
 
 
 def install(package=None) -> Installation:
-    """Point the reference's `multiply_rowmajor` names at the GPU version."""
+    """Point the reference's `multiply_rowmajor` / `multiply_colmajor` /
+    `multiply_mixed` names at the GPU versions."""
     if package is None:
         package = importlib.import_module("sparsemm")
     name = package.__name__
@@ -52,7 +57,10 @@ def install(package=None) -> Installation:
                 mod = importlib.import_module(modname)
             except ImportError:
                 continue
-        if mod is not None and hasattr(mod, "multiply_rowmajor"):
-            saved.append((mod, mod.multiply_rowmajor))
-            mod.multiply_rowmajor = multiply_rowmajor
+        if mod is None:
+            continue
+        for fname, fn in _NAMES.items():
+            if hasattr(mod, fname):
+                saved.append((mod, fname, getattr(mod, fname)))
+                setattr(mod, fname, fn)
     return Installation(saved)

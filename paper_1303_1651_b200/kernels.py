@@ -28,7 +28,7 @@ from enum import Enum
 import numpy as np
 
 from . import _lib
-from .formats import csr_arrays, make_like
+from .formats import CscMatrix, CsrMatrix, csc_arrays, csr_arrays, is_csr, make_like
 
 
 class StrategyKind(str, Enum):
@@ -153,3 +153,106 @@ def row_products_prefix(a, b) -> np.ndarray:
         ctypes.byref(_lib.csr_view(b.rows, b.cols, brp, bci, bv)), out.ctypes.data),
         "spmmm_row_products_prefix")
     return out
+
+
+# ---------------------------------------------------------------------------
+# Column-major and mixed storage orders.
+#
+# A CSC matrix's arrays are the CSR arrays of its transpose, and
+# multiply_colmajor(A, B) (kernels.py:335-363) accumulates, for each column c
+# of B, column k of A scaled by b[k, c] over B's column entries in ascending k
+# order — exactly the row-major product Bᵀ·Aᵀ on the same arrays, with the
+# same fold order per output entry and the same products (fp multiplication
+# commutes). So the column-major product is the row-major kernel on zero-copy
+# transposed views, bit for bit, with stats recorded per result column.
+
+
+def _dim_check(a, b):
+    if a.cols != b.rows:
+        raise ValueError(f"dimension mismatch: {a.cols} (cols of a) != {b.rows} (rows of b)")
+
+
+def estimate_nnz_csc(a, b) -> int:
+    """formats.py:292-299: Σ over B's entries of the nonzero count of the
+    matching A column (the count pass on the transposed views)."""
+    _dim_check(a, b)
+    if b.nnz == 0:
+        return 0
+    import ctypes
+
+    bp, bi, bv = csc_arrays(b)
+    ap, ai, av = csc_arrays(a)
+    out = ctypes.c_uint64()
+    ctx = _lib.default_context()
+    _lib.check(_lib.lib().spmmm_estimate_nnz(
+        ctx.handle, ctypes.byref(_lib.csr_view(b.cols, b.rows, bp, bi, bv)),
+        ctypes.byref(_lib.csr_view(a.cols, a.rows, ap, ai, av)), ctypes.byref(out)),
+        "spmmm_estimate_nnz")
+    return int(out.value)
+
+
+def _colmajor_views(ctx, a_view, b_view, a, b, strategy, stats, b_major_ptr):
+    sid = _strategy_id(strategy)
+    flags = _lib.FLAG_ROW_STATS if stats is not None else 0
+    # C^T = B^T · A^T: left operand = B's CSC arrays, right = A's
+    with _lib.multiply_views(ctx, b_view, a_view, sid, flags) as product:
+        cp, ri, v = product.download()
+        if stats is not None:
+            stats.multiplications += product.multiplications
+            _record_row_choices(stats, product, _choice_enum(strategy), b_major_ptr)
+    return make_like(a, a.rows, b.cols, cp, ri, v)
+
+
+def multiply_colmajor(a, b, strategy=StrategyKind.COMBINED, stats=None):
+    """Column-major mirror of multiply_rowmajor for two CSC matrices
+    (kernels.py:335-363), on the GPU; returns the left operand's CSC class."""
+    _dim_check(a, b)
+    ap, ai, av = csc_arrays(a)
+    if b is a:
+        bp, bi, bv = ap, ai, av
+    else:
+        bp, bi, bv = csc_arrays(b)
+    ctx = _lib.default_context()
+    a_view = _lib.csr_view(a.cols, a.rows, ap, ai, av)
+    b_view = _lib.csr_view(b.cols, b.rows, bp, bi, bv)
+    return _colmajor_views(ctx, a_view, b_view, a, b, strategy, stats, bp)
+
+
+def multiply_mixed(a, b, strategy=StrategyKind.COMBINED, stats=None):
+    """kernels.py:417-438: same-order pairs go to the matching kernel; for a
+    mixed pair the right operand is converted once (stats.conversions += 1),
+    on the device, and feeds the kernel without a host round trip. The result
+    is in the left operand's storage order."""
+    a_csr, b_csr = is_csr(a), is_csr(b)
+    if a_csr and b_csr:
+        return multiply_rowmajor(a, b, strategy, stats)
+    if not a_csr and not b_csr:
+        return multiply_colmajor(a, b, strategy, stats)
+    _dim_check(a, b)
+    if stats is not None:
+        stats.conversions += 1
+    ctx = _lib.default_context()
+    if a_csr:
+        # B (CSC) -> CSR on the device: its CSC arrays are the CSR of B^T
+        bp, bi, bv = csc_arrays(b)
+        with _lib.transpose_view(ctx, _lib.csr_view(b.cols, b.rows, bp, bi, bv)) as b_rm:
+            arp, aci, av = csr_arrays(a)
+            sid = _strategy_id(strategy)
+            flags = _lib.FLAG_ROW_STATS if stats is not None else 0
+            with _lib.multiply_views(ctx, _lib.csr_view(a.rows, a.cols, arp, aci, av),
+                                     _lib.product_view(b_rm), sid, flags) as product:
+                rp, ci, v = product.download()
+                if stats is not None:
+                    stats.multiplications += product.multiplications
+                    _record_row_choices(stats, product, _choice_enum(strategy), arp)
+        return make_like(a, a.rows, b.cols, rp, ci, v)
+    # A (CSC) with B (CSR): B -> CSC on the device (= the CSR of B^T), then
+    # the column-major product on the views
+    brp, bci, bv = csr_arrays(b)
+    with _lib.transpose_view(ctx, _lib.csr_view(b.rows, b.cols, brp, bci, bv)) as b_cm:
+        ap, ai, av = csc_arrays(a)
+        a_view = _lib.csr_view(a.cols, a.rows, ap, ai, av)
+        # (B's column pointers matter only for the zero-row quirk of stats)
+        b_major_ptr = b_cm.download()[0] if stats is not None and a.rows == 0 else None
+        return _colmajor_views(ctx, a_view, _lib.product_view(b_cm), a, b, strategy, stats,
+                               b_major_ptr)

@@ -7,6 +7,7 @@ GPU box (which has no /root/reference) can check against them:
 
     python tests/golden/make_golden.py small        # -> small_cases.npz  (seconds)
     python tests/golden/make_golden.py full         # -> fingerprints.json (~10 min)
+    python tests/golden/make_golden.py formats      # -> formats_cases.npz (seconds)
 
 * small_cases.npz  every operand pair plus the reference's C = A·B
   (`sparsemm.kernels.multiply_rowmajor`, COMBINED), its KernelStats
@@ -17,6 +18,12 @@ GPU box (which has no /root/reference) can check against them:
   rectangular and empty shapes, signed collision-heavy inputs, and long-row
   inputs (thousands of products per row, with exact cancellations) that
   exercise the long-row path.
+* formats_cases.npz  for a subset of the small cases: the reference's
+  storage-order conversions (csr_to_csc of A and B), its column-major product
+  `multiply_colmajor(A_csc, B_csc)` and both mixed products
+  `multiply_mixed(A, B_csc)` / `multiply_mixed(A_csc, B)` with their
+  KernelStats (multiplications, per-major choices, conversions) and
+  `estimate_nnz_csc` (kernels.py:335-363, 417-438; formats.py:292-357).
 * fingerprints.json  sha256 fingerprints (genmat.py:154-165 plus separate
   structure/value digests) of the full-size BASELINE configs C1..C5, both
   operands and reference products. C1..C3 operands come from the reference's
@@ -245,6 +252,70 @@ def run_small(out_path):
 
 
 # ----------------------------------------------------------------------------
+# storage-order fixtures
+
+
+def formats_subset(cases):
+    keep = ["hand_2x2", "cancellation", "transient_zero", "clean_after_cancelled",
+            "identity_left", "identity_right", "fd3_squared", "rect_7x13_13x5",
+            "rect_1x40_40x1", "rect_40x1_1x40", "quantized_cancel", "all_zero_left",
+            "all_zero_right", "empty_rows_mix", "zero_rows", "zero_inner", "zero_cols_out",
+            "wide_a_short_b"]
+    keep += [f"random_{s}" for s in range(0, 200, 5)] + [f"fd_{g}" for g in (1, 2, 5, 8, 13)]
+    return {k: cases[k] for k in keep}
+
+
+def run_formats(out_path):
+    from sparsemm.formats import csr_to_csc, estimate_nnz_csc
+    from sparsemm.kernels import multiply_colmajor, multiply_mixed
+
+    t0 = time.time()
+    store = {}
+    names = []
+
+    def put_csc(prefix, m):
+        store[f"{prefix}_shape"] = np.array([m.rows, m.cols], np.uint64)
+        store[f"{prefix}_ptr"] = np.asarray(m.col_ptr, np.uint64)
+        store[f"{prefix}_idx"] = np.asarray(m.row_idx, np.uint64)
+        store[f"{prefix}_v"] = np.asarray(m.values, np.float64)
+
+    def put_csr(prefix, m):
+        store[f"{prefix}_shape"] = np.array([m.rows, m.cols], np.uint64)
+        store[f"{prefix}_ptr"] = np.asarray(m.row_ptr, np.uint64)
+        store[f"{prefix}_idx"] = np.asarray(m.col_idx, np.uint64)
+        store[f"{prefix}_v"] = np.asarray(m.values, np.float64)
+
+    def put_stats(prefix, stats, n_major):
+        ch = np.full(n_major, -1, np.int8)
+        for r, c in stats.row_choices:
+            ch[r] = 0 if c is StrategyKind.MIN_MAX else 1
+        store[f"{prefix}_mults"] = np.array([stats.multiplications], np.uint64)
+        store[f"{prefix}_conv"] = np.array([stats.conversions], np.uint64)
+        store[f"{prefix}_choices"] = ch
+
+    for name, (a, b) in formats_subset(small_cases()).items():
+        a_csc, b_csc = csr_to_csc(a), csr_to_csc(b)
+        put_csr(f"{name}/a", a)
+        put_csr(f"{name}/b", b)
+        put_csc(f"{name}/a_csc", a_csc)
+        put_csc(f"{name}/b_csc", b_csc)
+        st = KernelStats()
+        put_csc(f"{name}/col", multiply_colmajor(a_csc, b_csc, StrategyKind.COMBINED, st))
+        put_stats(f"{name}/col", st, b.cols)
+        st = KernelStats()
+        put_csr(f"{name}/mix_rc", multiply_mixed(a, b_csc, StrategyKind.COMBINED, st))
+        put_stats(f"{name}/mix_rc", st, a.rows)
+        st = KernelStats()
+        put_csc(f"{name}/mix_cr", multiply_mixed(a_csc, b, StrategyKind.COMBINED, st))
+        put_stats(f"{name}/mix_cr", st, b.cols)
+        store[f"{name}/estimate_csc"] = np.array([estimate_nnz_csc(a_csc, b_csc)], np.uint64)
+        names.append(name)
+    store["_names"] = np.array(names)
+    np.savez_compressed(out_path, **store)
+    print(f"wrote {out_path}: {len(names)} cases in {time.time() - t0:.1f}s")
+
+
+# ----------------------------------------------------------------------------
 # full-size fingerprints
 
 
@@ -302,5 +373,7 @@ if __name__ == "__main__":
         run_small(os.path.join(HERE, "small_cases.npz"))
     elif mode == "full":
         run_full(os.path.join(HERE, "fingerprints.json"), set(sys.argv[2:]) or None)
+    elif mode == "formats":
+        run_formats(os.path.join(HERE, "formats_cases.npz"))
     else:
-        raise SystemExit("usage: make_golden.py small|full [labels...]")
+        raise SystemExit("usage: make_golden.py small|full|formats [labels...]")

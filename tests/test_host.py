@@ -115,14 +115,21 @@ def test_install_patches_every_reference_name():
     orig = object()
     for m in (pkg, kern, bench):
         m.multiply_rowmajor = orig
+    kern.multiply_colmajor = kern.multiply_mixed = orig
+    pkg.multiply_mixed = orig
     sys.modules.update({"fakesparsemm": pkg, "fakesparsemm.kernels": kern,
                         "fakesparsemm.bench": bench})
+    from paper_1303_1651_b200 import multiply_colmajor, multiply_mixed
     try:
         with install(pkg):
             assert kern.multiply_rowmajor is multiply_rowmajor
             assert bench.multiply_rowmajor is multiply_rowmajor
             assert pkg.multiply_rowmajor is multiply_rowmajor
+            assert kern.multiply_colmajor is multiply_colmajor
+            assert kern.multiply_mixed is multiply_mixed and pkg.multiply_mixed is multiply_mixed
+            assert not hasattr(bench, "multiply_mixed")
         assert kern.multiply_rowmajor is orig and bench.multiply_rowmajor is orig
+        assert kern.multiply_colmajor is orig and kern.multiply_mixed is orig
     finally:
         for n in ("fakesparsemm", "fakesparsemm.kernels", "fakesparsemm.bench"):
             sys.modules.pop(n, None)
