@@ -8,12 +8,14 @@ Public surface (mirrors the reference's names for this path):
 and the storage-order neighbours:
     multiply_colmajor, multiply_mixed, estimate_nnz_csc, CscMatrix,
     csr_to_csc, csc_to_csr
+Matrix Market I/O (native): load_matrix_market, save_matrix_market
 """
 
 from ._lib import build as _build_lib
 from .formats import (INDEX_DTYPE, VALUE_DTYPE, CscMatrix, CsrMatrix, csc_to_csr, csr_to_csc,
                       validate_csr)
 from .install import install
+from .mtxio import load_matrix_market, save_matrix_market
 from .kernels import (
     KernelStats,
     StrategyKind,
@@ -37,7 +39,7 @@ def build(verbose: bool = False) -> str:
 
 __all__ = [
     "CscMatrix", "csc_to_csr", "csr_to_csc", "estimate_nnz_csc", "multiply_colmajor",
-    "multiply_mixed", "CsrMatrix", "FlopCount", "INDEX_DTYPE", "KernelStats", "StrategyKind", "VALUE_DTYPE",
+    "multiply_mixed", "CsrMatrix", "load_matrix_market", "save_matrix_market", "FlopCount", "INDEX_DTYPE", "KernelStats", "StrategyKind", "VALUE_DTYPE",
     "build", "bytes_alg", "combined_select", "count_mults", "estimate_nnz",
     "inner_loop_balance", "install", "multiply_rowmajor", "roofline", "row_products_prefix",
     "validate_csr",

@@ -11,7 +11,8 @@ import pytest
 
 from conftest import ROOT, have_gpu
 
-HEADERS = [os.path.join(ROOT, "include", h) for h in ("spmmm.h", "spmmm_gen.h")]
+HEADERS = sorted(os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include"))
+                 if h.endswith(".h"))
 
 
 def declared_functions():
