@@ -216,11 +216,11 @@ class Context:
         check(lib().spmmm_synchronize(self._h), "spmmm_synchronize")
 
     def last_timings(self) -> dict:
-        names = (ctypes.c_char_p * 8)()
-        ms = (ctypes.c_double * 8)()
+        names = (ctypes.c_char_p * 16)()
+        ms = (ctypes.c_double * 16)()
         n = ctypes.c_int(0)
-        check(lib().spmmm_last_timings(self._h, names, ms, 8, ctypes.byref(n)), "timings")
-        return {names[i].decode(): ms[i] for i in range(min(n.value, 8))}
+        check(lib().spmmm_last_timings(self._h, names, ms, 16, ctypes.byref(n)), "timings")
+        return {names[i].decode(): ms[i] for i in range(min(n.value, 16))}
 
     def last_launch_count(self) -> int:
         n = ctypes.c_int(0)

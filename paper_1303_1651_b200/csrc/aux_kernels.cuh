@@ -31,8 +31,16 @@ enum Ctrl : int {
   kCtrlKMinInv = 19,    // ~(smallest column of A), 0 if A has no entries
   kCtrlKMax1 = 20,      // largest column of A + 1, 0 if none
   kCtrlNnz = 21,        // nnz(C), written by k_fused's last tile
-  kCtrlWords = 24
+  kCtrlHugeProducts = 22, // Σ products of rows past kHugeMin (k_esc_plan scratch size)
+  kCtrlParts = 23,      // column-range parts written by k_esc_plan
+  kCtrlPlanTicket = 24, // k_esc_plan's dynamic row counter
+  kCtrlScrCursor = 25,  // k_esc_plan's scratch allocator (slots)
+  kCtrlWords = 32
 };
+
+// rows past this many products are split into column-range parts in ESC mode
+// (esc.cuh); k_count sums their products for the host
+constexpr uint32_t kHugeMin = 4096;
 
 // ---------------------------------------------------------------------------
 // K1: per-row product counts. formats.py:276-289 per row. A warp takes 32
@@ -47,7 +55,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
        i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = 0;
   const uint32_t lane = lane_id();
-  uint64_t tot = 0, mx = 0, nonshort = 0, bmax = 0, kmin = ~0ull, kmax1 = 0;
+  uint64_t tot = 0, mx = 0, nonshort = 0, bmax = 0, kmin = ~0ull, kmax1 = 0, huge = 0;
   uint32_t need = 0, err = 0;
   const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
   const uint64_t gw = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -116,6 +124,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       if (p > 0x7fffffffull) err |= 8u;
       prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
       tot += p;
+      huge += p > kHugeMin ? p : 0;
       mx = p > mx ? p : mx;
       if (p > 32 || (p > 0 && hi - lo > 32)) {
         need = 1;
@@ -132,6 +141,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
     const uint64_t ok1 = __shfl_xor_sync(kFull, kmax1, d);
     kmax1 = ok1 > kmax1 ? ok1 : kmax1;
     tot += __shfl_xor_sync(kFull, tot, d);
+    huge += __shfl_xor_sync(kFull, huge, d);
     nonshort += __shfl_xor_sync(kFull, nonshort, d);
     const uint64_t o = __shfl_xor_sync(kFull, mx, d);
     mx = o > mx ? o : mx;
@@ -140,7 +150,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
   }
   // block-level combine, then one set of atomics per block (same-address
   // atomics from every warp serialise in L2)
-  __shared__ unsigned long long s_red[8][8];
+  __shared__ unsigned long long s_red[9][8];
   const uint32_t warp = threadIdx.x >> 5;
   if (lane == 0) {
     s_red[0][warp] = tot;
@@ -151,14 +161,15 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
     s_red[5][warp] = kmax1;
     s_red[6][warp] = need;
     s_red[7][warp] = err;
+    s_red[8][warp] = huge;
   }
   __syncthreads();
-  if (threadIdx.x < 8) {
+  if (threadIdx.x < 9) {
     const uint32_t f = threadIdx.x;
     unsigned long long x = 0;
     for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
       const unsigned long long y = s_red[f][w];
-      x = f < 2 ? x + y : (f < 6 ? (y > x ? y : x) : (x | y));
+      x = (f < 2 || f == 8) ? x + y : (f < 6 ? (y > x ? y : x) : (x | y));
     }
     if (x) {
       switch (f) {
@@ -169,6 +180,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
         case 4: atomicMax(ctrl + kCtrlKMinInv, x); break;
         case 5: atomicMax(ctrl + kCtrlKMax1, x); break;
         case 6: atomicOr(ctrl + kCtrlNeedTable, 1ull); break;
+        case 8: atomicAdd(ctrl + kCtrlHugeProducts, x); break;
         default: atomicOr(ctrl + kCtrlError, x); break;
       }
     }
@@ -278,6 +290,12 @@ __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __res
 // lookup idea, kernels.py:106-113 / 216-227, on the GPU).
 constexpr int kLongThreads = 512;
 
+struct PartDesc {  // one column range of a huge row, products staged in q order
+  uint32_t li;     // list index of the row
+  uint32_t cnt;    // products in the range
+  uint64_t off;    // first scratch slot
+};
+
 struct LongParams {
   DevCsr A, B;
   const uint32_t* prod;
@@ -299,6 +317,17 @@ struct LongParams {
   const unsigned long long* n_sub;    // their count
   unsigned long long* ticket;         // dynamic row counter
   uint32_t* ovf;                      // cluster variant: rows handed on to k_long
+  // ESC mode (esc.cuh): column-range parts of the huge rows
+  struct PartDesc* parts;             // [max parts]
+  uint64_t* part_off;                 // staging offset per part
+  uint32_t* part_nnz;                 // entries per part
+  uint32_t* row_pbase;                // per huge-list position: first part
+  uint32_t* row_np;                   // per huge-list position: parts (0: whole row staged)
+  const uint32_t* huge;               // huge sub-list
+  uint32_t* scr_col;                  // part scratch: columns
+  double* scr_val;                    // part scratch: products
+  uint64_t scr_cap;                   // scratch slots
+  uint64_t max_parts;
   uint32_t* st_min;
   uint32_t* st_max;
   uint32_t* st_touch;
@@ -583,6 +612,10 @@ struct CopyParams {
   double* c_v;
   uint64_t rows;
   uint32_t long_min;         // rows past it are in the sub-lists
+  const uint32_t* row_np;    // ESC mode: parts per huge row (else null)
+  const uint32_t* row_pbase;
+  const uint64_t* part_off;
+  const uint32_t* part_nnz;
 };
 
 // Copy the staged rows into their slots of C (after k_fused wrote row_ptr).
@@ -601,6 +634,22 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
     if (t >= n_big) break;
     const uint32_t li = t < n_mid ? p.big[t] : p.big[p.rows + (t - n_mid)];
     const uint64_t dst = p.c_rp[p.list[li]];
+    const uint32_t np = (t >= n_mid && p.row_np) ? p.row_np[t - n_mid] : 0u;
+    if (np) {  // ESC parts of a huge row, in column order
+      const uint32_t pb = p.row_pbase[t - n_mid];
+      uint64_t d = dst;
+      for (uint32_t j = 0; j < np; ++j) {
+        const uint64_t so = p.part_off[pb + j];
+        const uint32_t pc = p.part_nnz[pb + j];
+        for (uint32_t i = threadIdx.x; i < pc; i += blockDim.x) {
+          __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + d + i,
+                 (unsigned long long)__ldcs(p.l_ci + so + i));
+          __stcs(p.c_v + d + i, __ldcs(p.l_v + so + i));
+        }
+        d += pc;
+      }
+      continue;
+    }
     const uint64_t src = p.l_off[li];
     const uint32_t cnt = p.l_nnz[li];
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {

@@ -1,0 +1,804 @@
+// Split-mode rows by expand–sort–compress (ESC), for skewed inputs (C5).
+//
+// In split mode the non-short rows are computed before k_fused and staged
+// (see run_long in spmmm.cu). When a row's products hit mostly distinct
+// columns — C5's rows are random, nnz(C) ≈ products — a hash table is pure
+// overhead: every product is inserted once and the table must still be sorted
+// afterwards. ESC instead
+//   expand:   writes every product of the row to shared memory in product
+//             order q (q runs through (k, j) in A-entry order, i.e. the
+//             reference's k order, kernels.py:163-180): value p_q = fl(a·b)
+//             indexed by q, key (column, q);
+//   sort:     sorts the keys by (column, q) — equal columns stay in q order;
+//   compress: folds each run of equal columns left to right from 0.0 with
+//             separately rounded adds (the reference's dense[x] += p) and
+//             keeps a run iff its sum != 0.0 (kernels.py:296-298).
+// So C[r, x] is bit-identical to the reference, like every other path.
+//
+//   k_esc_warp:  rows of <= kEscWarpLimit products, one warp per row, keys
+//                sorted in registers (runtime-loop bitonic network).
+//   k_esc_block: rows of (kEscWarpLimit, cap] products, one block per row:
+//                one counting pass partitions the keys into column-range
+//                buckets of ~32 (so a bucket is a small independent sort),
+//                one warp sorts and folds each bucket in registers.
+// Keys are 32-bit: (column << 9 | q) in the warp kernel (columns < 2^23,
+// checked on the host), (column offset in bucket << qbits | q) in the block
+// kernel.
+#pragma once
+
+#include "aux_kernels.cuh"
+#include "kernels.cuh"
+
+namespace spmmm {
+
+constexpr int kEscWarps = 8;
+constexpr int kEscQBits = 9;
+constexpr uint32_t kEscWarpLimit = 1u << kEscQBits;  // products per warp row
+constexpr int kEscColBits = 32 - kEscQBits;           // columns < 2^23
+
+constexpr int kEscThreads = 512;
+constexpr uint32_t kEscBucketAvg = 32;  // target keys per bucket
+constexpr uint32_t kEscMaxBuckets = 1024;
+// rows of (kEscWarpLimit, kEscBlockCap] products; two blocks per SM. In-bucket
+// keys: qb = log2(cap) = 12 bits of q, so a bucket spans <= 2^20 columns
+// (nb >= 32 buckets over < 2^23 columns: <= 2^18).
+constexpr uint32_t kEscBlockCap = kHugeMin;
+
+__host__ __device__ constexpr size_t esc_warp_smem_bytes() {
+  return size_t(kEscWarps) * kEscWarpLimit * (sizeof(uint32_t) + sizeof(double));
+}
+
+// ---- register bitonic sort of a run of keys in shared memory -----------------
+// E*32 keys, E per lane (element e*32 + lane). E = 1, 2: the fully unrolled
+// network (device.cuh); larger E: the stage loops run at run time and only
+// the per-element work is unrolled (small code — the sizes vary per row).
+template <int JE, int E>
+__device__ __forceinline__ void bitonic_reg_exchange(uint32_t (&key)[E], uint32_t k) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if ((e & JE) == 0) {
+      const int e2 = e | JE;
+      const bool up = ((uint32_t(e) << 5) & k) == 0;
+      const uint32_t a = key[e], b = key[e2];
+      key[e] = keep_minmax(a, b, up);
+      key[e2] = keep_minmax(a, b, !up);
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void bitonic_loop(uint32_t (&key)[E]) {
+  const uint32_t lane = lane_id();
+#pragma unroll 1
+  for (uint32_t k = 2; k <= uint32_t(E) * 32u; k <<= 1) {
+#pragma unroll 1
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const uint32_t je = j >> 5;
+        if constexpr (E > 1) { if (je == 1) bitonic_reg_exchange<1>(key, k); }
+        if constexpr (E > 2) { if (je == 2) bitonic_reg_exchange<2>(key, k); }
+        if constexpr (E > 4) { if (je == 4) bitonic_reg_exchange<4>(key, k); }
+        if constexpr (E > 8) { if (je == 8) bitonic_reg_exchange<8>(key, k); }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t p = __shfl_xor_sync(kFull, key[e], j);
+          const bool up = (((uint32_t(e) << 5) | lane) & k) == 0;
+          key[e] = keep_minmax(key[e], p, lower == up);
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void sort_run_fixed(uint32_t* kb, uint32_t n) {
+  const uint32_t lane = lane_id();
+  uint32_t key[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t idx = uint32_t(e) * 32u + lane;
+    key[e] = idx < n ? kb[idx] : kEmptyKey;
+  }
+  if constexpr (E <= 2) bitonic_sort<E>(key);
+  else bitonic_loop<E>(key);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t idx = uint32_t(e) * 32u + lane;
+    if (idx < n) kb[idx] = key[e];
+  }
+}
+
+__device__ void warp_sort_smem(uint32_t* k, uint32_t n);
+
+// Sort kb[0..n) ascending in place (warp-collective, n warp-uniform).
+__device__ __forceinline__ void sort_run(uint32_t* kb, uint32_t n) {
+  if (n <= 32) sort_run_fixed<1>(kb, n);
+  else if (n <= 64) sort_run_fixed<2>(kb, n);
+  else if (n <= 128) sort_run_fixed<4>(kb, n);
+  else if (n <= 256) sort_run_fixed<8>(kb, n);
+  else if (n <= 512) sort_run_fixed<16>(kb, n);
+  else warp_sort_smem(kb, n);
+  __syncwarp();
+}
+
+// In-place ascending sort of n keys in shared memory by one warp, for any n
+// (buckets that outgrow the register sort: clustered columns). Bitonic with
+// the "flip" first step, so every comparator is ascending and the virtual
+// +inf padding past n never moves — pairs reaching past n are skipped.
+__device__ __noinline__ void warp_sort_smem(uint32_t* k, uint32_t n) {
+  const uint32_t lane = lane_id();
+  uint32_t np = 1;
+  while (np < n) np <<= 1;
+  for (uint32_t m = 2; m <= np; m <<= 1) {
+    // flip: i pairs with i ^ (m - 1) inside each block of m
+    for (uint32_t t = lane; t < np / 2; t += 32) {
+      const uint32_t i = (t / (m / 2)) * m + (t % (m / 2));
+      const uint32_t pj = i ^ (m - 1);
+      if (pj < n) {
+        const uint32_t a = k[i], b = k[pj];
+        if (a > b) { k[i] = b; k[pj] = a; }
+      }
+    }
+    __syncwarp();
+    for (uint32_t j = m / 4; j > 0; j >>= 1) {
+      for (uint32_t t = lane; t < np / 2; t += 32) {
+        const uint32_t i = 2 * t - (t & (j - 1));
+        if (i + j < n) {
+          const uint32_t a = k[i], b = k[i + j];
+          if (a > b) { k[i] = b; k[i + j] = a; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ---- the fold over a sorted run of keys --------------------------------------
+// keys[0..n) sorted by (column part << qb | q); vals indexed by q. For
+// element i of this lane: head = first of its column run; acc = left fold of
+// the run from 0.0 in q order. Returns the head flag.
+template <bool STATS>
+__device__ __forceinline__ bool fold_at(const uint32_t* keys, const double* vals, uint32_t n,
+                                        uint32_t i, uint32_t qb, double& acc,
+                                        uint32_t& touches) {
+  const uint32_t qmask = (1u << qb) - 1u;
+  const uint32_t key = keys[i];
+  const uint32_t col = key >> qb;
+  const bool head = i == 0 || (keys[i - 1] >> qb) != col;
+  acc = 0.0;
+  if (head) {
+    acc = __dadd_rn(0.0, vals[key & qmask]);  // dense[x] == 0.0: a touch
+    if (STATS) ++touches;
+    for (uint32_t j = i + 1; j < n; ++j) {
+      const uint32_t kj = keys[j];
+      if ((kj >> qb) != col) break;
+      if (STATS && acc == 0.0) ++touches;  // re-touch after an exact zero
+      acc = __dadd_rn(acc, vals[kj & qmask]);
+    }
+  }
+  return head;
+}
+
+// ---- k_esc_warp ----------------------------------------------------------------
+template <bool STATS>
+__global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams p_in) {
+  extern __shared__ __align__(16) unsigned char esc_sm[];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  double* sval = reinterpret_cast<double*>(esc_sm) + warp * kEscWarpLimit;
+  uint32_t* skey =
+      reinterpret_cast<uint32_t*>(esc_sm + kEscWarps * kEscWarpLimit * sizeof(double)) +
+      warp * kEscWarpLimit;
+  RowsParams p = p_in;
+  p.B.pol = policy_evict_last();
+  p.A.pol = policy_evict_first();
+  const uint64_t n_list = *p.n_list;
+#pragma unroll 1
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.ticket, 1ull);
+    const uint64_t li = __shfl_sync(kFull, t, 0);
+    if (li >= n_list) break;
+    const uint32_t r = p.list[li];
+    const uint32_t P = p.prod[r];
+    if (P > kEscWarpLimit) continue;  // block kernel
+    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
+    // ---- expand: product q -> skey[q] = col << 9 | q, sval[q] = a * b ----
+    uint32_t base = 0;
+#pragma unroll 1
+    for (uint64_t ab = lo; ab < hi; ab += 32) {
+      const uint32_t na = uint32_t(hi - ab < 32 ? hi - ab : 32);
+      uint64_t bs = 0;
+      uint32_t len = 0;
+      double av = 0.0;
+      if (lane < na) {
+        const uint64_t k = ld_idx(p.A.ci + ab + lane, p.A.pol);
+        av = ld_val(p.A.v + ab + lane, p.A.pol);
+        bs = ld_idx(p.B.rp + k, p.B.pol);
+        len = uint32_t(ld_idx(p.B.rp + k + 1, p.B.pol) - bs);
+      }
+      const uint32_t incl = warp_incl_scan(len);
+      const uint32_t excl = incl - len;
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);  // lanes past na: len 0
+      // four chunks of 32 products per round: their loads are in flight together
+#pragma unroll 1
+      for (uint32_t c = 0; c < tot; c += 128) {
+        uint32_t col[4];
+        double bv[4], a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = c + 32u * u + lane;
+          int i = 0;  // owner: the largest entry with excl <= q
+#pragma unroll
+          for (int st = 16; st > 0; st >>= 1) {
+            const uint32_t ex = __shfl_sync(kFull, excl, i + st);
+            if (ex <= q) i += st;
+          }
+          const uint64_t src = __shfl_sync(kFull, bs, i) + (q - __shfl_sync(kFull, excl, i));
+          a[u] = __shfl_sync(kFull, av, i);
+          col[u] = 0;
+          bv[u] = 0.0;
+          if (q < tot) {
+            col[u] = uint32_t(ld_idx(p.B.ci + src, p.B.pol));
+            bv[u] = ld_val(p.B.v + src, p.B.pol);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = c + 32u * u + lane;
+          if (q < tot) {
+            skey[base + q] = (col[u] << kEscQBits) | (base + q);
+            sval[base + q] = __dmul_rn(a[u], bv[u]);
+          }
+        }
+      }
+      base += tot;
+    }
+    __syncwarp();
+    // ---- sort (column, q) ----
+    sort_run(skey, P);
+    // ---- compress: fold runs, drop exact zeros, write out in column order ----
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)P);  // upper bound
+    off = __shfl_sync(kFull, off, 0);
+    uint32_t cnt = 0, touches = 0;
+#pragma unroll 1
+    for (uint32_t i0 = 0; i0 < P; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      double acc = 0.0;
+      bool keep = false;
+      if (i < P) keep = fold_at<STATS>(skey, sval, P, i, kEscQBits, acc, touches) && acc != 0.0;
+      const uint32_t m = __ballot_sync(kFull, keep);
+      if (keep) {
+        const uint64_t pos = off + cnt + __popc(m & lanemask_lt());
+        __stcs(p.l_ci + pos, uint64_t(skey[i] >> kEscQBits));
+        __stcs(p.l_v + pos, acc);
+      }
+      cnt += __popc(m);
+    }
+    if (STATS) {
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) touches += __shfl_xor_sync(kFull, touches, d);
+    }
+    if (lane == 0) {
+      p.l_off[li] = off;
+      p.l_nnz[li] = cnt;
+      if (STATS) {
+        p.st_min[r] = skey[0] >> kEscQBits;
+        p.st_max[r] = skey[P - 1] >> kEscQBits;
+        p.st_touch[r] = touches;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- k_esc_plan ------------------------------------------------------------------
+// Huge rows (> kHugeMin products): one block per row cuts the row's column
+// range [cmin, cmax] into nparts equal ranges (~kPartTarget products each)
+// and stages every product, in q order, into its part's scratch region. Each
+// part is then an independent k_esc_block work item of <= kEscBlockCap
+// products; a column lives in exactly one part, so its fold order is
+// untouched. The row's A entries are cut into one contiguous segment per
+// warp (segments are contiguous in q); pass 1 counts each warp's products per
+// part, a scan over warps gives every (warp, part) its first slot, pass 2
+// stages the products (chunks of 32 in q order, ranks in lane order: a
+// stable scatter). A row whose busiest part outgrows its region (columns far
+// from uniform over the range), or that finds the scratch full, goes to
+// k_long instead.
+constexpr uint32_t kPartTarget = kEscBlockCap / 2;
+constexpr uint32_t kMaxParts = 64;
+constexpr int kPlanThreads = 512;
+
+// One warp's segment [e0, e1) of A entries: count (SCATTER = false) or stage
+// (SCATTER = true) its products per part. cnt: this warp's per-part counters
+// (pass 1) or next free slot (pass 2).
+template <bool SCATTER>
+__device__ __forceinline__ void plan_segment(const LongParams& pp, uint64_t es, uint64_t ehi,
+                                             uint32_t gq, uint32_t qs, uint32_t qe, uint32_t cmn,
+                                             uint32_t width, uint32_t region, uint64_t sbase,
+                                             uint32_t* cnt) {
+  const uint32_t lane = lane_id();
+  // entries from es (whose first product is row product gq) until product qe
+#pragma unroll 1
+  for (uint64_t ab = es; ab < ehi && gq < qe; ab += 32) {
+    const uint32_t na = uint32_t(ehi - ab < 32 ? ehi - ab : 32);
+    uint64_t bs = 0;
+    uint32_t len = 0;
+    double av = 0.0;
+    if (lane < na) {
+      const uint64_t k = ld_idx(pp.A.ci + ab + lane, pp.A.pol);
+      if (SCATTER) av = ld_val(pp.A.v + ab + lane, pp.A.pol);
+      bs = ld_idx(pp.B.rp + k, pp.B.pol);
+      len = uint32_t(ld_idx(pp.B.rp + k + 1, pp.B.pol) - bs);
+    }
+    const uint32_t incl = warp_incl_scan(len);
+    const uint32_t excl = incl - len;
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    // this segment's products of the group: local q in [qlo, qhi)
+    const uint32_t qlo = qs > gq ? qs - gq : 0u;
+    const uint32_t qhi = qe - gq < tot ? qe - gq : tot;
+    gq += tot;
+#pragma unroll 1
+    for (uint32_t c = qlo; c < qhi; c += 128) {
+      uint32_t col[4];
+      double bv[4], a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t q = c + 32u * u + lane;
+        int i = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const uint32_t ex = __shfl_sync(kFull, excl, i + st);
+          if (ex <= q) i += st;
+        }
+        const uint64_t src = __shfl_sync(kFull, bs, i) + (q - __shfl_sync(kFull, excl, i));
+        a[u] = SCATTER ? __shfl_sync(kFull, av, i) : 0.0;
+        col[u] = 0;
+        bv[u] = 0.0;
+        if (q < qhi) {
+          col[u] = uint32_t(ld_idx(pp.B.ci + src, pp.B.pol));
+          if (SCATTER) bv[u] = ld_val(pp.B.v + src, pp.B.pol);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t q = c + 32u * u + lane;
+        const bool act = q < qhi;
+        const uint32_t part = act ? (col[u] - cmn) / width : kEmptyKey;
+        const uint32_t peers = __match_any_sync(kFull, part);
+        const uint32_t leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (act && lane == leader) {
+          old = cnt[part];
+          cnt[part] = old + __popc(peers);
+        }
+        if (SCATTER) {
+          const uint32_t pos = __shfl_sync(kFull, old, leader) + __popc(peers & lanemask_lt());
+          if (act) {
+            const uint64_t slot = sbase + uint64_t(part) * region + pos;
+            __stcg(pp.scr_col + slot, col[u]);
+            __stcg(pp.scr_val + slot, __dmul_rn(a[u], bv[u]));
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(kPlanThreads, 2) k_esc_plan(LongParams p) {
+  constexpr int NW = kPlanThreads / 32;
+  __shared__ uint32_t s_cnt[NW][kMaxParts];
+  __shared__ uint32_t s_h, s_min, s_max, s_over;
+  __shared__ unsigned long long s_sbase;
+  __shared__ uint64_t s_seg_e[NW];
+  __shared__ uint32_t s_seg_q[NW];
+  __shared__ uint32_t s_scan[NW + 1];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = lane_id();
+  LongParams pp = p;
+  pp.B.pol = policy_evict_last();
+  pp.A.pol = policy_evict_first();
+  const uint32_t n_huge = uint32_t(p.ctrl[kCtrlHugeRows]);
+#pragma unroll 1
+  while (true) {
+    if (tid == 0) {
+      s_h = uint32_t(atomicAdd(p.ctrl + kCtrlPlanTicket, 1ull));
+      s_min = kEmptyKey;
+      s_max = 0;
+      s_over = 0;
+    }
+    __syncthreads();
+    const uint32_t h = s_h;
+    if (h >= n_huge) break;
+    const uint32_t li = p.huge[h];
+    const uint32_t r = p.list[li];
+    const uint32_t P = p.prod[r];
+    const uint64_t lo = ld_idx(pp.A.rp + r), hi = ld_idx(pp.A.rp + r + 1);
+    // column range of the row (first and last column of every B row), and
+    // where each warp's equal share of the row's products starts: the entry
+    // holding product qs_w = w*P/NW and that entry's first product
+    uint32_t cmn = kEmptyKey, cmx = 0, run = 0;
+#pragma unroll 1
+    for (uint64_t e0 = lo; e0 < hi; e0 += kPlanThreads) {
+      const uint64_t e = e0 + tid;
+      uint64_t bs = 0, be = 0;
+      if (e < hi) {
+        const uint64_t k = ld_idx(pp.A.ci + e, pp.A.pol);
+        bs = ld_idx(pp.B.rp + k, pp.B.pol);
+        be = ld_idx(pp.B.rp + k + 1, pp.B.pol);
+      }
+      if (be > bs) {
+        const uint32_t c0 = uint32_t(ld_idx(pp.B.ci + bs, pp.B.pol));
+        const uint32_t c1 = uint32_t(ld_idx(pp.B.ci + be - 1, pp.B.pol));
+        cmn = c0 < cmn ? c0 : cmn;
+        cmx = c1 > cmx ? c1 : cmx;
+      }
+      const uint32_t len = uint32_t(be - bs);
+      uint32_t total;
+      const uint32_t ex = run + block_excl_scan<kPlanThreads>(len, s_scan, total);
+      if (len) {
+#pragma unroll 1
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t qs = uint32_t(uint64_t(w) * P / NW);
+          if (ex <= qs && qs < ex + len) {
+            s_seg_e[w] = e;
+            s_seg_q[w] = ex;
+          }
+        }
+      }
+      run += total;
+    }
+    cmn = __reduce_min_sync(kFull, cmn);
+    cmx = __reduce_max_sync(kFull, cmx);
+    if (lane == 0) {
+      atomicMin(&s_min, cmn);
+      atomicMax(&s_max, cmx);
+    }
+    for (uint32_t j = lane; j < kMaxParts; j += 32) s_cnt[warp][j] = 0;
+    __syncthreads();
+    cmn = s_min;
+    cmx = s_max;
+    uint32_t nparts = (P + kPartTarget - 1) / kPartTarget;
+    nparts = nparts < kMaxParts ? nparts : kMaxParts;
+    const uint32_t width = (cmx - cmn) / nparts + 1;
+    // region per part: 5/4 of the mean part plus slack, at most a block's cap
+    uint32_t region = P / nparts + P / nparts / 4 + 64;
+    region = region < kEscBlockCap ? region : kEscBlockCap;
+    // this warp's segment of A entries
+    // this warp's products [qs, qe) of the row, starting in entry es
+    const uint32_t qs = uint32_t(uint64_t(warp) * P / NW);
+    const uint32_t qe = uint32_t(uint64_t(warp + 1) * P / NW);
+    const uint64_t es = s_seg_e[warp];
+    const uint32_t gq = s_seg_q[warp];
+    plan_segment<false>(pp, es, hi, gq, qs, qe, cmn, width, region, 0, s_cnt[warp]);
+    __syncthreads();
+    // per part: exclusive scan over warps -> each warp's first slot
+    if (tid < nparts) {
+      uint32_t run = 0;
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t c = s_cnt[w][tid];
+        s_cnt[w][tid] = run;
+        run += c;
+      }
+      if (run > region) atomicOr(&s_over, 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t sb = 0;
+      if (!s_over) {
+        sb = atomicAdd(p.ctrl + kCtrlScrCursor, (unsigned long long)nparts * region);
+        if (sb + uint64_t(nparts) * region > p.scr_cap) s_over = 1;
+      }
+      s_sbase = sb;
+      if (s_over) {
+        p.ovf[atomicAdd(p.ctrl + kCtrlOvfRows, 1ull)] = li;
+        p.row_np[h] = 0;
+      }
+    }
+    __syncthreads();
+    const bool over = s_over != 0;
+    __syncthreads();  // everyone has read s_over before the loop head resets it
+    if (over) continue;
+    const uint64_t sbase = s_sbase;
+    plan_segment<true>(pp, es, hi, gq, qs, qe, cmn, width, region, sbase, s_cnt[warp]);
+    __syncthreads();
+    // after pass 2 the last warp's cursors are the part totals
+    if (warp == 0) {
+      uint32_t nz = 0;
+      for (uint32_t j0 = 0; j0 < nparts; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        nz += __popc(__ballot_sync(kFull, j < nparts && s_cnt[NW - 1][j] > 0));
+      }
+      unsigned long long pbase = 0;
+      if (lane == 0) pbase = atomicAdd(p.ctrl + kCtrlParts, (unsigned long long)nz);
+      pbase = __shfl_sync(kFull, pbase, 0);
+      uint32_t rank = 0;
+      for (uint32_t j0 = 0; j0 < nparts; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const uint32_t tot = j < nparts ? s_cnt[NW - 1][j] : 0u;
+        const uint32_t m = __ballot_sync(kFull, tot > 0);
+        if (tot > 0) {
+          PartDesc d;
+          d.li = li;
+          d.cnt = tot;
+          d.off = sbase + uint64_t(j) * region;
+          p.parts[pbase + rank + __popc(m & lanemask_lt())] = d;
+        }
+        rank += __popc(m);
+      }
+      if (lane == 0) {
+        p.row_pbase[h] = uint32_t(pbase);
+        p.row_np[h] = nz;
+        p.l_nnz[li] = 0;
+        if (STATS) {
+          p.st_min[r] = cmn;
+          p.st_max[r] = cmx;
+          p.st_touch[r] = 0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- k_esc_block ---------------------------------------------------------------
+
+__host__ __device__ constexpr size_t esc_block_smem_bytes(uint32_t cap) {
+  return size_t(cap) * (sizeof(double) + 2 * sizeof(uint32_t)) +
+         size_t(kEscMaxBuckets) * 3 * sizeof(uint32_t);
+}
+
+// Rows of (kEscWarpLimit, cap] products (LongParams.sub), one block per row.
+template <bool STATS>
+__global__ void __launch_bounds__(kEscThreads, 2) k_esc_block(LongParams p, uint32_t cap) {
+  constexpr int NT = kEscThreads;
+  extern __shared__ __align__(16) unsigned char esc_sm[];
+  double* sval = reinterpret_cast<double*>(esc_sm);               // [cap] by q
+  uint32_t* scol = reinterpret_cast<uint32_t*>(sval + cap);       // [cap] column by q
+  uint32_t* bkey = scol + cap;                                    // [cap] bucketed keys
+  uint32_t* hist = bkey + cap;                                    // [kEscMaxBuckets]
+  uint32_t* start = hist + kEscMaxBuckets;                        // bucket starts
+  uint32_t* kept = start + kEscMaxBuckets;                        // kept per bucket, then out offsets
+  __shared__ uint32_t s_excl[NT + 1];
+  __shared__ uint64_t s_bs[NT];
+  __shared__ double s_av[NT];
+  __shared__ uint32_t s_scan[NT / 32 + 1];
+  __shared__ uint32_t s_li, s_min, s_max, s_touch, s_bt;
+  __shared__ unsigned long long s_off;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  uint32_t qb = 1;
+  while ((1u << qb) < cap) ++qb;
+  LongParams pp = p;
+  pp.B.pol = policy_evict_last();
+  pp.A.pol = policy_evict_first();
+  const uint32_t n_sub = uint32_t(*(volatile const unsigned long long*)p.n_sub);
+  const uint32_t n_parts =
+      p.parts ? uint32_t(*(volatile const unsigned long long*)(p.ctrl + kCtrlParts)) : 0u;
+#pragma unroll 1
+  while (true) {
+    if (tid == 0) {
+      s_li = uint32_t(atomicAdd(p.ticket, 1ull));
+      s_min = kEmptyKey;
+      s_max = 0;
+      s_touch = 0;
+    }
+    __syncthreads();
+    const uint32_t t_row = s_li;
+    if (t_row >= n_sub + n_parts) break;
+    // work item: a whole mid row, or one column-range part of a huge row
+    const bool is_part = t_row >= n_sub;
+    uint32_t li, P;
+    uint64_t scr = 0;
+    if (is_part) {
+      const PartDesc d = p.parts[t_row - n_sub];
+      li = d.li;
+      P = d.cnt;
+      scr = d.off;
+    } else {
+      li = p.sub[t_row];
+    }
+    const uint32_t r = p.list[li];
+    if (!is_part) P = p.prod[r];
+    const uint64_t lo = is_part ? 0 : ld_idx(pp.A.rp + r), hi = is_part ? 0 : ld_idx(pp.A.rp + r + 1);
+    uint32_t base = 0, cmn = kEmptyKey, cmx = 0;
+    // part: its products are staged in q order by k_esc_plan
+    for (uint32_t i = tid; is_part && i < P; i += NT) {
+      const uint32_t c = __ldcs(p.scr_col + scr + i);
+      scol[i] = c;
+      sval[i] = __ldcs(p.scr_val + scr + i);
+      cmn = c < cmn ? c : cmn;
+      cmx = c > cmx ? c : cmx;
+    }
+    // ---- expand (whole rows) ----
+#pragma unroll 1
+    for (uint64_t ab = lo; ab < hi; ab += NT) {
+      const uint64_t e = ab + tid;
+      uint32_t len = 0;
+      uint64_t bs = 0;
+      double av = 0.0;
+      if (e < hi) {
+        const uint64_t k = ld_idx(pp.A.ci + e, pp.A.pol);
+        av = ld_val(pp.A.v + e, pp.A.pol);
+        bs = ld_idx(pp.B.rp + k, pp.B.pol);
+        len = uint32_t(ld_idx(pp.B.rp + k + 1, pp.B.pol) - bs);
+      }
+      uint32_t total;
+      const uint32_t ex = block_excl_scan<NT>(len, s_scan, total);
+      s_excl[tid] = ex;
+      s_bs[tid] = bs;
+      s_av[tid] = av;
+      if (tid == 0) s_excl[NT] = total;
+      __syncthreads();
+#pragma unroll 1
+      for (uint32_t c = 0; c < total; c += 4 * NT) {
+        uint32_t col[4];
+        double bv[4], a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = c + uint32_t(u) * NT + tid;
+          col[u] = 0;
+          bv[u] = 0.0;
+          a[u] = 0.0;
+          if (q < total) {
+            int i = 0;
+#pragma unroll
+            for (int st = NT / 2; st > 0; st >>= 1)
+              if (s_excl[i + st] <= q) i += st;
+            const uint64_t src = s_bs[i] + (q - s_excl[i]);
+            a[u] = s_av[i];
+            col[u] = uint32_t(ld_idx(pp.B.ci + src, pp.B.pol));
+            bv[u] = ld_val(pp.B.v + src, pp.B.pol);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = c + uint32_t(u) * NT + tid;
+          if (q < total) {
+            scol[base + q] = col[u];
+            sval[base + q] = __dmul_rn(a[u], bv[u]);
+            cmn = col[u] < cmn ? col[u] : cmn;
+            cmx = col[u] > cmx ? col[u] : cmx;
+          }
+        }
+      }
+      base += total;
+      __syncthreads();  // s_excl / s_bs / s_av reused by the next A chunk
+    }
+    cmn = __reduce_min_sync(kFull, cmn);
+    cmx = __reduce_max_sync(kFull, cmx);
+    if (lane == 0) {
+      atomicMin(&s_min, cmn);
+      atomicMax(&s_max, cmx);
+    }
+    // buckets: nb (power of two) column ranges of 2^sh columns from cmin,
+    // ~kEscBucketAvg keys each; in-bucket key = offset << qb | q
+    uint32_t nb = 2;
+    while (nb * kEscBucketAvg < P && nb < kEscMaxBuckets) nb <<= 1;
+    for (uint32_t b = tid; b < nb; b += NT) hist[b] = 0;
+    if (tid == 0) s_bt = NT / 32;  // buckets below were taken statically
+    __syncthreads();
+    const uint32_t cmin = s_min, range = s_max - cmin;
+    uint32_t sh = 0;
+    while ((range >> sh) >= nb) ++sh;
+    // ---- partition: histogram, bucket starts, scatter ----
+    for (uint32_t q = tid; q < P; q += NT) atomicAdd(hist + ((scol[q] - cmin) >> sh), 1u);
+    __syncthreads();
+    {
+      const uint32_t h0 = 2 * tid < nb ? hist[2 * tid] : 0u;
+      const uint32_t h1 = 2 * tid + 1 < nb ? hist[2 * tid + 1] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<NT>(h0 + h1, s_scan, tot);
+      if (2 * tid < nb) {
+        start[2 * tid] = ex;
+        kept[2 * tid] = ex;  // scatter cursors for now
+      }
+      if (2 * tid + 1 < nb) {
+        start[2 * tid + 1] = ex + h0;
+        kept[2 * tid + 1] = ex + h0;
+      }
+    }
+    __syncthreads();
+    const uint32_t omask = (1u << sh) - 1u;
+    for (uint32_t q = tid; q < P; q += NT) {
+      const uint32_t rel = scol[q] - cmin;
+      const uint32_t pos = atomicAdd(kept + (rel >> sh), 1u);
+      bkey[pos] = ((rel & omask) << qb) | q;
+    }
+    __syncthreads();
+    // ---- per bucket (one warp): sort, fold; heads' sums go to sval[q] ----
+    uint32_t touches = 0;
+#pragma unroll 1
+    // buckets taken dynamically (sort costs vary with the bucket size)
+    for (uint32_t b = warp;;) {
+      if (b >= nb) break;
+      const uint32_t sz = hist[b];
+      uint32_t* kb = bkey + start[b];
+      if (sz > 1) sort_run(kb, sz);
+      uint32_t cnt = 0;
+      for (uint32_t i0 = 0; i0 < sz; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        double acc = 0.0;
+        bool head = false;
+        if (i < sz) {
+          head = fold_at<STATS>(kb, sval, sz, i, qb, acc, touches);
+          if (head) sval[kb[i] & ((1u << qb) - 1u)] = acc;  // only this head reads it again
+        }
+        cnt += __popc(__ballot_sync(kFull, head && acc != 0.0));
+      }
+      if (lane == 0) kept[b] = cnt;
+      uint32_t nb2 = 0;
+      if (lane == 0) nb2 = atomicAdd(&s_bt, 1u);
+      b = __shfl_sync(kFull, nb2, 0);
+    }
+    __syncthreads();
+    // ---- output offsets per bucket, then the row ----
+    uint32_t n_out;
+    {
+      const uint32_t k0 = 2 * tid < nb ? kept[2 * tid] : 0u;
+      const uint32_t k1 = 2 * tid + 1 < nb ? kept[2 * tid + 1] : 0u;
+      const uint32_t ex = block_excl_scan<NT>(k0 + k1, s_scan, n_out);
+      if (STATS) {
+        uint32_t t = touches;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
+        if (lane == 0 && t) atomicAdd(&s_touch, t);
+      }
+      if (2 * tid < nb) kept[2 * tid] = ex;
+      if (2 * tid + 1 < nb) kept[2 * tid + 1] = ex + k0;
+    }
+    if (tid == 0) {
+      s_off = n_out ? atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)n_out) : 0ull;
+      if (is_part) {
+        p.part_off[t_row - n_sub] = s_off;
+        p.part_nnz[t_row - n_sub] = n_out;
+        atomicAdd(p.l_nnz + li, n_out);  // the row's total (zeroed by k_esc_plan)
+      } else {
+        p.l_off[li] = s_off;
+        p.l_nnz[li] = n_out;
+      }
+    }
+    __syncthreads();
+    const uint64_t off = s_off;
+#pragma unroll 1
+    for (uint32_t b = warp; b < nb; b += NT / 32) {
+      const uint32_t sz = hist[b];
+      const uint32_t* kb = bkey + start[b];
+      const uint32_t blo = cmin + (b << sh);
+      uint32_t o = kept[b];
+      for (uint32_t i0 = 0; i0 < sz; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool keep = false;
+        uint32_t key = 0;
+        double v = 0.0;
+        if (i < sz) {
+          key = kb[i];
+          const bool head = i == 0 || (kb[i - 1] >> qb) != (key >> qb);
+          v = sval[key & ((1u << qb) - 1u)];
+          keep = head && v != 0.0;
+        }
+        const uint32_t m = __ballot_sync(kFull, keep);
+        if (keep) {
+          const uint64_t pos = off + o + __popc(m & lanemask_lt());
+          __stcs(p.l_ci + pos, uint64_t(blo + (key >> qb)));
+          __stcs(p.l_v + pos, v);
+        }
+        o += __popc(m);
+      }
+    }
+    if (STATS && tid == 0) {
+      if (is_part) {  // range set by k_esc_plan
+        atomicAdd(p.st_touch + r, s_touch);
+      } else {
+        p.st_min[r] = cmin;
+        p.st_max[r] = s_max;
+        p.st_touch[r] = s_touch;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace spmmm

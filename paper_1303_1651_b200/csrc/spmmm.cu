@@ -24,6 +24,7 @@
 #include "../../include/spmmm.h"
 #include "aux_kernels.cuh"
 #include "convert.cuh"
+#include "esc.cuh"
 #include "fused_launch.cuh"
 
 using namespace spmmm;
@@ -96,8 +97,9 @@ void release(DevBuf& b, cudaStream_t s) {
 }
 
 const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
-                                    "k_rows", "k_long_smem", "k_long_cluster", "k_pack_ell"};
-constexpr int kNumKernels = 9;
+                                    "k_rows", "k_long_smem", "k_long_cluster", "k_pack_ell",
+                                    "k_esc_warp", "k_esc_block", "k_esc_plan"};
+constexpr int kNumKernels = 12;
 
 }  // namespace
 
@@ -118,10 +120,12 @@ struct spmmm_context {
   DevBuf stage_ci, stage_v;  // staged pre-computed rows (run_long -> k_copy_long)
   bool long_smem_attr[2] = {false, false};  // k_long_smem opt-in smem set
   bool rows_attr[2] = {false, false};       // k_rows opt-in smem set
+  bool esc_attr[2] = {false, false};        // k_esc_* opt-in smem set
   int long_clusters = 0;                     // resident kLongParts-block clusters
   DevBuf sub;                                // per-kernel row sub-lists
   DevBuf ell;                                // ELL records of B (short rows)
   DevBuf tr_scratch;                         // storage-order conversion scratch
+  DevBuf parts, part_off, part_nnz, row_parts, scr_col, scr_val;  // ESC parts of huge rows
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -420,7 +424,8 @@ int launch_long_smem(spmmm_context* c, const LongParams& lp, bool cluster) {
 // k_collect (rows of class long for `list_limit`), staged with their nnz, and
 // copied into place by k_copy_long after k_fused.
 int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_prod,
-             uint32_t list_limit, bool split, uint64_t total, bool stats, spmmm_product* p,
+             uint32_t list_limit, bool split, bool esc, uint64_t total, bool stats,
+             spmmm_product* p,
              DevBuf& stage_ci, DevBuf& stage_v, Timer& tm) {
   const Trace tr;
   const uint64_t rows = A.rows;
@@ -432,13 +437,16 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   uint32_t* mid_list = static_cast<uint32_t*>(c->sub.p);
   uint32_t* huge_list = mid_list + rows;
   uint32_t* ovf_list = mid_list + 2 * rows;
-  // split mode: k_rows takes rows up to kRowsLimit; else k_fused up to kMediumLimit
-  const uint32_t long_min = split ? kRowsLimit : kMediumLimit;
+  // split mode: k_rows (k_esc_warp) takes rows up to kRowsLimit
+  // (kEscWarpLimit); else k_fused up to kMediumLimit
+  const uint32_t long_min = esc ? kEscWarpLimit : split ? kRowsLimit : kMediumLimit;
+  // rows past huge_min: the cluster variant (and k_long for its overflow)
+  const uint32_t huge_min = esc ? kEscBlockCap : kLongSmemProducts;
   tr.mark("  run_long: lists");
   CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
   tr.mark("  run_long: buffers");
-  const bool any_huge = max_prod > kLongSmemProducts;  // some row needs k_long
+  const bool any_huge = max_prod > huge_min;  // some row needs the cluster / k_long
   // workspace: one table (>= 2x the distinct columns a row can have) and one
   // column bitmap per resident block
   uint64_t distinct = std::min<uint64_t>(max_prod, std::max<uint64_t>(B.cols, 1));
@@ -469,7 +477,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(1);
     k_collect<<<unsigned(blocks), 256, 0, c->stream>>>(
-        A, static_cast<const uint32_t*>(c->prod.p), list_limit, long_min, kLongSmemProducts,
+        A, static_cast<const uint32_t*>(c->prod.p), list_limit, long_min, huge_min,
         static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p), mid_list, huge_list,
         static_cast<unsigned long long*>(c->ctrl.p));
     CUDA_TRY(cudaGetLastError());
@@ -492,6 +500,27 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     rp.st_min = p->st;
     rp.st_max = p->st ? p->st + rows : nullptr;
     rp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+    if (esc) {
+      const size_t smem = esc_warp_smem_bytes();
+      if (!c->esc_attr[stats]) {  // once per context (device)
+        auto set = [&](const void* f, size_t bytes) {
+          return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+        };
+        CUDA_TRY(set(reinterpret_cast<const void*>(stats ? k_esc_warp<true> : k_esc_warp<false>),
+                     smem));
+        CUDA_TRY(set(reinterpret_cast<const void*>(stats ? k_esc_block<true> : k_esc_block<false>),
+                     esc_block_smem_bytes(kEscBlockCap)));
+        c->esc_attr[stats] = true;
+      }
+      const unsigned grid_rows = unsigned(c->sms) * 4;
+      tm.begin(9);
+      if (stats) k_esc_warp<true><<<grid_rows, kEscWarps * 32, smem, c->stream>>>(rp);
+      else k_esc_warp<false><<<grid_rows, kEscWarps * 32, smem, c->stream>>>(rp);
+      CUDA_TRY(cudaGetLastError());
+      tm.end(9);
+      ++c->last_launches;
+      tr.mark("  run_long: k_esc_warp launched");
+    } else {
     const size_t smem = rows_smem_bytes();
     if (!c->rows_attr[stats]) {  // once per context (device)
       if (stats)
@@ -510,6 +539,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     tm.end(5);
     ++c->last_launches;
     tr.mark("  run_long: k_rows launched");
+    }
   }
   if (max_prod <= long_min) return SPMMM_OK;
   LongParams lp;
@@ -536,16 +566,68 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   lp.st_touch = p->st ? p->st + 2 * rows : nullptr;
   unsigned long long* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
   lp.ovf = ovf_list;
+  lp.parts = nullptr;
+  lp.part_off = nullptr;
+  lp.part_nnz = nullptr;
+  lp.row_pbase = nullptr;
+  lp.row_np = nullptr;
+  lp.huge = huge_list;
+  lp.scr_col = nullptr;
+  lp.scr_val = nullptr;
+  lp.scr_cap = 0;
+  lp.max_parts = 0;
+  if (esc && any_huge) {
+    // parts: sum over huge rows of ceil(P / kPartTarget) <= 1.5 * huge / kPartTarget;
+    // scratch slots <= 1.25 * huge + 64 per part (k_esc_plan's regions)
+    const uint64_t huge = c->h_ctrl[kCtrlHugeProducts];
+    const uint64_t max_parts = huge / (kPartTarget / 2) + 16;
+    const uint64_t max_rows = huge / kHugeMin + 16;
+    const uint64_t slots = huge + huge / 2 + 4096;
+    CUDA_TRY(ensure(c->parts, max_parts * sizeof(PartDesc), c->stream));
+    CUDA_TRY(ensure(c->part_off, max_parts * sizeof(uint64_t), c->stream));
+    CUDA_TRY(ensure(c->part_nnz, max_parts * sizeof(uint32_t), c->stream));
+    CUDA_TRY(ensure(c->row_parts, 2 * max_rows * sizeof(uint32_t), c->stream));
+    CUDA_TRY(ensure(c->scr_col, slots * sizeof(uint32_t), c->stream));
+    CUDA_TRY(ensure(c->scr_val, slots * sizeof(double), c->stream));
+    lp.parts = static_cast<PartDesc*>(c->parts.p);
+    lp.part_off = static_cast<uint64_t*>(c->part_off.p);
+    lp.part_nnz = static_cast<uint32_t*>(c->part_nnz.p);
+    lp.row_pbase = static_cast<uint32_t*>(c->row_parts.p);
+    lp.row_np = lp.row_pbase + max_rows;
+    lp.scr_col = static_cast<uint32_t*>(c->scr_col.p);
+    lp.scr_val = static_cast<double*>(c->scr_val.p);
+    lp.scr_cap = slots;
+    lp.max_parts = max_parts;
+  }
   // rows of (long_min, kLongSmemProducts] products: a block and on-chip tables
   lp.sub = mid_list;
   lp.n_sub = ctrl + kCtrlMidRows;
   lp.ticket = ctrl + kCtrlLongSmemTicket;
-  tm.begin(6);
-  int rc = stats ? launch_long_smem<true>(c, lp, false) : launch_long_smem<false>(c, lp, false);
-  if (rc) return rc;
-  tm.end(6);
+  int rc = SPMMM_OK;
+  if (esc) {
+    if (any_huge) {
+      tm.begin(11);
+      if (stats) k_esc_plan<true><<<c->sms * 2, kPlanThreads, 0, c->stream>>>(lp);
+      else k_esc_plan<false><<<c->sms * 2, kPlanThreads, 0, c->stream>>>(lp);
+      CUDA_TRY(cudaGetLastError());
+      tm.end(11);
+      ++c->last_launches;
+    }
+    const size_t smem = esc_block_smem_bytes(kEscBlockCap);
+    tm.begin(10);
+    if (stats) k_esc_block<true><<<c->sms * 2, kEscThreads, smem, c->stream>>>(lp, kEscBlockCap);
+    else k_esc_block<false><<<c->sms * 2, kEscThreads, smem, c->stream>>>(lp, kEscBlockCap);
+    CUDA_TRY(cudaGetLastError());
+    tm.end(10);
+  } else {
+    tm.begin(6);
+    rc = stats ? launch_long_smem<true>(c, lp, false) : launch_long_smem<false>(c, lp, false);
+    if (rc) return rc;
+    tm.end(6);
+  }
   ++c->last_launches;
   if (any_huge) {
+    if (!esc) {
     // longer rows: a cluster of blocks per row, one column range each
     lp.sub = huge_list;
     lp.n_sub = ctrl + kCtrlHugeRows;
@@ -555,6 +637,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     if (rc) return rc;
     tm.end(7);
     ++c->last_launches;
+    }
     // rows whose column ranges outgrew the on-chip tables: global tables
     lp.sub = ovf_list;
     lp.n_sub = ctrl + kCtrlOvfRows;
@@ -617,6 +700,10 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   // C4) medium rows are computed inline by the medium variant.
   const uint64_t nonshort = c->h_ctrl[kCtrlNonShort];
   const bool split = need_table && nonshort * 4 <= rows;
+  // split-mode rows by expand-sort-compress (esc.cuh) when the 32-bit sort
+  // keys can hold the columns; SPMMM_NO_ESC=1 keeps the hash-table kernels
+  static const bool no_esc = std::getenv("SPMMM_NO_ESC") != nullptr;
+  const bool esc = split && !no_esc && B.cols <= (1ull << kEscColBits);
   const bool medium = need_table && !split;
   const uint32_t medium_limit = medium ? kMediumLimit : 0u;
   const int pos_bits = medium ? kPosBits : 5;
@@ -663,7 +750,8 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   auto fail_staged = [&](int code) { return cleanup(code); };
   const bool has_long = split || (medium && max_prod > medium_limit);
   if (rows && has_long) {
-    rc = run_long(c, A, B, max_prod, medium_limit, split, total, stats, p, stage_ci, stage_v, tm);
+    rc = run_long(c, A, B, max_prod, medium_limit, split, esc, total, stats, p, stage_ci,
+                  stage_v, tm);
     if (rc) return fail_staged(rc);
     tr.mark("long rows launched");
   }
@@ -752,7 +840,12 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       cp.c_ci = p->ci;
       cp.c_v = p->v;
       cp.rows = rows;
-      cp.long_min = split ? kRowsLimit : kMediumLimit;
+      cp.long_min = esc ? kEscWarpLimit : split ? kRowsLimit : kMediumLimit;
+      const bool parts = esc && max_prod > kEscBlockCap;
+      cp.row_pbase = parts ? static_cast<const uint32_t*>(c->row_parts.p) : nullptr;
+      cp.row_np = parts ? cp.row_pbase + (c->h_ctrl[kCtrlHugeProducts] / kHugeMin + 16) : nullptr;
+      cp.part_off = parts ? static_cast<const uint64_t*>(c->part_off.p) : nullptr;
+      cp.part_nnz = parts ? static_cast<const uint32_t*>(c->part_nnz.p) : nullptr;
       k_copy_long<<<c->sms * 8, 256, 0, c->stream>>>(cp);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "k_copy_long: %s",

@@ -264,3 +264,73 @@ def test_full_size_config_matches_reference(label):
     assert d["row_ptr_sha256"] == fp["c"]["row_ptr_sha256"]
     assert d["col_idx_sha256"] == fp["c"]["col_idx_sha256"]
     assert d["values_sha256"] == fp["c"]["values_sha256"]
+
+
+def _skewed_csr(rng, rows, cols, lmax, values, window=None, far_every=0):
+    """Zipf(2) row lengths clipped to [1, lmax] (C5's shape at test size).
+    `window`: columns crowd into [0, window) (duplicate-heavy products);
+    `far_every`: every n-th row also gets the last column (wide column range
+    around a narrow cluster: oversized sort buckets)."""
+    lens = np.minimum(rng.zipf(2.0, rows), lmax)
+    span = cols if window is None else min(window, cols)
+    lens = np.minimum(lens, span - 1)
+    rp = np.zeros(rows + 1, np.uint64)
+    rp[1:] = np.cumsum(lens)
+    parts = []
+    for r in range(rows):
+        c = rng.choice(span - 1, lens[r], replace=False) if lens[r] > 64 else \
+            np.unique(rng.integers(0, span - 1, lens[r] * 2))[:lens[r]]
+        while c.size < lens[r]:
+            c = np.unique(np.concatenate([c, rng.integers(0, span - 1, lens[r])]))[:lens[r]]
+        if far_every and r % far_every == 0 and c.size:
+            c[-1] = cols - 1
+        parts.append(np.sort(c))
+    ci = np.concatenate(parts).astype(np.uint64)
+    lens = np.array([p.size for p in parts])
+    rp[1:] = np.cumsum(lens)
+    if values == "quantized":  # exact cancellations and transient zeros
+        v = rng.choice([-2.0, -1.0, 1.0, 2.0], ci.size)
+    else:
+        v = rng.uniform(-1.0, 1.0, ci.size)
+    return CsrMatrix(rows, cols, rp, ci, v)
+
+
+@pytest.mark.parametrize("case", ["random", "dups", "clustered"])
+@pytest.mark.parametrize("values", ["uniform", "quantized"])
+def test_split_mode_esc_kernels(case, values):
+    """Skewed operands (non-short rows a minority): split mode, with the
+    expand-sort-compress kernels for rows up to kEscBlockCap products (warp
+    rows, block rows with ~32-key buckets, oversized buckets) and the cluster
+    variant past it. Bitwise against the oracle, stats included; the ESC
+    kernels must actually have run."""
+    rng = np.random.default_rng({"random": 1, "dups": 2, "clustered": 3}[case])
+    n = 30_000
+    if case == "random":
+        a = _skewed_csr(rng, n, n, 3000, values)
+        b = _skewed_csr(rng, n, 2_000_000, 200, values)
+    elif case == "dups":
+        a = _skewed_csr(rng, n, n, 3000, values)
+        b = _skewed_csr(rng, n, 5000, 200, values, window=3000)
+    else:
+        a = _skewed_csr(rng, n, n, 3000, values)
+        b = _skewed_csr(rng, n, 5_000_000, 100, values, window=4000, far_every=3)
+    ref = oracle.multiply_rowmajor(a, b, row_choices=True, threads=8)
+    ctx = _lib.Context(0)
+    arp, aci, av = a.row_ptr, a.col_idx, a.values
+    brp, bci, bv = b.row_ptr, b.col_idx, b.values
+    va = _lib.csr_view(a.rows, a.cols, arp, aci, av)
+    vb = _lib.csr_view(b.rows, b.cols, brp, bci, bv)
+    with _lib.multiply_views(ctx, va, vb, 6, _lib.FLAG_TIMING | _lib.FLAG_ROW_STATS) as p:
+        rp, ci, v = p.download()
+        names = set(ctx.last_timings())
+        stats = KernelStats()
+        from paper_1303_1651_b200.kernels import _record_row_choices
+        _record_row_choices(stats, p, StrategyKind, arp)
+        mults = p.multiplications
+    ctx.close()
+    assert {"k_esc_warp", "k_esc_block", "k_esc_plan"} <= names, names
+    assert mults == ref.multiplications
+    assert_csr_bitwise_equal(CsrMatrix(a.rows, b.cols, rp, ci, v),
+                             CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx, ref.values),
+                             f"esc/{case}/{values}")
+    assert np.array_equal(_choices_array(stats, a.rows), ref.row_choices)
