@@ -106,6 +106,27 @@ int spmmm_product_device_arrays(const spmmm_product* p, const uint64_t** row_ptr
 /* Copies C into caller-owned host buffers (rows+1, nnz, nnz entries). */
 int spmmm_product_download(spmmm_product* p, uint64_t* row_ptr, uint64_t* col_idx,
                            double* values);
+
+/* Result of spmmm_multiply_host: C in page-locked host memory from the
+ * library's pool (return each array with spmmm_host_free). col_idx / values
+ * hold `nnz` entries (their blocks may be larger). */
+typedef struct {
+  uint64_t rows, cols, nnz, mults;
+  uint64_t* row_ptr;
+  uint64_t* col_idx;
+  double* values;
+} spmmm_host_csr;
+
+/* C = A·B for HOST operands, block-pipelined: A's and B's structure go up
+ * first and one count pass validates and sizes the product; then A's values go
+ * up in `blocks` row blocks (<= 16) while each block is computed as soon as
+ * the B rows it reads are resident, and its part of C streams down — uploads,
+ * kernels and downloads overlap. Same bytes, errors and multiplication count
+ * as spmmm_multiply + spmmm_product_download (kernels.py:302-332); row stats
+ * are not available here (use spmmm_multiply). Replaces, like spmmm_multiply,
+ * sparsemm.kernels.multiply_rowmajor (kernels.py:302-332) for the drop-in. */
+int spmmm_multiply_host(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b, int strategy,
+                        uint32_t flags, int blocks, spmmm_host_csr* out);
 /* Same, into caller-owned DEVICE buffers on the product's device (ordered on
  * the context stream; e.g. tensors that a collective then sends). */
 int spmmm_product_copy_device(spmmm_product* p, uint64_t* row_ptr, uint64_t* col_idx,

@@ -37,7 +37,7 @@ FLAG_TIMING = 2
 EXPORTS = (
     "spmmm_abi_version", "spmmm_last_error", "spmmm_device_count",
     "spmmm_context_create", "spmmm_context_destroy", "spmmm_synchronize",
-    "spmmm_multiply", "spmmm_product_shape", "spmmm_product_device_arrays",
+    "spmmm_multiply", "spmmm_multiply_host", "spmmm_product_shape", "spmmm_product_device_arrays",
     "spmmm_product_download", "spmmm_product_copy_device", "spmmm_product_row_stats",
     "spmmm_product_destroy", "spmmm_estimate_nnz", "spmmm_row_products_prefix",
     "spmmm_transpose",
@@ -48,6 +48,19 @@ EXPORTS = (
     "spmmm_mtx_last_error", "spmmm_mtx_write", "spmmm_mtx_read", "spmmm_mtx_shape",
     "spmmm_mtx_copy", "spmmm_mtx_free",
 )
+
+
+class SpmmmHostCsr(ctypes.Structure):
+    """spmmm_host_csr (include/spmmm.h): a result in pinned pool memory."""
+    _fields_ = [
+        ("rows", ctypes.c_uint64),
+        ("cols", ctypes.c_uint64),
+        ("nnz", ctypes.c_uint64),
+        ("mults", ctypes.c_uint64),
+        ("row_ptr", ctypes.c_void_p),
+        ("col_idx", ctypes.c_void_p),
+        ("values", ctypes.c_void_p),
+    ]
 
 
 class SpmmmCsr(ctypes.Structure):
@@ -94,6 +107,8 @@ def _declare(lib):
         "spmmm_product_shape": (i, [vp, p_u64, p_u64, p_u64, p_u64]),
         "spmmm_product_device_arrays": (i, [vp, pp, pp, pp]),
         "spmmm_product_download": (i, [vp, vp, vp, vp]),
+        "spmmm_multiply_host": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr), i,
+                                    ctypes.c_uint32, i, ctypes.POINTER(SpmmmHostCsr)]),
         "spmmm_product_copy_device": (i, [vp, vp, vp, vp]),
         "spmmm_product_row_stats": (i, [vp, vp, vp, vp]),
         "spmmm_product_destroy": (i, [vp]),
@@ -305,6 +320,32 @@ def multiply_views(ctx: Context, a: SpmmmCsr, b: SpmmmCsr, strategy_id: int,
     check(lib().spmmm_multiply(ctx.handle, ctypes.byref(a), ctypes.byref(b), int(strategy_id),
                                int(flags), ctypes.byref(h)), "spmmm_multiply")
     return Product(ctx, h)
+
+
+def _pool_array(ptr: int, n: int, dtype) -> np.ndarray:
+    """numpy view of n elements of a pinned pool block (freed with the array)."""
+    import weakref
+
+    dtype = np.dtype(dtype)
+    nbytes = max(int(n) * dtype.itemsize, 1)
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    weakref.finalize(buf, lib().spmmm_host_free, ctypes.c_void_p(ptr))
+    return np.frombuffer(buf, dtype=dtype, count=int(n))
+
+
+def multiply_host(ctx: Context, a: SpmmmCsr, b: SpmmmCsr, strategy_id: int, flags: int = 0,
+                  blocks: int = 8):
+    """spmmm_multiply_host: block-pipelined C = A·B of host operands.
+    Returns (row_ptr, col_idx, values, multiplications) as numpy arrays in
+    pinned pool memory."""
+    out = SpmmmHostCsr()
+    check(lib().spmmm_multiply_host(ctx.handle, ctypes.byref(a), ctypes.byref(b),
+                                    int(strategy_id), int(flags), int(blocks),
+                                    ctypes.byref(out)), "spmmm_multiply_host")
+    rp = _pool_array(out.row_ptr, out.rows + 1, np.uint64)
+    ci = _pool_array(out.col_idx, out.nnz, np.uint64)
+    v = _pool_array(out.values, out.nnz, np.float64)
+    return rp, ci, v, int(out.mults)
 
 
 def transpose_view(ctx: Context, m: SpmmmCsr) -> Product:

@@ -100,6 +100,7 @@ const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused",
                                     "k_rows", "k_long_smem", "k_long_cluster", "k_pack_ell",
                                     "k_esc_warp", "k_esc_block", "k_esc_plan"};
 constexpr int kNumKernels = 12;
+constexpr int kMaxPipeBlocks = 16;  // spmmm_multiply_host row blocks
 
 }  // namespace
 
@@ -126,6 +127,11 @@ struct spmmm_context {
   DevBuf ell;                                // ELL records of B (short rows)
   DevBuf tr_scratch;                         // storage-order conversion scratch
   DevBuf parts, part_off, part_nnz, row_parts, scr_col, scr_val;  // ESC parts of huge rows
+  // spmmm_multiply_host: copy streams (uploads, downloads) and their events
+  cudaStream_t s_up = nullptr, s_down = nullptr;
+  cudaEvent_t pev[3 * kMaxPipeBlocks + 2] = {};
+  DevBuf aux;                          // per-block max columns
+  unsigned long long* h_aux = nullptr; // pinned mirror
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -268,6 +274,24 @@ struct Timer {
   }
 };
 
+// ---- small readbacks -----------------------------------------------------------
+// Control words reach the host through a kernel storing into page-locked host
+// memory (UVA-mapped), not cudaMemcpy: in the pipelined host path the copy
+// engine is busy streaming C down, and a tiny memcpy would queue behind it.
+__global__ void k_readback(const unsigned long long* __restrict__ src,
+                           unsigned long long* __restrict__ host, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    volatile unsigned long long* h = host + i;
+    *h = src[i];
+  }
+}
+
+cudaError_t readback(const unsigned long long* dsrc, unsigned long long* hdst, int n,
+                     cudaStream_t s) {
+  k_readback<<<1, 64, 0, s>>>(dsrc, hdst, n);
+  return cudaGetLastError();
+}
+
 // ---- the count pass ----------------------------------------------------------
 
 // Look-back state of k_fused: the level-1.. counters first (zeroed by k_count
@@ -311,8 +335,8 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
     tm.end(0);
     ++c->last_launches;
   }
-  CUDA_TRY(cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, kCtrlWords * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(readback(static_cast<const unsigned long long*>(c->ctrl.p), c->h_ctrl, kCtrlWords,
+                    c->stream));
   CUDA_TRY(cudaEventRecord(c->ev_count, c->stream));
   if (pack && A.rows) {
     // the ELL copy of B (if k_count's results call for it) overlaps the readback
@@ -858,9 +882,8 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   // one read-back: the watchdog word through nnz(C) (rows == 0: nnz is 0)
   static_assert(kCtrlNnz > kCtrlFault, "ctrl layout");
   if (!rows) c->h_ctrl[kCtrlNnz] = 0;
-  e = cudaMemcpyAsync(c->h_ctrl + kCtrlFault, static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault,
-                      (rows ? kCtrlNnz - kCtrlFault + 1 : 1) * sizeof(uint64_t),
-                      cudaMemcpyDeviceToHost, c->stream);
+  e = readback(static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlFault, c->h_ctrl + kCtrlFault,
+               rows ? kCtrlNnz - kCtrlFault + 1 : 1, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
   if (c->h_ctrl[kCtrlFault]) {
@@ -882,6 +905,265 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   return SPMMM_OK;
 }
 
+
+// ---- block-pipelined product of host operands (spmmm_multiply_host) ---------
+//
+// PCIe, not the kernels, bounds a product whose operands and result live on
+// the host (C2: 0.37 GB up, 0.91 GB down against ~1.5 ms of kernels). The
+// structure of A and B goes up first and one count pass sizes everything;
+// then A's values go up in G row blocks while block j is computed (as soon as
+// every B row it reads is resident) and block j's C streams down, so uploads,
+// kernels and downloads overlap (PCIe is full duplex). Each block is the
+// ordinary device product of a row block of A (rows are independent,
+// kernels.py:323-329); its row_ptr is shifted by the nnz before it on the
+// device and it lands at its offset in one result, so the bytes are those
+// of spmmm_multiply.
+
+constexpr int kPipeSplit = 64;
+
+struct PipeBounds {
+  uint64_t r[kMaxPipeBlocks + 1];
+};
+
+__global__ void k_block_maxcol(const uint64_t* __restrict__ rp, const uint64_t* __restrict__ ci,
+                               const PipeBounds bounds, unsigned long long* __restrict__ out) {
+  // kPipeSplit blocks per row block, each a slice of its entries
+  const uint32_t j = blockIdx.x / kPipeSplit, part = blockIdx.x % kPipeSplit;
+  const uint64_t e0 = rp[bounds.r[j]], e1 = rp[bounds.r[j + 1]];
+  uint64_t m = 0;
+  for (uint64_t e = e0 + uint64_t(part) * blockDim.x + threadIdx.x; e < e1;
+       e += uint64_t(kPipeSplit) * blockDim.x)
+    m = ci[e] > m ? ci[e] : m;
+  m = __reduce_max_sync(0xffffffffu, uint32_t(m));  // columns < 2^32 (checked)
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out + j, (unsigned long long)m);
+}
+
+__global__ void k_zero_u64(uint64_t* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+
+__global__ void k_add_offset(uint64_t* __restrict__ rp, uint64_t n, uint64_t off) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    rp[i] += off;
+}
+
+int pipe_setup(spmmm_context* c) {
+  if (c->s_up) return SPMMM_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s_up, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s_down, cudaStreamNonBlocking));
+  for (cudaEvent_t& ev : c->pev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaMallocHost(&c->h_aux, 2 * kMaxPipeBlocks * sizeof(unsigned long long)));
+  return SPMMM_OK;
+}
+
+int host_alloc_internal(uint64_t bytes, void** ptr) { return spmmm_host_alloc(bytes, ptr); }
+int host_free_internal(void* ptr) { return ptr ? spmmm_host_free(ptr) : SPMMM_OK; }
+
+int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
+                       uint32_t flags, int blocks, spmmm_host_csr* out) {
+  if (!out) return fail(SPMMM_ERR_INVALID, "out is NULL");
+  if (strategy < SPMMM_STRATEGY_BFDOUBLE || strategy > SPMMM_STRATEGY_COMBINED)
+    return fail(SPMMM_ERR_INVALID, "unknown strategy %d", strategy);
+  int rc = check_view(a, "a");
+  if (rc) return rc;
+  rc = check_view(b, "b");
+  if (rc) return rc;
+  if (a->memory != SPMMM_MEM_HOST || b->memory != SPMMM_MEM_HOST)
+    return fail(SPMMM_ERR_INVALID, "spmmm_multiply_host takes host operands");
+  if (flags & SPMMM_FLAG_ROW_STATS)
+    return fail(SPMMM_ERR_INVALID, "row stats need spmmm_multiply");
+  if (a->cols != b->rows)
+    return fail(SPMMM_ERR_DIMENSION, "dimension mismatch: %llu (cols of a) != %llu (rows of b)",
+                (unsigned long long)a->cols, (unsigned long long)b->rows);
+  if (b->cols > 0xffffffffull)
+    return fail(SPMMM_ERR_UNSUPPORTED, "b.cols=%llu exceeds the 32-bit column range",
+                (unsigned long long)b->cols);
+  if (a->rows >= 0xffffffffull)
+    return fail(SPMMM_ERR_UNSUPPORTED, "a.rows=%llu exceeds the 32-bit row range",
+                (unsigned long long)a->rows);
+  const uint64_t* arp = a->row_ptr;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const Trace tr;
+  rc = pipe_setup(c);
+  if (rc) return rc;
+  const bool same = a->row_ptr == b->row_ptr && a->col_idx == b->col_idx &&
+                    a->values == b->values && a->rows == b->rows && a->nnz == b->nnz;
+  const int G = std::max(1, std::min(blocks, kMaxPipeBlocks));
+  cudaEvent_t* ev_struct = &c->pev[0];
+  cudaEvent_t* ev_bv = &c->pev[1];
+  cudaEvent_t* ev_av = &c->pev[2];
+  cudaEvent_t* ev_comp = &c->pev[2 + kMaxPipeBlocks];
+  cudaEvent_t* ev_down = &c->pev[2 + 2 * kMaxPipeBlocks];
+  // device operands
+  const size_t rpb = (a->rows + 1) * 8;
+  CUDA_TRY(ensure(c->a_rp, rpb, c->stream));
+  CUDA_TRY(ensure(c->a_ci, a->nnz * 8, c->stream));
+  CUDA_TRY(ensure(c->a_v, a->nnz * 8, c->stream));
+  if (!same) {
+    CUDA_TRY(ensure(c->b_rp, (b->rows + 1) * 8, c->stream));
+    CUDA_TRY(ensure(c->b_ci, b->nnz * 8, c->stream));
+    CUDA_TRY(ensure(c->b_v, b->nnz * 8, c->stream));
+  }
+  CUDA_TRY(ensure(c->aux, (2 * kMaxPipeBlocks + 2) * 8, c->stream));
+  // buffers (re)allocated on the context stream must exist before s_up uses them
+  CUDA_TRY(cudaEventRecord(*ev_struct, c->stream));
+  CUDA_TRY(cudaStreamWaitEvent(c->s_up, *ev_struct, 0));
+  uint64_t* d_arp = static_cast<uint64_t*>(c->a_rp.p);
+  uint64_t* d_aci = static_cast<uint64_t*>(c->a_ci.p);
+  double* d_av = static_cast<double*>(c->a_v.p);
+  // 1. structure (and B's values) up
+  CUDA_TRY(cudaMemcpyAsync(d_arp, a->row_ptr, rpb, cudaMemcpyHostToDevice, c->s_up));
+  if (a->nnz)
+    CUDA_TRY(cudaMemcpyAsync(d_aci, a->col_idx, a->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
+  if (!same) {
+    CUDA_TRY(cudaMemcpyAsync(c->b_rp.p, b->row_ptr, (b->rows + 1) * 8, cudaMemcpyHostToDevice,
+                             c->s_up));
+    if (b->nnz)
+      CUDA_TRY(cudaMemcpyAsync(c->b_ci.p, b->col_idx, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
+  }
+  CUDA_TRY(cudaEventRecord(*ev_struct, c->s_up));
+  if (!same && b->nnz)
+    CUDA_TRY(cudaMemcpyAsync(c->b_v.p, b->values, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
+  CUDA_TRY(cudaEventRecord(*ev_bv, c->s_up));
+  // row blocks of about equal nnz(A); A's values go up block by block
+  uint64_t bound[kMaxPipeBlocks + 1];
+  bound[0] = 0;
+  for (int j = 1; j < G; ++j) {
+    const uint64_t target = a->nnz * uint64_t(j) / uint64_t(G);
+    bound[j] = uint64_t(std::lower_bound(arp, arp + a->rows + 1, target) - arp);
+    bound[j] = std::max(bound[j], bound[j - 1]);
+    bound[j] = std::min<uint64_t>(bound[j], a->rows);
+  }
+  bound[G] = a->rows;
+  // the value uploads below trust these entries (k_count checks the rest)
+  for (int j = 0; j < G && a->rows; ++j)
+    if (arp[bound[j]] > arp[bound[j + 1]] || arp[bound[j + 1]] > a->nnz)
+      return fail(SPMMM_ERR_INVALID, "malformed a.row_ptr (decreasing or past nnz)");
+  for (int j = 0; j < G; ++j) {
+    const uint64_t e0 = a->rows ? arp[bound[j]] : 0, e1 = a->rows ? arp[bound[j + 1]] : 0;
+    if (e1 > e0)
+      CUDA_TRY(cudaMemcpyAsync(d_av + e0, a->values + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice,
+                               c->s_up));
+    CUDA_TRY(cudaEventRecord(ev_av[j], c->s_up));
+  }
+  // 2. one count pass over all of A: validation, and the size of the result
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, *ev_struct, 0));
+  DevCsr A{d_arp, d_aci, d_av, a->rows, a->cols, a->nnz};
+  DevCsr B = A;
+  if (!same)
+    B = DevCsr{static_cast<const uint64_t*>(c->b_rp.p), static_cast<const uint64_t*>(c->b_ci.p),
+               static_cast<const double*>(c->b_v.p), b->rows, b->cols, b->nnz};
+  B.cols = b->cols;
+  Timer tm0{c, false};
+  auto drain = [&](int code) {
+    cudaStreamSynchronize(c->s_up);
+    cudaStreamSynchronize(c->s_down);
+    cudaStreamSynchronize(c->stream);
+    return code;
+  };
+  tr.mark("pipe: uploads issued");
+  rc = run_count(c, A, B, tm0, false);
+  if (rc) return drain(rc);
+  tr.mark("pipe: count done");
+  const uint64_t total = c->h_ctrl[kCtrlTotal];
+  // 3. A·A: block j reads B rows up to its largest column
+  uint64_t need[kMaxPipeBlocks];
+  for (int j = 0; j < G; ++j) need[j] = uint64_t(j);
+  if (same && a->rows) {
+    uint64_t* d_aux = static_cast<uint64_t*>(c->aux.p);
+    // (bounds by value: a small memcpy would queue behind the uploads)
+    PipeBounds pb;
+    for (int j = 0; j <= G; ++j) pb.r[j] = bound[j];
+    k_zero_u64<<<1, 32, 0, c->stream>>>(d_aux, G);
+    k_block_maxcol<<<G * kPipeSplit, 256, 0, c->stream>>>(d_arp, d_aci, pb,
+                                             reinterpret_cast<unsigned long long*>(d_aux));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(readback(reinterpret_cast<const unsigned long long*>(d_aux), c->h_aux, G, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    tr.mark("pipe: max columns read back");
+    for (int j = 0; j < G; ++j) {
+      const uint64_t row = c->h_aux[j];  // rows [0, row] of B = A must be resident
+      int u = int(std::upper_bound(bound, bound + G + 1, row) - bound) - 1;
+      u = std::min(std::max(u, j), G - 1);
+      need[j] = uint64_t(u);
+    }
+  }
+  // 4. the result, in pinned host memory from the pool
+  void *hrp = nullptr, *hci = nullptr, *hv = nullptr;
+  rc = host_alloc_internal(rpb, &hrp);
+  if (!rc) rc = host_alloc_internal(std::max<uint64_t>(total, 1) * 8, &hci);
+  if (!rc) rc = host_alloc_internal(std::max<uint64_t>(total, 1) * 8, &hv);
+  auto free_out = [&]() {
+    host_free_internal(hrp);
+    host_free_internal(hci);
+    host_free_internal(hv);
+  };
+  if (rc) {
+    free_out();
+    return drain(rc);
+  }
+  tr.mark("pipe: outputs allocated");
+  uint64_t* out_rp = static_cast<uint64_t*>(hrp);
+  uint64_t* out_ci = static_cast<uint64_t*>(hci);
+  double* out_v = static_cast<double*>(hv);
+  out_rp[0] = 0;
+  // 5. blocks: compute when their inputs are resident, then stream down
+  spmmm_product* prods[kMaxPipeBlocks] = {};
+  auto release_all = [&]() {
+    for (int j = 0; j < G; ++j)
+      if (prods[j]) {
+        product_release(c, prods[j]);
+        delete prods[j];
+      }
+  };
+  uint64_t off = 0, mults = 0;
+  for (int j = 0; j < G; ++j) {
+    const uint64_t r0 = bound[j], r1 = bound[j + 1];
+    if (r1 == r0) continue;
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, ev_av[same ? need[j] : j], 0));
+    if (!same) CUDA_TRY(cudaStreamWaitEvent(c->stream, *ev_bv, 0));
+    spmmm_csr va{r1 - r0, a->cols, a->nnz, d_arp + r0, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
+    spmmm_csr vb{B.rows, B.cols, B.nnz, B.rp, B.ci, B.v, SPMMM_MEM_DEVICE, 0};
+    rc = multiply_impl(c, &va, &vb, strategy, flags & SPMMM_FLAG_TIMING, &prods[j]);
+    if (rc) {
+      drain(0);
+      release_all();
+      free_out();
+      return rc;
+    }
+    spmmm_product* p = prods[j];
+    if (off) {
+      k_add_offset<<<std::max<unsigned>(1, unsigned(std::min<uint64_t>((r1 - r0 + 256) / 256, 1024))),
+                     256, 0, c->stream>>>(p->rp, r1 - r0 + 1, off);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaEventRecord(ev_comp[j], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
+    CUDA_TRY(cudaMemcpyAsync(out_rp + r0, p->rp, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost,
+                             c->s_down));
+    if (p->nnz) {
+      CUDA_TRY(cudaMemcpyAsync(out_ci + off, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
+      CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
+    }
+    CUDA_TRY(cudaEventRecord(ev_down[j], c->s_down));  // (arrays live until the end)
+    off += p->nnz;
+    mults += p->mults;
+    tr.mark("pipe: block computed, download issued");
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->s_down));
+  CUDA_TRY(cudaStreamSynchronize(c->s_up));
+  tr.mark("pipe: downloads done");
+  release_all();
+  out->rows = a->rows;
+  out->cols = b->cols;
+  out->nnz = off;
+  out->mults = mults;
+  out->row_ptr = out_rp;
+  out->col_idx = out_ci;
+  out->values = out_v;
+  return SPMMM_OK;
+}
 }  // namespace
 
 // =============================================================================
@@ -955,7 +1237,8 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
                     &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
-                    &c->a_v, &c->b_rp, &c->b_ci, &c->b_v})
+                    &c->a_v, &c->b_rp, &c->b_ci, &c->b_v, &c->parts, &c->part_off, &c->part_nnz,
+                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
   c->cache.clear();
@@ -963,6 +1246,11 @@ int spmmm_context_destroy(spmmm_context* c) {
   for (int k = 0; k < 2 * kNumKernels; ++k)
     if (c->ev[k]) cudaEventDestroy(c->ev[k]);
   if (c->ev_count) cudaEventDestroy(c->ev_count);
+  for (cudaEvent_t ev : c->pev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->s_up) cudaStreamDestroy(c->s_up);
+  if (c->s_down) cudaStreamDestroy(c->s_down);
+  if (c->h_aux) cudaFreeHost(c->h_aux);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -981,6 +1269,13 @@ int spmmm_multiply(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int
   if (!c) return fail(SPMMM_ERR_INVALID, "context is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
   return multiply_impl(c, a, b, strategy, flags, out);
+}
+
+int spmmm_multiply_host(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
+                        uint32_t flags, int blocks, spmmm_host_csr* out) {
+  if (!c) return fail(SPMMM_ERR_INVALID, "context is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  return multiply_host_impl(c, a, b, strategy, flags, blocks, out);
 }
 
 int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, uint64_t* nnz,

@@ -45,6 +45,11 @@ class StrategyKind(str, Enum):
 
 _STRATEGY_IDS = {s.value: i for i, s in enumerate(StrategyKind)}
 
+# multiply_rowmajor without stats on operands of at least this many A entries
+# takes the block-pipelined host path (spmmm_multiply_host)
+PIPELINE_MIN_NNZ = 1 << 20
+PIPELINE_BLOCKS = 8
+
 
 @dataclass
 class KernelStats:
@@ -111,6 +116,11 @@ def multiply_rowmajor(a, b, strategy=StrategyKind.COMBINED, stats=None):
     vb = _lib.csr_view(b.rows, b.cols, brp, bci, bv)
     flags = _lib.FLAG_ROW_STATS if stats is not None else 0
     ctx = _lib.default_context()
+    if stats is None and len(av) >= PIPELINE_MIN_NNZ:
+        # large host operands: uploads, kernels and downloads overlap in row
+        # blocks (spmmm_multiply_host); the same bytes as the path below
+        rp, ci, v, _ = _lib.multiply_host(ctx, va, vb, sid, 0, PIPELINE_BLOCKS)
+        return make_like(a, a.rows, b.cols, rp, ci, v)
     with _lib.multiply_views(ctx, va, vb, sid, flags) as product:
         rp, ci, v = product.download()
         if stats is not None:

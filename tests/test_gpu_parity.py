@@ -334,3 +334,74 @@ def test_split_mode_esc_kernels(case, values):
                              CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx, ref.values),
                              f"esc/{case}/{values}")
     assert np.array_equal(_choices_array(stats, a.rows), ref.row_choices)
+
+
+def _host_views(a, b):
+    return (_lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values),
+            _lib.csr_view(b.rows, b.cols, b.row_ptr, b.col_idx, b.values))
+
+
+@pytest.mark.parametrize("blocks", [1, 3, 8, 16])
+def test_pipelined_host_product_matches_oracle(blocks):
+    """spmmm_multiply_host (row blocks: values up, compute, C down, overlapped)
+    gives the bytes of the one-shot path: A·A (blocks wait for the B rows they
+    read), A·B, skewed rows (split mode per block), empty rows, empty A."""
+    rng = np.random.default_rng(blocks)
+    fd = genmat.gen_fd(200)
+    z = genmat.gen_zipf(30_000, 5)
+    rect_a = _rand_csr(rng, 700, 300, 12, "quantized")
+    rect_b = _rand_csr(rng, 300, 900, 10, "quantized")
+    zero_a = CsrMatrix(50, 300, np.zeros(51, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    ctx = _lib.Context(0)
+    for name, a, b in [("fd200^2", fd, fd), ("zipf", z, genmat.gen_zipf(30_000, 6)),
+                       ("rect", rect_a, rect_b), ("zero", zero_a, rect_b),
+                       ("zipf^2", z, z)]:
+        va, vb = _host_views(a, b)
+        if b is a:
+            vb = va
+        rp, ci, v, mults = _lib.multiply_host(ctx, va, vb, 6, 0, blocks)
+        ref = oracle.multiply_rowmajor(a, b, threads=8)
+        assert mults == ref.multiplications, name
+        assert_csr_bitwise_equal(CsrMatrix(a.rows, b.cols, rp, ci, v),
+                                 CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx,
+                                           ref.values), f"pipelined/{name}/{blocks}")
+    ctx.close()
+
+
+def test_pipelined_host_product_errors():
+    ctx = _lib.Context(0)
+    b = CsrMatrix(3, 3, np.array([0, 1, 2, 3], np.uint64), np.array([0, 1, 2], np.uint64),
+                  np.ones(3))
+    bad_rp = CsrMatrix(2, 3, np.array([0, 2, 1], np.uint64), np.array([0, 1], np.uint64),
+                       np.array([1.0, 2.0]))
+    bad_col = CsrMatrix(1, 3, np.array([0, 1], np.uint64), np.array([7], np.uint64), np.ones(1))
+    past = CsrMatrix(1, 3, np.array([0, 5], np.uint64), np.array([0, 1], np.uint64), np.ones(2))
+    for a, what in [(bad_rp, "row_ptr"), (bad_col, "col_idx"), (past, "row_ptr")]:
+        va, vb = _host_views(a, b)
+        with pytest.raises(ValueError, match=what):
+            _lib.multiply_host(ctx, va, vb, 6, 0, 2)
+    va, vb = _host_views(b, bad_rp)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        _lib.multiply_host(ctx, va, vb, 6, 0, 2)
+    # the context stays usable after errors
+    va, vb = _host_views(b, b)
+    rp, ci, v, m = _lib.multiply_host(ctx, va, vb, 6, 0, 2)
+    assert m == 3 and list(ci) == [0, 1, 2]
+    ctx.close()
+
+
+@pytest.mark.parametrize("label", ["C2_fd2048", "C3_random2M", "C4_fd3_100", "C5_zipf2M"])
+def test_full_size_drop_in_without_stats_matches_reference(label):
+    """The drop-in without stats takes the pipelined host path at these sizes."""
+    from paper_1303_1651_b200 import kernels as km
+
+    fp = fingerprints().get(label)
+    if fp is None:
+        pytest.skip(f"{label} missing from fingerprints.json")
+    a, b = _config_ops(label)
+    assert len(a.values) >= km.PIPELINE_MIN_NNZ
+    c = multiply_rowmajor(a, b)
+    d = genmat.digests(c)
+    assert d["row_ptr_sha256"] == fp["c"]["row_ptr_sha256"]
+    assert d["col_idx_sha256"] == fp["c"]["col_idx_sha256"]
+    assert d["values_sha256"] == fp["c"]["values_sha256"]
