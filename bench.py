@@ -58,9 +58,9 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic(config_label):
-    """DRAM bytes per k_fused launch from the committed ncu --set full summary
-    of this config (profiles/*.json), or None."""
+def profile_traffic(config_label, kernel="k_fused"):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    summary of this config (profiles/*.json), or None."""
     pdir = os.path.join(ROOT, "profiles")
     best = None
     if os.path.isdir(pdir):
@@ -72,7 +72,7 @@ def profile_traffic(config_label):
                     d = json.load(f)
             except Exception:
                 continue
-            ent = d.get("configs", {}).get(config_label, {}).get("k_fused")
+            ent = d.get("configs", {}).get(config_label, {}).get(kernel)
             if ent and ent.get("dram_bytes") is not None:
                 best = (int(ent["dram_bytes"]), name)
     return best
@@ -350,19 +350,34 @@ def main():
     flops = 2.0 * total_mults
     value = flops / (ms_per_step * 1e-3) / 1e9
 
-    # ---- roofline of the dominant kernel (k_fused) ----
+    # ---- roofline of the dominant kernel ----
+    # k_fused for C1-C4 (it computes every row); in split mode (C5) the
+    # expand-sort-compress block kernel, whose units are the products of the
+    # rows past kEscWarpLimit (512) — the rows it computes (mid rows whole,
+    # huge rows as column-range parts). Bytes per unit: the workload's
+    # bytes_alg / products.
     nnz_a = len(a.values)
     balg = bytes_alg(a.rows, nnz_a, total_mults, total_nnz)
     peak, peak_src = hbm_peak()
-    kf_ms = kernel_ms.get("k_fused", 0.0) / args.steps
     per_kernel = {k: round(v / args.steps, 4) for k, v in kernel_ms.items()}
-    achieved = balg / (kf_ms * 1e-3) / 1e9 if kf_ms > 0 else None
-    traffic = profile_traffic(label)
+    dom = max(kernel_ms, key=kernel_ms.get) if kernel_ms else "k_fused"
+    if dom not in ("k_fused", "k_esc_block"):
+        dom = "k_fused"
+    kf_ms = kernel_ms.get(dom, 0.0) / args.steps
+    units, launch_bytes = total_mults, balg
+    if dom == "k_esc_block" and not distributed:
+        prefix = row_products_prefix(a, b)
+        prod = np.diff(prefix.astype(np.int64))
+        units = int(prod[prod > 512].sum())
+        launch_bytes = int(round(balg * units / max(total_mults, 1)))
+    achieved = launch_bytes / (kf_ms * 1e-3) / 1e9 if kf_ms > 0 else None
+    traffic = profile_traffic(label, dom)
     roof = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
             "peak": peak, "unit": "GB/s",
             "frac": round(achieved / (peak * world), 4) if achieved else None,
             "traffic": traffic[0] if traffic else None,
-            "kernel": "k_fused", "bytes_alg_per_launch": balg,
+            "kernel": dom, "bytes_alg_per_launch": launch_bytes,
+            "units_per_launch": units, "bytes_per_unit": round(balg / max(total_mults, 1), 2),
             "kernel_ms_per_launch": round(kf_ms, 4),
             "step_frac": round(balg / (ms_per_step * 1e-3) / 1e9 / (peak * world), 4),
             "peak_source": peak_src,

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
   uint32_t need = 0, err = 0;
   const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
   const uint64_t gw = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr uint64_t kSerial = 64;  // rows up to this many entries: one thread
+  constexpr uint64_t kSerial = 32;  // rows up to this many entries: one thread
   for (uint64_t base = gw * 32; base < A.rows; base += nwarps * 32) {
     const uint64_t r = base + lane;
     uint64_t lo = 0, hi = 0;
