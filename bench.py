@@ -252,7 +252,8 @@ def main():
     from paper_1303_1651_b200 import _lib
     from paper_1303_1651_b200 import device as dev
     from paper_1303_1651_b200.distributed import partition_rows
-    from paper_1303_1651_b200.kernels import multiply_rowmajor, row_products_prefix
+    from paper_1303_1651_b200.kernels import (PIPELINE_MIN_NNZ, multiply_rowmajor,
+                                              row_products_prefix)
     from paper_1303_1651_b200.perfmodel import bytes_alg
 
     if not torch.cuda.is_available():
@@ -430,10 +431,14 @@ def main():
         if not same:
             h2d += 8 * (b.rows + 1) + 16 * len(b.values)
         d2h = 8 * (c.rows + 1) + 16 * len(c.values)
+        if _lib.last_transfer is not None and nnz_a >= PIPELINE_MIN_NNZ:
+            # the pipelined path moves C's column indices as u32
+            h2d = _lib.last_transfer["h2d_bytes"]
+            d2h = _lib.last_transfer["d2h_bytes"]
         line["e2e"] = {"value": round(flops / e2e_s / 1e9, 3), "unit": UNIT,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "ms_per_step": round(e2e_s * 1e3, 3), "steps": len(times),
-                       "api": "paper_1303_1651_b200.multiply_rowmajor (pinned numpy in, numpy out backed by the pinned pool)"}
+                       "api": "paper_1303_1651_b200.multiply_rowmajor (pinned numpy in, numpy out backed by the pinned pool; block-pipelined spmmm_multiply_host for >= 2^20 A entries)"}
 
     # ---- CPU baseline: the oracle port, 1 thread, bounded sample ----
     if not args.no_cpu_baseline and rank == 0 and not distributed:

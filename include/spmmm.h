@@ -109,12 +109,14 @@ int spmmm_product_download(spmmm_product* p, uint64_t* row_ptr, uint64_t* col_id
 
 /* Result of spmmm_multiply_host: C in page-locked host memory from the
  * library's pool (return each array with spmmm_host_free). col_idx / values
- * hold `nnz` entries (their blocks may be larger). */
+ * hold `nnz` entries (their blocks may be larger). Column indices travel
+ * down as u32 for large results and are widened by host threads. */
 typedef struct {
   uint64_t rows, cols, nnz, mults;
   uint64_t* row_ptr;
   uint64_t* col_idx;
   double* values;
+  uint64_t h2d_bytes, d2h_bytes;  /* PCIe bytes this call moved each way */
 } spmmm_host_csr;
 
 /* C = A·B for HOST operands, block-pipelined: A's and B's structure go up

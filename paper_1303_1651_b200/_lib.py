@@ -60,6 +60,8 @@ class SpmmmHostCsr(ctypes.Structure):
         ("row_ptr", ctypes.c_void_p),
         ("col_idx", ctypes.c_void_p),
         ("values", ctypes.c_void_p),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
     ]
 
 
@@ -345,7 +347,13 @@ def multiply_host(ctx: Context, a: SpmmmCsr, b: SpmmmCsr, strategy_id: int, flag
     rp = _pool_array(out.row_ptr, out.rows + 1, np.uint64)
     ci = _pool_array(out.col_idx, out.nnz, np.uint64)
     v = _pool_array(out.values, out.nnz, np.float64)
+    global last_transfer
+    last_transfer = {"h2d_bytes": int(out.h2d_bytes), "d2h_bytes": int(out.d2h_bytes)}
     return rp, ci, v, int(out.mults)
+
+
+# PCIe bytes of the last multiply_host call (bench.py's e2e accounting)
+last_transfer = None
 
 
 def transpose_view(ctx: Context, m: SpmmmCsr) -> Product:

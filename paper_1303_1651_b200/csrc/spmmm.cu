@@ -17,7 +17,13 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <atomic>
+#include <functional>
+#include <condition_variable>
+#include <immintrin.h>
 #include <mutex>
+#include <thread>
+#include <sched.h>
 #include <string>
 #include <vector>
 
@@ -101,6 +107,7 @@ const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused",
                                     "k_esc_warp", "k_esc_block", "k_esc_plan"};
 constexpr int kNumKernels = 12;
 constexpr int kMaxPipeBlocks = 16;  // spmmm_multiply_host row blocks
+constexpr uint64_t kNarrowMin = 1 << 20;  // results past this many products: u32 indices down
 
 }  // namespace
 
@@ -129,7 +136,8 @@ struct spmmm_context {
   DevBuf parts, part_off, part_nnz, row_parts, scr_col, scr_val;  // ESC parts of huge rows
   // spmmm_multiply_host: copy streams (uploads, downloads) and their events
   cudaStream_t s_up = nullptr, s_down = nullptr;
-  cudaEvent_t pev[3 * kMaxPipeBlocks + 2] = {};
+  cudaEvent_t pev[4 * kMaxPipeBlocks + 2] = {};
+  DevBuf ci32;                         // narrowed column indices of C blocks
   DevBuf aux;                          // per-block max columns
   unsigned long long* h_aux = nullptr; // pinned mirror
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
@@ -938,6 +946,15 @@ __global__ void k_block_maxcol(const uint64_t* __restrict__ rp, const uint64_t* 
   if ((threadIdx.x & 31) == 0 && m) atomicMax(out + j, (unsigned long long)m);
 }
 
+// C's column indices go down as u32 (columns < 2^32 are checked): half the
+// PCIe bytes of col_idx; host threads widen them while the values follow.
+__global__ void k_narrow(const uint64_t* __restrict__ src, uint32_t* __restrict__ dst,
+                         uint64_t n) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = uint32_t(__ldcs(reinterpret_cast<const unsigned long long*>(src) + i));
+}
+
 __global__ void k_zero_u64(uint64_t* p, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
 }
@@ -953,8 +970,44 @@ int pipe_setup(spmmm_context* c) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s_up, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s_down, cudaStreamNonBlocking));
   for (cudaEvent_t& ev : c->pev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  // the widening workers sleep on these instead of spinning next to the
+  // thread that issues the work
+  for (int j = 0; j < kMaxPipeBlocks; ++j) {
+    cudaEvent_t& ev = c->pev[2 + 3 * kMaxPipeBlocks + j];
+    CUDA_TRY(cudaEventDestroy(ev));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync));
+  }
   CUDA_TRY(cudaMallocHost(&c->h_aux, 2 * kMaxPipeBlocks * sizeof(unsigned long long)));
   return SPMMM_OK;
+}
+
+// u32 -> u64 widening of downloaded column indices (host). AVX2 with
+// streaming stores when the CPU has it: the result is written once and not
+// read back soon, so skipping the read-for-ownership halves the memory
+// traffic that competes with the DMA landing the next blocks.
+__attribute__((target("avx2"))) void widen_avx2(const uint32_t* in, uint64_t* out, uint64_t n) {
+  uint64_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(out + i) & 31)) {
+    out[i] = in[i];
+    ++i;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(in + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(in + i + 4));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + i), _mm256_cvtepu32_epi64(a));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + i + 4), _mm256_cvtepu32_epi64(b));
+  }
+  for (; i < n; ++i) out[i] = in[i];
+  _mm_sfence();
+}
+
+void widen(const uint32_t* in, uint64_t* out, uint64_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) {
+    widen_avx2(in, out, n);
+    return;
+  }
+  for (uint64_t i = 0; i < n; ++i) out[i] = in[i];
 }
 
 int host_alloc_internal(uint64_t bytes, void** ptr) { return spmmm_host_alloc(bytes, ptr); }
@@ -1108,7 +1161,80 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   uint64_t* out_ci = static_cast<uint64_t*>(hci);
   double* out_v = static_cast<double*>(hv);
   out_rp[0] = 0;
-  // 5. blocks: compute when their inputs are resident, then stream down
+  // 5. blocks: compute when their inputs are resident, then stream down.
+  // Column indices travel as u32 into a pinned staging area; worker threads
+  // widen each block into the result as soon as its indices have landed.
+  cudaEvent_t* ev_ci = &c->pev[2 + 3 * kMaxPipeBlocks];
+  static const bool no_narrow = std::getenv("SPMMM_NO_NARROW") != nullptr;
+  static const int widen_threads = std::getenv("SPMMM_WIDEN_THREADS")
+                                       ? std::atoi(std::getenv("SPMMM_WIDEN_THREADS")) : 0;
+  const bool narrow = total >= kNarrowMin && !no_narrow;
+  void* hci32 = nullptr;
+  if (narrow) {
+    CUDA_TRY(ensure(c->ci32, total * 4, c->stream));
+    rc = host_alloc_internal(total * 4, &hci32);
+    if (rc) {
+      free_out();
+      return drain(rc);
+    }
+  }
+  uint32_t* d_ci32 = static_cast<uint32_t*>(c->ci32.p);
+  uint32_t* h_ci32 = static_cast<uint32_t*>(hci32);
+  uint64_t blk_off[kMaxPipeBlocks] = {}, blk_n[kMaxPipeBlocks] = {};
+  std::atomic<int> issued{0};
+  std::mutex issue_mu;
+  std::condition_variable issue_cv;
+  auto publish = [&](int n) {
+    {
+      std::lock_guard<std::mutex> lk(issue_mu);
+      issued.store(n, std::memory_order_release);
+    }
+    issue_cv.notify_all();
+  };
+  std::atomic<bool> abort_widen{false};
+  std::vector<std::thread> workers;
+  int nthreads = 1;
+  if (narrow) {
+    cpu_set_t cs;
+    int ncpu = sched_getaffinity(0, sizeof(cs), &cs) == 0 ? CPU_COUNT(&cs) : 8;
+    nthreads = widen_threads > 0 ? widen_threads : std::max(1, std::min(ncpu / 4, 4));
+    for (int w = 0; w < nthreads; ++w) {
+      workers.emplace_back([&, w]() {
+        cudaSetDevice(c->device);
+        for (int j = 0; j < G; ++j) {
+          {
+            std::unique_lock<std::mutex> lk(issue_mu);
+            issue_cv.wait(lk, [&]() {
+              return issued.load(std::memory_order_acquire) > j ||
+                     abort_widen.load(std::memory_order_relaxed);
+            });
+          }
+          if (abort_widen.load(std::memory_order_relaxed)) return;
+          const uint64_t n = blk_n[j];
+          if (!n) continue;
+          if (cudaEventSynchronize(ev_ci[j]) != cudaSuccess) return;
+          const uint64_t i0 = blk_off[j] + n * uint64_t(w) / uint64_t(nthreads);
+          const uint64_t i1 = blk_off[j] + n * uint64_t(w + 1) / uint64_t(nthreads);
+          widen(h_ci32 + i0, out_ci + i0, i1 - i0);
+        }
+      });
+    }
+  }
+  auto stop_workers = [&]() {
+    abort_widen.store(true);
+    publish(G + 1);
+    for (auto& t : workers) t.join();
+    workers.clear();
+    if (hci32) host_free_internal(hci32);
+    hci32 = nullptr;
+  };
+  // every early return below (CUDA_TRY included) stops the workers first
+  struct WorkerGuard {
+    std::function<void()> f;
+    ~WorkerGuard() {
+      if (f) f();
+    }
+  } guard{stop_workers};
   spmmm_product* prods[kMaxPipeBlocks] = {};
   auto release_all = [&]() {
     for (int j = 0; j < G; ++j)
@@ -1128,6 +1254,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     rc = multiply_impl(c, &va, &vb, strategy, flags & SPMMM_FLAG_TIMING, &prods[j]);
     if (rc) {
       drain(0);
+      stop_workers();
       release_all();
       free_out();
       return rc;
@@ -1142,15 +1269,38 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
     CUDA_TRY(cudaMemcpyAsync(out_rp + r0, p->rp, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost,
                              c->s_down));
-    if (p->nnz) {
+    if (p->nnz && narrow) {
+      k_narrow<<<std::min<unsigned>(unsigned((p->nnz + 255) / 256), unsigned(c->sms) * 8), 256, 0,
+                 c->stream>>>(p->ci, d_ci32 + off, p->nnz);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(ev_comp[j], c->stream));
+      CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
+      CUDA_TRY(cudaMemcpyAsync(h_ci32 + off, d_ci32 + off, p->nnz * 4, cudaMemcpyDeviceToHost,
+                               c->s_down));
+      CUDA_TRY(cudaEventRecord(ev_ci[j], c->s_down));
+      CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
+    } else if (p->nnz) {
       CUDA_TRY(cudaMemcpyAsync(out_ci + off, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
       CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
     }
     CUDA_TRY(cudaEventRecord(ev_down[j], c->s_down));  // (arrays live until the end)
+    blk_off[j] = off;
+    blk_n[j] = narrow ? p->nnz : 0;
+    publish(j + 1);
     off += p->nnz;
     mults += p->mults;
     tr.mark("pipe: block computed, download issued");
   }
+  publish(G);  // (skipped empty blocks)
+  if (tr.on) {
+    cudaStreamSynchronize(c->s_down);
+    tr.mark("pipe: downloads done (trace only: waits before joining)");
+  }
+  for (auto& t : workers) t.join();
+  tr.mark("pipe: widening done");
+  workers.clear();
+  guard.f = nullptr;
+  if (hci32) host_free_internal(hci32);
   CUDA_TRY(cudaStreamSynchronize(c->s_down));
   CUDA_TRY(cudaStreamSynchronize(c->s_up));
   tr.mark("pipe: downloads done");
@@ -1159,6 +1309,8 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   out->cols = b->cols;
   out->nnz = off;
   out->mults = mults;
+  out->h2d_bytes = rpb + a->nnz * 16 + (same ? 0 : (b->rows + 1) * 8 + b->nnz * 16);
+  out->d2h_bytes = rpb + off * (narrow ? 12 : 16);
   out->row_ptr = out_rp;
   out->col_idx = out_ci;
   out->values = out_v;
@@ -1238,7 +1390,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
                     &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v, &c->parts, &c->part_off, &c->part_nnz,
-                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux})
+                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
   c->cache.clear();
