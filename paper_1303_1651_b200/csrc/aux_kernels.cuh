@@ -622,8 +622,38 @@ struct CopyParams {
 // Rows of the sub-lists (long: up to tens of thousands of entries) are copied
 // by whole blocks first; the remaining listed rows (<= long_min products) by
 // one warp each. Both take rows dynamically.
+// One staged run to its slot of C: U loads in flight per thread (a plain
+// load -> store loop is one memory round trip per step).
+template <int U>
+__device__ __forceinline__ void copy_run(unsigned long long* __restrict__ dci,
+                                         double* __restrict__ dv,
+                                         const uint64_t* __restrict__ sci,
+                                         const double* __restrict__ sv, uint32_t n,
+                                         uint32_t t0, uint32_t step) {
+  uint32_t i = t0;
+  for (; i + (U - 1) * step < n; i += U * step) {
+    unsigned long long c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = (unsigned long long)__ldcs(sci + i + u * step);
+      v[u] = __ldcs(sv + i + u * step);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      __stcs(dci + i + u * step, c[u]);
+      __stcs(dv + i + u * step, v[u]);
+    }
+  }
+  for (; i < n; i += step) {
+    __stcs(dci + i, (unsigned long long)__ldcs(sci + i));
+    __stcs(dv + i, __ldcs(sv + i));
+  }
+}
+
 __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
   __shared__ uint32_t s_t;
+  unsigned long long* cci = reinterpret_cast<unsigned long long*>(p.c_ci);
   const uint32_t n_mid = uint32_t(p.ctrl[kCtrlMidRows]);
   const uint32_t n_big = n_mid + uint32_t(p.ctrl[kCtrlHugeRows]);
   while (true) {
@@ -641,40 +671,27 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
       for (uint32_t j = 0; j < np; ++j) {
         const uint64_t so = p.part_off[pb + j];
         const uint32_t pc = p.part_nnz[pb + j];
-        for (uint32_t i = threadIdx.x; i < pc; i += blockDim.x) {
-          __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + d + i,
-                 (unsigned long long)__ldcs(p.l_ci + so + i));
-          __stcs(p.c_v + d + i, __ldcs(p.l_v + so + i));
-        }
+        copy_run<4>(cci + d, p.c_v + d, p.l_ci + so, p.l_v + so, pc, threadIdx.x, blockDim.x);
         d += pc;
       }
       continue;
     }
     const uint64_t src = p.l_off[li];
     const uint32_t cnt = p.l_nnz[li];
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-      __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + dst + i,
-             (unsigned long long)__ldcs(p.l_ci + src + i));
-      __stcs(p.c_v + dst + i, __ldcs(p.l_v + src + i));
-    }
+    copy_run<4>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, threadIdx.x, blockDim.x);
   }
+  // the other listed rows (<= long_min products): one warp each, static
+  // assignment (their costs are alike; no ticket traffic)
   const uint32_t lane = lane_id();
   const uint32_t n = uint32_t(p.ctrl[kCtrlLongRows]);
-  while (true) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(p.tickets + 1, 1ull);
-    const uint32_t li = uint32_t(__shfl_sync(kFull, t, 0));
-    if (li >= n) break;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t li = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < n; li += nwarps) {
     const uint32_t r = p.list[li];
     if (p.prod[r] > p.long_min) continue;  // copied above
     const uint64_t dst = p.c_rp[r];
     const uint64_t src = p.l_off[li];
     const uint32_t cnt = p.l_nnz[li];
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      __stcs(reinterpret_cast<unsigned long long*>(p.c_ci) + dst + i,
-             (unsigned long long)__ldcs(p.l_ci + src + i));
-      __stcs(p.c_v + dst + i, __ldcs(p.l_v + src + i));
-    }
+    copy_run<4>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, lane, 32);
   }
 }
 
