@@ -307,6 +307,16 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
 // stable scatter). A row whose busiest part outgrows its region (columns far
 // from uniform over the range), or that finds the scratch full, goes to
 // k_long instead.
+// x / w for x, w < 2^24 (exact in fp32): a float estimate, corrected by one
+// step either way (the estimate is off by at most one). ~6 instructions
+// against ~25 for an integer division.
+__device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, float inv_w) {
+  uint32_t q = __float2uint_rz(float(x) * inv_w);
+  if (q * w > x) --q;
+  else if ((q + 1) * w <= x) ++q;
+  return q;
+}
+
 constexpr uint32_t kPartTarget = kEscBlockCap / 2;
 constexpr uint32_t kMaxParts = 64;
 constexpr int kPlanThreads = 512;
@@ -320,6 +330,7 @@ __device__ __forceinline__ void plan_segment(const LongParams& pp, uint64_t es, 
                                              uint32_t width, uint32_t region, uint64_t sbase,
                                              uint32_t* cnt) {
   const uint32_t lane = lane_id();
+  const float inv_w = 1.0f / float(width);
   // entries from es (whose first product is row product gq) until product qe
 #pragma unroll 1
   for (uint64_t ab = es; ab < ehi && gq < qe; ab += 32) {
@@ -366,7 +377,7 @@ __device__ __forceinline__ void plan_segment(const LongParams& pp, uint64_t es, 
       for (int u = 0; u < 4; ++u) {
         const uint32_t q = c + 32u * u + lane;
         const bool act = q < qhi;
-        const uint32_t part = act ? (col[u] - cmn) / width : kEmptyKey;
+        const uint32_t part = act ? div_small(col[u] - cmn, width, inv_w) : kEmptyKey;
         const uint32_t peers = __match_any_sync(kFull, part);
         const uint32_t leader = __ffs(peers) - 1;
         uint32_t old = 0;

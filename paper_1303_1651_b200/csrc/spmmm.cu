@@ -138,6 +138,9 @@ struct spmmm_context {
   cudaStream_t s_up = nullptr, s_down = nullptr;
   cudaEvent_t pev[4 * kMaxPipeBlocks + 2] = {};
   DevBuf ci32;                         // narrowed column indices of C blocks
+  // split mode: k_esc_warp runs on its own stream beside k_esc_plan/k_esc_block
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf aux;                          // per-block max columns
   unsigned long long* h_aux = nullptr; // pinned mirror
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
@@ -274,11 +277,11 @@ int resolve(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, DevCsr* A,
 struct Timer {
   spmmm_context* c;
   bool on;
-  void begin(int k) {
-    if (on) { cudaEventRecord(c->ev[2 * k], c->stream); c->ev_used[k] = true; }
+  void begin(int k, cudaStream_t s = nullptr) {
+    if (on) { cudaEventRecord(c->ev[2 * k], s ? s : c->stream); c->ev_used[k] = true; }
   }
-  void end(int k) {
-    if (on) cudaEventRecord(c->ev[2 * k + 1], c->stream);
+  void end(int k, cudaStream_t s = nullptr) {
+    if (on) cudaEventRecord(c->ev[2 * k + 1], s ? s : c->stream);
   }
 };
 
@@ -461,6 +464,15 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
              DevBuf& stage_ci, DevBuf& stage_v, Timer& tm) {
   const Trace tr;
   const uint64_t rows = A.rows;
+  bool esc_forked = false;
+  auto join_esc = [&]() -> int {
+    if (esc_forked) {
+      esc_forked = false;
+      if (cudaStreamWaitEvent(c->stream, c->ev_join, 0) != cudaSuccess)
+        return fail(SPMMM_ERR_CUDA, "joining the k_esc_warp stream failed");
+    }
+    return SPMMM_OK;
+  };
   CUDA_TRY(ensure(c->lmap, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->list, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->l_off, rows * sizeof(uint64_t), c->stream));
@@ -544,12 +556,29 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
                      esc_block_smem_bytes(kEscBlockCap)));
         c->esc_attr[stats] = true;
       }
-      const unsigned grid_rows = unsigned(c->sms) * 4;
-      tm.begin(9);
-      if (stats) k_esc_warp<true><<<grid_rows, kEscWarps * 32, smem, c->stream>>>(rp);
-      else k_esc_warp<false><<<grid_rows, kEscWarps * 32, smem, c->stream>>>(rp);
+      // the warp rows are independent of the block rows: their kernel runs on
+      // a second stream, overlapping k_esc_plan / k_esc_block (all three are
+      // latency bound); the context stream joins it before k_fused
+      static const bool serial = std::getenv("SPMMM_SERIAL_ESC") != nullptr;
+      cudaStream_t ws = c->stream;
+      if (!serial) {
+        if (!c->s_aux) {
+          CUDA_TRY(cudaStreamCreateWithFlags(&c->s_aux, cudaStreamNonBlocking));
+          CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+          CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        }
+        CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->s_aux, c->ev_fork, 0));
+        ws = c->s_aux;
+        esc_forked = true;
+      }
+      const unsigned grid_rows = unsigned(c->sms) * (serial ? 4 : 2);
+      tm.begin(9, ws);
+      if (stats) k_esc_warp<true><<<grid_rows, kEscWarps * 32, smem, ws>>>(rp);
+      else k_esc_warp<false><<<grid_rows, kEscWarps * 32, smem, ws>>>(rp);
       CUDA_TRY(cudaGetLastError());
-      tm.end(9);
+      tm.end(9, ws);
+      if (esc_forked) CUDA_TRY(cudaEventRecord(c->ev_join, c->s_aux));
       ++c->last_launches;
       tr.mark("  run_long: k_esc_warp launched");
     } else {
@@ -573,7 +602,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     tr.mark("  run_long: k_rows launched");
     }
   }
-  if (max_prod <= long_min) return SPMMM_OK;
+  if (max_prod <= long_min) return join_esc();
   LongParams lp;
   lp.A = A;
   lp.B = B;
@@ -654,7 +683,10 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   } else {
     tm.begin(6);
     rc = stats ? launch_long_smem<true>(c, lp, false) : launch_long_smem<false>(c, lp, false);
-    if (rc) return rc;
+    if (rc) {
+      join_esc();
+      return rc;
+    }
     tm.end(6);
   }
   ++c->last_launches;
@@ -666,7 +698,10 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     lp.ticket = ctrl + kCtrlHugeTicket;
     tm.begin(7);
     rc = stats ? launch_long_smem<true>(c, lp, true) : launch_long_smem<false>(c, lp, true);
-    if (rc) return rc;
+    if (rc) {
+      join_esc();
+      return rc;
+    }
     tm.end(7);
     ++c->last_launches;
     }
@@ -681,7 +716,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     tm.end(2);
     ++c->last_launches;
   }
-  return SPMMM_OK;
+  return join_esc();
 }
 
 int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
@@ -1401,6 +1436,9 @@ int spmmm_context_destroy(spmmm_context* c) {
   for (cudaEvent_t ev : c->pev)
     if (ev) cudaEventDestroy(ev);
   if (c->s_up) cudaStreamDestroy(c->s_up);
+  if (c->s_aux) cudaStreamDestroy(c->s_aux);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->s_down) cudaStreamDestroy(c->s_down);
   if (c->h_aux) cudaFreeHost(c->h_aux);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
