@@ -482,6 +482,32 @@ __device__ __forceinline__ uint32_t apply_chunk(const Tab& tab, const Chunk& c,
   return __popc(__ballot_sync(kFull, fresh));
 }
 
+// One whole B row (<= 32 entries) as a chunk: entry i of the group, one
+// product per lane (distinct columns). The fast path of medium_accumulate for
+// groups whose B rows all fit a warp and are long enough that packing several
+// into one chunk would not pay (C4: 27-entry rows) — no cursor bookkeeping.
+__device__ __forceinline__ Chunk entry_chunk(const DevCsr& B, const Group& g, uint32_t i) {
+  Chunk c;
+  c.n = 0;
+  c.single = true;
+  c.col = kEmptyKey;
+  c.bv = 0.0;
+  c.a = 0.0;
+  c.i_next = i + 1;
+  c.off_next = 0;
+  if (i < g.nent) {  // warp-uniform
+    const uint32_t lane = lane_id();
+    c.n = __shfl_sync(kFull, g.len, i & 31u);
+    const uint64_t bs = __shfl_sync(kFull, g.bs, i & 31u);
+    c.a = __shfl_sync(kFull, g.av, i & 31u);
+    if (lane < c.n) {
+      c.col = ld_idx(B.ci + bs + lane, B.pol);
+      c.bv = ld_val(B.v + bs + lane, B.pol);
+    }
+  }
+  return c;
+}
+
 // Accumulate the whole row into `tab`. Returns false (and leaves the table
 // dirty) if the row's distinct columns exceed `limit`.
 template <class Tab, bool STATS>
@@ -505,6 +531,26 @@ __device__ __forceinline__ bool medium_accumulate(const DevCsr& A, const DevCsr&
     }
     g.incl = warp_incl_scan(g.len);
     g.excl = g.incl - g.len;
+    const uint32_t lmax = __reduce_max_sync(kFull, g.len);
+    if (lmax <= 32 && __shfl_sync(kFull, g.incl, 31) >= 16u * g.nent) {
+      // every B row is one chunk, three in flight, applied in entry order
+      Chunk e0 = entry_chunk(B, g, 0), e1 = entry_chunk(B, g, 1), e2 = entry_chunk(B, g, 2);
+#pragma unroll 1
+      for (uint32_t i = 0; i < g.nent; i += 3) {
+        inserted += apply_chunk<Tab, STATS>(tab, e0, touches);
+        if (inserted > limit) return false;
+        e0 = entry_chunk(B, g, i + 3);
+        if (i + 1 >= g.nent) break;
+        inserted += apply_chunk<Tab, STATS>(tab, e1, touches);
+        if (inserted > limit) return false;
+        e1 = entry_chunk(B, g, i + 4);
+        if (i + 2 >= g.nent) break;
+        inserted += apply_chunk<Tab, STATS>(tab, e2, touches);
+        if (inserted > limit) return false;
+        e2 = entry_chunk(B, g, i + 5);
+      }
+      continue;
+    }
     // three chunks in flight
     Chunk c0 = make_chunk(B, g, 0, 0);
     Chunk c1 = make_chunk(B, g, c0.i_next, c0.off_next);
