@@ -72,7 +72,11 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       }
     }
     uint64_t p = 0;
-    const bool serial = hi - lo <= kSerial;
+    // rows past kSerial entries: the whole warp, one row at a time. When only
+    // a few rows of the warp pass 8 entries (skewed inputs), those go to the
+    // warp too, so 31 short rows do not wait on one lane's 30-entry loop.
+    const uint32_t few = __popc(__ballot_sync(kFull, hi - lo > 8));
+    const bool serial = hi - lo <= (few <= 4 ? 8 : kSerial);
     if (serial) {
       // four entries per round: their two dependent load levels overlap
       for (uint64_t e0 = lo; e0 < hi; e0 += 4) {
