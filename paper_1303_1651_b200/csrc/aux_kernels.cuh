@@ -111,15 +111,34 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       big &= big - 1;
       const uint64_t blo = __shfl_sync(kFull, lo, src), bhi = __shfl_sync(kFull, hi, src);
       uint64_t s = 0;
-      for (uint64_t e = blo + lane; e < bhi; e += 32) {
-        const uint64_t k = ld_idx(A.ci + e);
-        if (k >= B.rows) { err |= 2u; continue; }
-        const uint64_t b0 = ld_idx(B.rp + k), b1 = ld_idx(B.rp + k + 1);
-        if (b1 < b0 || b1 > B.nnz) { err |= 4u; continue; }
-        s += b1 - b0;
-        bmax = b1 - b0 > bmax ? b1 - b0 : bmax;
-        kmin = k < kmin ? k : kmin;
-        kmax1 = k + 1 > kmax1 ? k + 1 : kmax1;
+      // four entries per lane per round: a 4096-entry row is 32 rounds of two
+      // dependent loads, not 128 (such rows set the kernel's tail)
+      for (uint64_t e0 = blo + lane; e0 < bhi; e0 += 128) {
+        uint64_t k[4], b0[4], b1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t e = e0 + 32u * u;
+          k[u] = e < bhi ? ld_idx(A.ci + e) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          b0[u] = b1[u] = 0;
+          if (k[u] != ~0ull && k[u] < B.rows) {
+            b0[u] = ld_idx(B.rp + k[u]);
+            b1[u] = ld_idx(B.rp + k[u] + 1);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k[u] == ~0ull) continue;
+          if (k[u] >= B.rows) { err |= 2u; continue; }
+          if (b1[u] < b0[u] || b1[u] > B.nnz) { err |= 4u; continue; }
+          const uint64_t l = b1[u] - b0[u];
+          s += l;
+          bmax = l > bmax ? l : bmax;
+          kmin = k[u] < kmin ? k[u] : kmin;
+          kmax1 = k[u] + 1 > kmax1 ? k[u] + 1 : kmax1;
+        }
       }
       s = warp_sum64(s);
       if (lane == src) p = s;

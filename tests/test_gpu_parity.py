@@ -405,3 +405,26 @@ def test_full_size_drop_in_without_stats_matches_reference(label):
     assert d["row_ptr_sha256"] == fp["c"]["row_ptr_sha256"]
     assert d["col_idx_sha256"] == fp["c"]["col_idx_sha256"]
     assert d["values_sha256"] == fp["c"]["values_sha256"]
+
+
+def test_drop_in_pipelined_path_equals_stats_path():
+    """Without stats, large operands take spmmm_multiply_host (u32 column
+    indices down, widened on the host); with stats, the one-shot path. Same
+    bytes, and both match the oracle (A·A stencil and skewed A·B)."""
+    from paper_1303_1651_b200 import _lib as L
+    from paper_1303_1651_b200 import kernels as km
+
+    cases = [("fd600^2", genmat.gen_fd(600), None),
+             ("zipf200k", genmat.gen_zipf(200_000, 7), genmat.gen_zipf(200_000, 8))]
+    for name, a, b in cases:
+        b = a if b is None else b
+        assert len(a.values) >= km.PIPELINE_MIN_NNZ or name.startswith("zipf")
+        L.last_transfer = None
+        c_fast = multiply_rowmajor(a, b)
+        if len(a.values) >= km.PIPELINE_MIN_NNZ:
+            assert L.last_transfer is not None, name
+            assert L.last_transfer["d2h_bytes"] < 8 * (a.rows + 1) + 16 * len(c_fast.values)
+        stats = KernelStats()
+        c_stats = multiply_rowmajor(a, b, StrategyKind.COMBINED, stats)
+        assert_csr_bitwise_equal(c_fast, c_stats, name)
+        assert_csr_bitwise_equal(c_fast, _oracle_csr(a, b), name)
