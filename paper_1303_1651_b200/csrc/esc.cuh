@@ -319,6 +319,7 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, float inv_
 
 constexpr uint32_t kPartTarget = kEscBlockCap / 2;
 constexpr uint32_t kMaxParts = 64;
+constexpr uint32_t kGiantRow = 16384;  // planned first
 constexpr int kPlanThreads = 512;
 
 // One warp's segment [e0, e1) of A entries: count (SCATTER = false) or stage
@@ -422,11 +423,18 @@ __global__ void __launch_bounds__(kPlanThreads, 2) k_esc_plan(LongParams p) {
       s_over = 0;
     }
     __syncthreads();
-    const uint32_t h = s_h;
-    if (h >= n_huge) break;
+    // two sweeps over the list: rows past kGiantRow products first, so the
+    // longest rows do not start last and set the kernel's tail
+    const uint32_t t = s_h;
+    if (t >= 2 * n_huge) break;
+    const uint32_t h = t < n_huge ? t : t - n_huge;
     const uint32_t li = p.huge[h];
     const uint32_t r = p.list[li];
     const uint32_t P = p.prod[r];
+    if ((t < n_huge) != (P > kGiantRow)) {
+      __syncthreads();  // everyone has read s_h before the loop head rewrites it
+      continue;
+    }
     const uint64_t lo = ld_idx(pp.A.rp + r), hi = ld_idx(pp.A.rp + r + 1);
     // column range of the row (first and last column of every B row), and
     // where each warp's equal share of the row's products starts: the entry
