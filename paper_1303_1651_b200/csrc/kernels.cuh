@@ -206,6 +206,21 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       constexpr int kLock = R < SPMMM_LOCK ? R : SPMMM_LOCK;
       int ngroups = R / kLock;
       asm volatile("" : "+r"(ngroups));  // opaque: keep one copy of the group body
+      // ELL path, two groups: the second group's A entries are loaded now and
+      // its B records prefetched into L2 while the first group waits on its
+      // loads (one lane per (row, entry): 4 rows x 8 entries)
+      const uint32_t* pf1 = nullptr;
+      if constexpr (!MEDIUM) {
+        if (p.ell && ngroups > 1) {
+          const uint32_t pi = lane >> 3, pe = lane & 7;
+          const uint32_t src = uint32_t(kLock) + (pi < uint32_t(kLock) ? pi : 0u);
+          const uint64_t plo = __shfl_sync(kFull, rpv, src);
+          const uint32_t pna = __shfl_sync(kFull, my_na, src);
+          const uint32_t pcl = __shfl_sync(kFull, my_cls, src);
+          if (pi < uint32_t(kLock) && pcl == kRowShort && pe < pna && pe < kEllEntries)
+            pf1 = p.ell + ld_idx(p.A.ci + plo + pe, p.A.pol) * kEllWords;
+        }
+      }
 #pragma unroll 1
       for (int h = 0; h < ngroups; ++h) {
         uint64_t hlo[kLock];
@@ -222,7 +237,8 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
         for (int i = 0; i < kLock; ++i) any |= hon[i];
         if (!any) continue;
         ShortOut so[kLock];
-        short_rows<kLock, WIDE, STATS, !MEDIUM>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz, hmin, hmax, htouch);
+        short_rows<kLock, WIDE, STATS, !MEDIUM>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz, hmin,
+                                                hmax, htouch, h == 0 ? pf1 : nullptr);
 #pragma unroll
         for (int i = 0; i < kLock; ++i) {
           if (!hon[i]) continue;

@@ -42,7 +42,8 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
                                            const uint64_t (&lo)[R], const uint32_t (&na)[R],
                                            const bool (&on)[R], ShortOut (&out)[R],
                                            uint32_t (&nnz)[R], uint32_t (&smin)[R],
-                                           uint32_t (&smax)[R], uint32_t (&stouch)[R]) {
+                                           uint32_t (&smax)[R], uint32_t (&stouch)[R],
+                                           const uint32_t* pf = nullptr) {
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   // narrow variant: every index and offset fits 32 bits (checked on the host)
   using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
@@ -73,6 +74,8 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
         bv[i] = ld_val(reinterpret_cast<const double*>(rec + kEllValOff) + j, B.pol);
       }
     }
+    // the next group's records into L2 while this group waits on its own
+    if (pf) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pf));
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const bool valid = col[i] != kEmptyKey;
