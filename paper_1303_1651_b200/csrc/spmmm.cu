@@ -1177,11 +1177,17 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
       need[j] = uint64_t(u);
     }
   }
-  // 4. the result, in pinned host memory from the pool
+  // 4. the result, in pinned host memory from the pool. nnz(C) <= products,
+  // but stencil products compress ~6x (C4): reserve min(products, 8 nnz(A))
+  // and, should a block overflow that, redo the product in one shot (below).
+  const char* cap_knob = std::getenv("SPMMM_PIPE_CAP");  // test knob, read per call
+  const uint64_t cap_env = cap_knob ? std::strtoull(cap_knob, nullptr, 10) : 0;
+  const uint64_t cap = cap_env ? std::min(total, cap_env)
+                               : std::min(total, std::max<uint64_t>(8 * a->nnz, 1ull << 20));
   void *hrp = nullptr, *hci = nullptr, *hv = nullptr;
   rc = host_alloc_internal(rpb, &hrp);
-  if (!rc) rc = host_alloc_internal(std::max<uint64_t>(total, 1) * 8, &hci);
-  if (!rc) rc = host_alloc_internal(std::max<uint64_t>(total, 1) * 8, &hv);
+  if (!rc) rc = host_alloc_internal(std::max<uint64_t>(cap, 1) * 8, &hci);
+  if (!rc) rc = host_alloc_internal(std::max<uint64_t>(cap, 1) * 8, &hv);
   auto free_out = [&]() {
     host_free_internal(hrp);
     host_free_internal(hci);
@@ -1206,8 +1212,8 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   const bool narrow = total >= kNarrowMin && !no_narrow;
   void* hci32 = nullptr;
   if (narrow) {
-    CUDA_TRY(ensure(c->ci32, total * 4, c->stream));
-    rc = host_alloc_internal(total * 4, &hci32);
+    CUDA_TRY(ensure(c->ci32, cap * 4, c->stream));
+    rc = host_alloc_internal(cap * 4, &hci32);
     if (rc) {
       free_out();
       return drain(rc);
@@ -1279,6 +1285,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
       }
   };
   uint64_t off = 0, mults = 0;
+  bool overflow = false;
   for (int j = 0; j < G; ++j) {
     const uint64_t r0 = bound[j], r1 = bound[j + 1];
     if (r1 == r0) continue;
@@ -1295,6 +1302,10 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
       return rc;
     }
     spmmm_product* p = prods[j];
+    if (off + p->nnz > cap) {
+      overflow = true;
+      break;
+    }
     if (off) {
       k_add_offset<<<std::max<unsigned>(1, unsigned(std::min<uint64_t>((r1 - r0 + 256) / 256, 1024))),
                      256, 0, c->stream>>>(p->rp, r1 - r0 + 1, off);
@@ -1325,6 +1336,51 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     off += p->nnz;
     mults += p->mults;
     tr.mark("pipe: block computed, download issued");
+  }
+  if (overflow) {
+    // the reservation was too small: one product over the resident operands
+    // into exact-size arrays (the operands are all up once s_up drains)
+    guard.f = nullptr;
+    stop_workers();
+    CUDA_TRY(cudaStreamSynchronize(c->s_down));
+    CUDA_TRY(cudaStreamSynchronize(c->s_up));
+    release_all();
+    free_out();
+    tr.mark("pipe: reservation overflowed, one-shot product");
+    spmmm_csr va{a->rows, a->cols, a->nnz, d_arp, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
+    spmmm_csr vb{B.rows, B.cols, B.nnz, B.rp, B.ci, B.v, SPMMM_MEM_DEVICE, 0};
+    spmmm_product* p = nullptr;
+    rc = multiply_impl(c, &va, &vb, strategy, flags & SPMMM_FLAG_TIMING, &p);
+    if (rc) return rc;
+    hrp = hci = hv = nullptr;
+    rc = host_alloc_internal(rpb, &hrp);
+    if (!rc) rc = host_alloc_internal(std::max<uint64_t>(p->nnz, 1) * 8, &hci);
+    if (!rc) rc = host_alloc_internal(std::max<uint64_t>(p->nnz, 1) * 8, &hv);
+    cudaError_t e = rc ? cudaSuccess : cudaMemcpyAsync(hrp, p->rp, rpb, cudaMemcpyDeviceToHost,
+                                                       c->stream);
+    if (!rc && e == cudaSuccess && p->nnz)
+      e = cudaMemcpyAsync(hci, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (!rc && e == cudaSuccess && p->nnz)
+      e = cudaMemcpyAsync(hv, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    const uint64_t nnz = p->nnz, m = p->mults;
+    product_release(c, p);
+    delete p;
+    if (!rc && e != cudaSuccess) rc = fail(SPMMM_ERR_CUDA, "%s", cudaGetErrorString(e));
+    if (rc) {
+      free_out();
+      return rc;
+    }
+    out->rows = a->rows;
+    out->cols = b->cols;
+    out->nnz = nnz;
+    out->mults = m;
+    out->row_ptr = static_cast<uint64_t*>(hrp);
+    out->col_idx = static_cast<uint64_t*>(hci);
+    out->values = static_cast<double*>(hv);
+    out->h2d_bytes = rpb + a->nnz * 16 + (same ? 0 : (b->rows + 1) * 8 + b->nnz * 16);
+    out->d2h_bytes = rpb + nnz * 16;
+    return SPMMM_OK;
   }
   publish(G);  // (skipped empty blocks)
   if (tr.on) {

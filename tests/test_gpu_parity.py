@@ -352,9 +352,22 @@ def test_pipelined_host_product_matches_oracle(blocks):
     rect_a = _rand_csr(rng, 700, 300, 12, "quantized")
     rect_b = _rand_csr(rng, 300, 900, 10, "quantized")
     zero_a = CsrMatrix(50, 300, np.zeros(51, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    no_rows = CsrMatrix(0, 300, np.zeros(1, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    # empty rows around the block boundaries
+    gap_rp = np.array(rect_a.row_ptr, dtype=np.uint64).copy()
+    lens = np.diff(gap_rp.astype(np.int64))
+    lens[100:400] = 0
+    gap_ci = np.concatenate([np.asarray(rect_a.col_idx)[int(gap_rp[r]):int(gap_rp[r + 1])]
+                             for r in range(rect_a.rows) if lens[r]]).astype(np.uint64)
+    gap_v = np.concatenate([np.asarray(rect_a.values)[int(gap_rp[r]):int(gap_rp[r + 1])]
+                            for r in range(rect_a.rows) if lens[r]])
+    gap_rp2 = np.zeros(rect_a.rows + 1, np.uint64)
+    gap_rp2[1:] = np.cumsum(lens)
+    gap_a = CsrMatrix(rect_a.rows, rect_a.cols, gap_rp2, gap_ci, gap_v)
     ctx = _lib.Context(0)
     for name, a, b in [("fd200^2", fd, fd), ("zipf", z, genmat.gen_zipf(30_000, 6)),
                        ("rect", rect_a, rect_b), ("zero", zero_a, rect_b),
+                       ("no rows", no_rows, rect_b), ("gaps", gap_a, rect_b),
                        ("zipf^2", z, z)]:
         va, vb = _host_views(a, b)
         if b is a:
@@ -428,3 +441,24 @@ def test_drop_in_pipelined_path_equals_stats_path():
         c_stats = multiply_rowmajor(a, b, StrategyKind.COMBINED, stats)
         assert_csr_bitwise_equal(c_fast, c_stats, name)
         assert_csr_bitwise_equal(c_fast, _oracle_csr(a, b), name)
+
+
+def test_pipelined_host_product_reservation_overflow(monkeypatch):
+    """The pipelined path reserves min(products, 8 nnz(A)) result entries; a
+    result past the reservation is redone in one shot — same bytes. Forced
+    here with a tiny reservation (SPMMM_PIPE_CAP, read per call)."""
+    monkeypatch.setenv("SPMMM_PIPE_CAP", "1000")
+    ctx = _lib.Context(0)
+    for name, a, b in [("fd200^2", genmat.gen_fd(200), None),
+                       ("zipf", genmat.gen_zipf(30_000, 5), genmat.gen_zipf(30_000, 6))]:
+        b = a if b is None else b
+        va, vb = _host_views(a, b)
+        if b is a:
+            vb = va
+        rp, ci, v, mults = _lib.multiply_host(ctx, va, vb, 6, 0, 8)
+        ref = oracle.multiply_rowmajor(a, b, threads=8)
+        assert mults == ref.multiplications, name
+        assert_csr_bitwise_equal(CsrMatrix(a.rows, b.cols, rp, ci, v),
+                                 CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx,
+                                           ref.values), f"overflow/{name}")
+    ctx.close()
