@@ -207,9 +207,11 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       int ngroups = R / kLock;
       asm volatile("" : "+r"(ngroups));  // opaque: keep one copy of the group body
       // ELL path, two groups: the second group's A entries are loaded now and
-      // its B records prefetched into L2 while the first group waits on its
-      // loads (one lane per (row, entry): 4 rows x 8 entries)
-      const uint32_t* pf1 = nullptr;
+      // the B records they address are prefetched into L2 while the first
+      // group waits on its own loads (one lane per (row, entry): 4 rows x 8
+      // entries). (The same for B.row_ptr in the generic path measured
+      // neutral on C5.)
+      const void* pf1 = nullptr;
       if constexpr (!MEDIUM) {
         if (p.ell && ngroups > 1) {
           const uint32_t pi = lane >> 3, pe = lane & 7;
@@ -217,8 +219,10 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
           const uint64_t plo = __shfl_sync(kFull, rpv, src);
           const uint32_t pna = __shfl_sync(kFull, my_na, src);
           const uint32_t pcl = __shfl_sync(kFull, my_cls, src);
-          if (pi < uint32_t(kLock) && pcl == kRowShort && pe < pna && pe < kEllEntries)
+          if (pi < uint32_t(kLock) && pcl == kRowShort && pe < pna && pe < kEllEntries) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p.A.v + plo + pe));
             pf1 = p.ell + ld_idx(p.A.ci + plo + pe, p.A.pol) * kEllWords;
+          }
         }
       }
 #pragma unroll 1

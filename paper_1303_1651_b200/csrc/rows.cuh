@@ -43,7 +43,7 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
                                            const bool (&on)[R], ShortOut (&out)[R],
                                            uint32_t (&nnz)[R], uint32_t (&smin)[R],
                                            uint32_t (&smax)[R], uint32_t (&stouch)[R],
-                                           const uint32_t* pf = nullptr) {
+                                           const void* pf = nullptr) {
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   // narrow variant: every index and offset fits 32 bits (checked on the host)
   using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
