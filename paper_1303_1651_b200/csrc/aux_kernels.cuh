@@ -42,6 +42,28 @@ enum Ctrl : int {
 // (esc.cuh); k_count sums their products for the host
 constexpr uint32_t kHugeMin = 4096;
 
+// One ELL record: u32 col[6] (unused 0xffffffff) then f64 val[5] — B row r's
+// entries [lo, hi) (at most kEllSlots are stored).
+__device__ __forceinline__ void pack_ell_record(const DevCsr& B, uint64_t r, uint64_t lo,
+                                                uint64_t hi, uint4* __restrict__ ell) {
+  uint32_t c[kEllSlots + 1];
+  double v[kEllSlots];
+#pragma unroll
+  for (int j = 0; j < kEllSlots; ++j) {
+    const bool in = lo + j < hi;
+    c[j] = in ? uint32_t(ld_idx(B.ci + lo + j)) : kEmptyKey;
+    v[j] = in ? ld_val(B.v + lo + j) : 0.0;
+  }
+  c[kEllSlots] = kEmptyKey;
+  auto lo32 = [](double x) { return uint32_t(__double_as_longlong(x)); };
+  auto hi32 = [](double x) { return uint32_t(uint64_t(__double_as_longlong(x)) >> 32); };
+  uint4* rec = ell + r * 4;
+  rec[0] = make_uint4(c[0], c[1], c[2], c[3]);
+  rec[1] = make_uint4(c[4], c[5], lo32(v[0]), hi32(v[0]));
+  rec[2] = make_uint4(lo32(v[1]), hi32(v[1]), lo32(v[2]), hi32(v[2]));
+  rec[3] = make_uint4(lo32(v[3]), hi32(v[3]), lo32(v[4]), hi32(v[4]));
+}
+
 // ---------------------------------------------------------------------------
 // K1: per-row product counts. formats.py:276-289 per row. A warp takes 32
 // consecutive rows (one per lane); rows with many A entries are summed by the
@@ -50,7 +72,7 @@ constexpr uint32_t kHugeMin = 4096;
 __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
                                                unsigned long long* __restrict__ ctrl,
                                                unsigned long long* __restrict__ zero,
-                                               uint64_t nzero) {
+                                               uint64_t nzero, uint4* __restrict__ ell_self) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nzero;
        i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = 0;
@@ -143,6 +165,9 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       s = warp_sum64(s);
       if (lane == src) p = s;
     }
+    // C = A·A: row r of A is row r of B — its ELL record is written here, from
+    // entries this lane has just read, instead of by a k_pack_ell pass
+    if (ell_self && r < A.rows && hi - lo <= uint64_t(kEllSlots)) pack_ell_record(A, r, lo, hi, ell_self);
     if (r < A.rows) {
       if (p > 0x7fffffffull) err |= 8u;
       prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
@@ -242,22 +267,7 @@ __global__ void __launch_bounds__(256) k_pack_ell(DevCsr B, uint64_t a_rows,
     hi = hi < B.nnz ? hi : B.nnz;
     uint64_t lo = ld_idx(B.rp + r);
     lo = lo < hi ? lo : hi;
-    uint32_t c[kEllSlots + 1];
-    double v[kEllSlots];
-#pragma unroll
-    for (int j = 0; j < kEllSlots; ++j) {
-      const bool in = lo + j < hi;
-      c[j] = in ? uint32_t(ld_idx(B.ci + lo + j)) : kEmptyKey;
-      v[j] = in ? ld_val(B.v + lo + j) : 0.0;
-    }
-    c[kEllSlots] = kEmptyKey;
-    auto lo32 = [](double x) { return uint32_t(__double_as_longlong(x)); };
-    auto hi32 = [](double x) { return uint32_t(uint64_t(__double_as_longlong(x)) >> 32); };
-    uint4* rec = ell + r * 4;
-    rec[0] = make_uint4(c[0], c[1], c[2], c[3]);
-    rec[1] = make_uint4(c[4], c[5], lo32(v[0]), hi32(v[0]));
-    rec[2] = make_uint4(lo32(v[1]), hi32(v[1]), lo32(v[2]), hi32(v[2]));
-    rec[3] = make_uint4(lo32(v[3]), hi32(v[3]), lo32(v[4]), hi32(v[4]));
+    pack_ell_record(B, r, lo, hi, ell);
   }
 }
 
