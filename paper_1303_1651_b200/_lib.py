@@ -233,9 +233,10 @@ class Context:
         check(lib().spmmm_synchronize(self._h), "spmmm_synchronize")
 
     def last_timings(self) -> dict:
-        names = (ctypes.c_char_p * 16)()
-        ms = (ctypes.c_double * 16)()
-        n = ctypes.c_int(0)
+        # (buffers kept on the context: this is called once per bench step)
+        if not hasattr(self, "_tbuf"):
+            self._tbuf = ((ctypes.c_char_p * 16)(), (ctypes.c_double * 16)(), ctypes.c_int(0))
+        names, ms, n = self._tbuf
         check(lib().spmmm_last_timings(self._h, names, ms, 16, ctypes.byref(n)), "timings")
         return {names[i].decode(): ms[i] for i in range(min(n.value, 16))}
 
