@@ -72,7 +72,8 @@ __device__ __forceinline__ void pack_ell_record(const DevCsr& B, uint64_t r, uin
 __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
                                                unsigned long long* __restrict__ ctrl,
                                                unsigned long long* __restrict__ zero,
-                                               uint64_t nzero, uint4* __restrict__ ell_self) {
+                                               uint64_t nzero, uint4* __restrict__ ell_self,
+                                               uint4* __restrict__ ell_all) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nzero;
        i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = 0;
@@ -178,6 +179,19 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
         need = 1;
         ++nonshort;
       }
+    }
+  }
+  // speculative ELL copy of every B row (A != B, B rows of ~kEllSlots
+  // entries): the bandwidth-bound copy interleaves with the latency-bound
+  // count instead of following it; used only if k_count's results call for ELL
+  if (ell_all) {
+    for (uint64_t rb = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; rb < B.rows;
+         rb += uint64_t(gridDim.x) * blockDim.x) {
+      uint64_t bh = ld_idx(B.rp + rb + 1);
+      bh = bh < B.nnz ? bh : B.nnz;
+      uint64_t bl = ld_idx(B.rp + rb);
+      bl = bl < bh ? bl : bh;
+      pack_ell_record(B, rb, bl, bh, ell_all);
     }
   }
 #pragma unroll

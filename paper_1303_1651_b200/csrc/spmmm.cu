@@ -339,13 +339,20 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
   // C = A·A with A's rows its own B rows: k_count writes the ELL copy itself
   const bool self_pack = pack && A.rows && A.rp == B.rp && A.ci == B.ci && A.v == B.v &&
                          A.rows == B.rows;
+  // otherwise, B rows of about kEllSlots entries on average and A spanning
+  // most of B: k_count also copies every B row (speculatively)
+  static const bool no_spec = std::getenv("SPMMM_NO_SPEC_ELL") != nullptr;
+  const bool spec_pack = pack && !self_pack && !no_spec && A.rows && B.rows &&
+                         B.nnz <= uint64_t(kEllSlots) * B.rows + B.rows / 8 &&
+                         2 * A.rows >= B.rows;
   if (A.rows) {
     const uint64_t blocks = std::min<uint64_t>((A.rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(0);
     k_count<<<unsigned(blocks), 256, 0, c->stream>>>(
         A, B, static_cast<uint32_t*>(c->prod.p), static_cast<unsigned long long*>(c->ctrl.p),
         static_cast<unsigned long long*>(c->status.p), ncnt,
-        self_pack ? static_cast<uint4*>(c->ell.p) : nullptr);
+        self_pack ? static_cast<uint4*>(c->ell.p) : nullptr,
+        spec_pack ? static_cast<uint4*>(c->ell.p) : nullptr);
     CUDA_TRY(cudaGetLastError());
     tm.end(0);
     ++c->last_launches;
@@ -354,7 +361,7 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
   CUDA_TRY(readback(static_cast<const unsigned long long*>(c->ctrl.p), c->h_ctrl, kCtrlWords,
                     c->stream));
   CUDA_TRY(cudaEventRecord(c->ev_count, c->stream));
-  if (pack && A.rows && !self_pack) {
+  if (pack && A.rows && !self_pack && !spec_pack) {
     // the ELL copy of B (if k_count's results call for it) overlaps the readback
     tm.begin(8);
     k_pack_ell<<<unsigned(c->sms) * 16, 256, 0, c->stream>>>(
