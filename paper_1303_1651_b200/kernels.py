@@ -46,9 +46,16 @@ class StrategyKind(str, Enum):
 _STRATEGY_IDS = {s.value: i for i, s in enumerate(StrategyKind)}
 
 # multiply_rowmajor without stats on operands of at least this many A entries
-# takes the block-pipelined host path (spmmm_multiply_host)
-PIPELINE_MIN_NNZ = 1 << 20
-PIPELINE_BLOCKS = 8
+# takes the block-pipelined host path (spmmm_multiply_host), in row blocks of
+# about PIPELINE_BLOCK_NNZ A entries (2..8 blocks). Below it the per-block
+# fixed costs (a count readback each) outweigh the overlap (C2 sweep: grid
+# 512, 1.3M entries, pipelined 2.2 ms vs one-shot ~1.6 ms).
+PIPELINE_MIN_NNZ = 1 << 22
+PIPELINE_BLOCK_NNZ = 1 << 20
+
+
+def pipeline_blocks(nnz_a: int) -> int:
+    return max(2, min(8, nnz_a // PIPELINE_BLOCK_NNZ))
 
 
 @dataclass
@@ -119,7 +126,7 @@ def multiply_rowmajor(a, b, strategy=StrategyKind.COMBINED, stats=None):
     if stats is None and len(av) >= PIPELINE_MIN_NNZ:
         # large host operands: uploads, kernels and downloads overlap in row
         # blocks (spmmm_multiply_host); the same bytes as the path below
-        rp, ci, v, _ = _lib.multiply_host(ctx, va, vb, sid, 0, PIPELINE_BLOCKS)
+        rp, ci, v, _ = _lib.multiply_host(ctx, va, vb, sid, 0, pipeline_blocks(len(av)))
         return make_like(a, a.rows, b.cols, rp, ci, v)
     with _lib.multiply_views(ctx, va, vb, sid, flags) as product:
         rp, ci, v = product.download()

@@ -427,11 +427,11 @@ def test_drop_in_pipelined_path_equals_stats_path():
     from paper_1303_1651_b200 import _lib as L
     from paper_1303_1651_b200 import kernels as km
 
-    cases = [("fd600^2", genmat.gen_fd(600), None),
-             ("zipf200k", genmat.gen_zipf(200_000, 7), genmat.gen_zipf(200_000, 8))]
+    cases = [("fd1024^2", genmat.gen_fd(1024), None),
+             ("zipf800k", genmat.gen_zipf(800_000, 7), genmat.gen_zipf(800_000, 8))]
     for name, a, b in cases:
         b = a if b is None else b
-        assert len(a.values) >= km.PIPELINE_MIN_NNZ or name.startswith("zipf")
+        assert len(a.values) >= km.PIPELINE_MIN_NNZ, name
         L.last_transfer = None
         c_fast = multiply_rowmajor(a, b)
         if len(a.values) >= km.PIPELINE_MIN_NNZ:
