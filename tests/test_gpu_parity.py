@@ -462,3 +462,30 @@ def test_pipelined_host_product_reservation_overflow(monkeypatch):
                                  CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx,
                                            ref.values), f"overflow/{name}")
     ctx.close()
+
+
+@pytest.mark.parametrize("values", ["uniform", "quantized"])
+def test_split_mode_hash_kernels_past_esc_key_range(values):
+    """Columns past 2^23 do not fit ESC's 32-bit sort keys: split mode then
+    runs the hash-table kernels (k_rows, k_long_smem and its cluster variant,
+    k_long). Bitwise against the oracle, stats included."""
+    rng = np.random.default_rng(11)
+    n = 30_000
+    a = _skewed_csr(rng, n, n, 3000, values)
+    b = _skewed_csr(rng, n, 9_000_000, 200, values)
+    ref = oracle.multiply_rowmajor(a, b, row_choices=True, threads=8)
+    ctx = _lib.Context(0)
+    va = _lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values)
+    vb = _lib.csr_view(b.rows, b.cols, b.row_ptr, b.col_idx, b.values)
+    with _lib.multiply_views(ctx, va, vb, 6, _lib.FLAG_TIMING | _lib.FLAG_ROW_STATS) as p:
+        rp, ci, v = p.download()
+        names = set(ctx.last_timings())
+        stats = KernelStats()
+        from paper_1303_1651_b200.kernels import _record_row_choices
+        _record_row_choices(stats, p, StrategyKind, a.row_ptr)
+    ctx.close()
+    assert "k_rows" in names and "k_esc_warp" not in names, names
+    assert_csr_bitwise_equal(CsrMatrix(a.rows, b.cols, rp, ci, v),
+                             CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx, ref.values),
+                             f"hash/{values}")
+    assert np.array_equal(_choices_array(stats, a.rows), ref.row_choices)
