@@ -350,7 +350,7 @@ struct LongParams {
   unsigned long long* ctrl;
   uint64_t* l_off;
   uint32_t* l_nnz;
-  uint64_t* l_ci;
+  uint32_t* l_ci;  // staged columns (u32: columns < 2^32; widened by k_copy_long)
   double* l_v;
   uint32_t* ws_keys;   // [grid][slots]
   double* ws_vals;     // [grid][slots]
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
           const uint32_t col = (w << 5) | bit;
           const double v = __ldcg(vals + long_probe(keys, col, mask));
           zero |= v == 0.0;
-          p.l_ci[pos] = col;
+          p.l_ci[pos] = uint32_t(col);
           p.l_v[pos] = v;
           ++pos;
         }
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kLongThreads) k_long(LongParams p) {
       uint32_t out = 0;
       for (uint32_t c0 = 0; c0 < n_out; c0 += NT) {
         const uint32_t i = c0 + tid;
-        uint64_t ci = 0;
+        uint32_t ci = 0;
         double v = 0.0;
         bool keep = false;
         if (i < n_out) {
@@ -652,7 +652,7 @@ struct CopyParams {
   unsigned long long* tickets;  // [0] big rows, [1] other rows
   const uint64_t* l_off;
   const uint32_t* l_nnz;
-  const uint64_t* l_ci;
+  const uint32_t* l_ci;
   const double* l_v;
   const uint64_t* c_rp;
   uint64_t* c_ci;
@@ -674,7 +674,7 @@ struct CopyParams {
 template <int U>
 __device__ __forceinline__ void copy_run(unsigned long long* __restrict__ dci,
                                          double* __restrict__ dv,
-                                         const uint64_t* __restrict__ sci,
+                                         const uint32_t* __restrict__ sci,
                                          const double* __restrict__ sv, uint32_t n,
                                          uint32_t t0, uint32_t step) {
   uint32_t i = t0;
@@ -1126,7 +1126,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
         const uint32_t k = keys[s];
         if (k != kEmptyKey) {
           const uint32_t pos = atomicAdd(cursor + ((k - kmin) >> sh), 1u);
-          __stcg(p.l_ci + off + pos, uint64_t(k));
+          __stcg(p.l_ci + off + pos, uint32_t(k));
           __stcg(p.l_v + off + pos, vals[s]);
           keys[s] = kEmptyKey;
         }
@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
           key[e2] = ~0u;
           v[e2] = 0.0;
           if (idx < sz) {
-            key[e2] = ((uint32_t(__ldcg(p.l_ci + base + idx)) - blo) << 6) | idx;
+            key[e2] = ((__ldcg(p.l_ci + base + idx) - blo) << 6) | idx;
             v[e2] = __ldcg(p.l_v + base + idx);
           }
         }
@@ -1165,7 +1165,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
           const double t0 = __shfl_sync(kFull, v[0], pos & 31u);
           const double t1 = __shfl_sync(kFull, v[1], pos & 31u);
           if (idx < sz) {
-            __stcg(p.l_ci + base + idx, uint64_t(blo + (key[e2] >> 6)));
+            __stcg(p.l_ci + base + idx, uint32_t(blo + (key[e2] >> 6)));
             __stcg(p.l_v + base + idx, (pos >> 5) ? t1 : t0);
           }
         }
@@ -1180,7 +1180,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
           uint32_t np = 1;
           while (np < sz) np <<= 1;
           for (uint32_t t = tid; t < np; t += NT) {
-            keys[t] = t < sz ? uint32_t(__ldcg(p.l_ci + base + t)) : kEmptyKey;
+            keys[t] = t < sz ? __ldcg(p.l_ci + base + t) : kEmptyKey;
             if (t < sz) vals[t] = __ldcg(p.l_v + base + t);
           }
           __syncthreads();
@@ -1201,7 +1201,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long_smem(LongParams p) {
             }
           }
           for (uint32_t t = tid; t < sz; t += NT) {
-            __stcg(p.l_ci + base + t, uint64_t(keys[t]));
+            __stcg(p.l_ci + base + t, keys[t]);
             __stcg(p.l_v + base + t, vals[t]);
           }
           __syncthreads();

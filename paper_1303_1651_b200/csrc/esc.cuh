@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
       const uint32_t m = __ballot_sync(kFull, keep);
       if (keep) {
         const uint64_t pos = off + cnt + __popc(m & lanemask_lt());
-        __stcs(p.l_ci + pos, uint64_t(skey[i] >> kEscQBits));
+        __stcs(p.l_ci + pos, skey[i] >> kEscQBits);
         __stcs(p.l_v + pos, acc);
       }
       cnt += __popc(m);
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(kEscThreads, 2) k_esc_block(LongParams p, uint
         const uint32_t m = __ballot_sync(kFull, keep);
         if (keep) {
           const uint64_t pos = off + o + __popc(m & lanemask_lt());
-          __stcs(p.l_ci + pos, uint64_t(blo + (key >> qb)));
+          __stcs(p.l_ci + pos, blo + (key >> qb));
           __stcs(p.l_v + pos, v);
         }
         o += __popc(m);

@@ -393,7 +393,7 @@ struct RowsParams {
   unsigned long long* ticket;  // dynamic row counter
   uint64_t* l_off;
   uint32_t* l_nnz;
-  uint64_t* l_ci;
+  uint32_t* l_ci;
   double* l_v;
   uint32_t* st_min;
   uint32_t* st_max;
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kRowsWarps * 32, 2) k_rows(const RowsParams p_
     if (lane == 0) off = atomicAdd(p.cursor, (unsigned long long)cnt);
     off = __shfl_sync(kFull, off, 0);
     for (uint32_t t2 = lane; t2 < cnt; t2 += 32) {
-      __stcs(p.l_ci + off + t2, uint64_t(vk[t2]));
+      __stcs(p.l_ci + off + t2, vk[t2]);
       __stcs(p.l_v + off + t2, vv[t2]);
       vk[t2] = kEmptyKey;
     }

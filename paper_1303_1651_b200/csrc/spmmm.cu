@@ -499,7 +499,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   // rows past huge_min: the cluster variant (and k_long for its overflow)
   const uint32_t huge_min = esc ? kEscBlockCap : kLongSmemProducts;
   tr.mark("  run_long: lists");
-  CUDA_TRY(ensure(stage_ci, total * sizeof(uint64_t), c->stream));
+  CUDA_TRY(ensure(stage_ci, total * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(stage_v, total * sizeof(double), c->stream));
   tr.mark("  run_long: buffers");
   const bool any_huge = max_prod > huge_min;  // some row needs the cluster / k_long
@@ -551,7 +551,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     rp.ticket = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlRowsTicket;
     rp.l_off = static_cast<uint64_t*>(c->l_off.p);
     rp.l_nnz = static_cast<uint32_t*>(c->l_nnz.p);
-    rp.l_ci = static_cast<uint64_t*>(stage_ci.p);
+    rp.l_ci = static_cast<uint32_t*>(stage_ci.p);
     rp.l_v = static_cast<double*>(stage_v.p);
     rp.st_min = p->st;
     rp.st_max = p->st ? p->st + rows : nullptr;
@@ -623,7 +623,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   lp.ctrl = static_cast<unsigned long long*>(c->ctrl.p);
   lp.l_off = static_cast<uint64_t*>(c->l_off.p);
   lp.l_nnz = static_cast<uint32_t*>(c->l_nnz.p);
-  lp.l_ci = static_cast<uint64_t*>(stage_ci.p);
+  lp.l_ci = static_cast<uint32_t*>(stage_ci.p);
   lp.l_v = static_cast<double*>(stage_v.p);
   char* base = static_cast<char*>(c->ws.p);
   const size_t n = size_t(c->ws_grid) * c->ws_slots;
@@ -913,7 +913,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       cp.tickets = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCopyTickets;
       cp.l_off = static_cast<const uint64_t*>(c->l_off.p);
       cp.l_nnz = static_cast<const uint32_t*>(c->l_nnz.p);
-      cp.l_ci = static_cast<const uint64_t*>(stage_ci.p);
+      cp.l_ci = static_cast<const uint32_t*>(stage_ci.p);
       cp.l_v = static_cast<const double*>(stage_v.p);
       cp.c_rp = p->rp;
       cp.c_ci = p->ci;
