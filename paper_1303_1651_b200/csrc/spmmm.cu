@@ -1117,15 +1117,16 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   CUDA_TRY(cudaMemcpyAsync(d_arp, a->row_ptr, rpb, cudaMemcpyHostToDevice, c->s_up));
   if (a->nnz)
     CUDA_TRY(cudaMemcpyAsync(d_aci, a->col_idx, a->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
-  if (!same) {
+  // the count pass needs A's structure and B's row pointers only; B's columns
+  // and values follow it (every block needs all of B when A != B)
+  if (!same)
     CUDA_TRY(cudaMemcpyAsync(c->b_rp.p, b->row_ptr, (b->rows + 1) * 8, cudaMemcpyHostToDevice,
                              c->s_up));
-    if (b->nnz)
-      CUDA_TRY(cudaMemcpyAsync(c->b_ci.p, b->col_idx, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
-  }
   CUDA_TRY(cudaEventRecord(*ev_struct, c->s_up));
-  if (!same && b->nnz)
+  if (!same && b->nnz) {
+    CUDA_TRY(cudaMemcpyAsync(c->b_ci.p, b->col_idx, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
     CUDA_TRY(cudaMemcpyAsync(c->b_v.p, b->values, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
+  }
   CUDA_TRY(cudaEventRecord(*ev_bv, c->s_up));
   // row blocks of about equal nnz(A); A's values go up block by block
   uint64_t bound[kMaxPipeBlocks + 1];
