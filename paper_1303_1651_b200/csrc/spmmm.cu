@@ -1206,6 +1206,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     host_free_internal(hrp);
     host_free_internal(hci);
     host_free_internal(hv);
+    hrp = hci = hv = nullptr;
   };
   if (rc) {
     free_out();
@@ -1283,21 +1284,28 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     if (hci32) host_free_internal(hci32);
     hci32 = nullptr;
   };
-  // every early return below (CUDA_TRY included) stops the workers first
-  struct WorkerGuard {
-    std::function<void()> f;
-    ~WorkerGuard() {
-      if (f) f();
-    }
-  } guard{stop_workers};
   spmmm_product* prods[kMaxPipeBlocks] = {};
   auto release_all = [&]() {
     for (int j = 0; j < G; ++j)
       if (prods[j]) {
         product_release(c, prods[j]);
         delete prods[j];
+        prods[j] = nullptr;
       }
   };
+  // every early return below (CUDA_TRY included) stops the workers, drains the
+  // streams and returns the blocks and the result arrays
+  struct Guard {
+    std::function<void()> f;
+    ~Guard() {
+      if (f) f();
+    }
+  } guard{[&]() {
+    stop_workers();
+    drain(0);
+    release_all();
+    free_out();
+  }};
   uint64_t off = 0, mults = 0;
   bool overflow = false;
   for (int j = 0; j < G; ++j) {
@@ -1308,13 +1316,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     spmmm_csr va{r1 - r0, a->cols, a->nnz, d_arp + r0, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
     spmmm_csr vb{B.rows, B.cols, B.nnz, B.rp, B.ci, B.v, SPMMM_MEM_DEVICE, 0};
     rc = multiply_impl(c, &va, &vb, strategy, flags & SPMMM_FLAG_TIMING, &prods[j]);
-    if (rc) {
-      drain(0);
-      stop_workers();
-      release_all();
-      free_out();
-      return rc;
-    }
+    if (rc) return rc;  // (the guard cleans up)
     spmmm_product* p = prods[j];
     if (off + p->nnz > cap) {
       overflow = true;
@@ -1354,19 +1356,18 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   if (overflow) {
     // the reservation was too small: one product over the resident operands
     // into exact-size arrays (the operands are all up once s_up drains)
-    guard.f = nullptr;
     stop_workers();
     CUDA_TRY(cudaStreamSynchronize(c->s_down));
     CUDA_TRY(cudaStreamSynchronize(c->s_up));
     release_all();
     free_out();
+    guard.f = nullptr;
     tr.mark("pipe: reservation overflowed, one-shot product");
     spmmm_csr va{a->rows, a->cols, a->nnz, d_arp, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
     spmmm_csr vb{B.rows, B.cols, B.nnz, B.rp, B.ci, B.v, SPMMM_MEM_DEVICE, 0};
     spmmm_product* p = nullptr;
     rc = multiply_impl(c, &va, &vb, strategy, flags & SPMMM_FLAG_TIMING, &p);
     if (rc) return rc;
-    hrp = hci = hv = nullptr;
     rc = host_alloc_internal(rpb, &hrp);
     if (!rc) rc = host_alloc_internal(std::max<uint64_t>(p->nnz, 1) * 8, &hci);
     if (!rc) rc = host_alloc_internal(std::max<uint64_t>(p->nnz, 1) * 8, &hv);
@@ -1404,11 +1405,12 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   for (auto& t : workers) t.join();
   tr.mark("pipe: widening done");
   workers.clear();
-  guard.f = nullptr;
   if (hci32) host_free_internal(hci32);
+  hci32 = nullptr;
   CUDA_TRY(cudaStreamSynchronize(c->s_down));
   CUDA_TRY(cudaStreamSynchronize(c->s_up));
   tr.mark("pipe: downloads done");
+  guard.f = nullptr;  // success: the result arrays are the caller's
   release_all();
   out->rows = a->rows;
   out->cols = b->cols;
