@@ -40,7 +40,7 @@ enum Ctrl : int {
 
 // rows past this many products are split into column-range parts in ESC mode
 // (esc.cuh); k_count sums their products for the host
-constexpr uint32_t kHugeMin = 4096;
+constexpr uint32_t kHugeMin = 5120;
 
 // One ELL record: u32 col[6] (unused 0xffffffff) then f64 val[5] — B row r's
 // entries [lo, hi) (at most kEllSlots are stored).

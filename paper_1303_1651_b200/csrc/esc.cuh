@@ -317,7 +317,7 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, float inv_
   return q;
 }
 
-constexpr uint32_t kPartTarget = 2816;  // products per part (2048 and 1536 measured slower)
+constexpr uint32_t kPartTarget = 3584;  // products per part (1536-2816 measured slower)
 constexpr uint32_t kMaxParts = 64;
 constexpr uint32_t kGiantRow = 16384;  // planned first
 constexpr int kPlanThreads = 512;
