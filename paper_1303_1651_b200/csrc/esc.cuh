@@ -16,11 +16,14 @@
 // So C[r, x] is bit-identical to the reference, like every other path.
 //
 //   k_esc_warp:  rows of <= kEscWarpLimit products, one warp per row, keys
-//                sorted in registers (runtime-loop bitonic network).
-//   k_esc_block: rows of (kEscWarpLimit, cap] products, one block per row:
-//                one counting pass partitions the keys into column-range
-//                buckets of ~32 (so a bucket is a small independent sort),
-//                one warp sorts and folds each bucket in registers.
+//                sorted in registers (bitonic network per width).
+//   k_esc_plan:  rows past kEscBlockCap products: cut into column-range parts
+//                whose products are staged in q order.
+//   k_esc_block: work items of <= kEscBlockCap products (the rows between,
+//                whole, and the parts), one block each: one counting pass
+//                partitions the keys into column-range buckets of 24-48 keys
+//                (so a bucket is a small independent sort), one warp sorts
+//                and folds each bucket in registers.
 // Keys are 32-bit: (column << 9 | q) in the warp kernel (columns < 2^23,
 // checked on the host), (column offset in bucket << qbits | q) in the block
 // kernel.
