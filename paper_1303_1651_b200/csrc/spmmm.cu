@@ -136,7 +136,7 @@ struct spmmm_context {
   DevBuf parts, part_off, part_nnz, row_parts, scr_col, scr_val;  // ESC parts of huge rows
   // spmmm_multiply_host: copy streams (uploads, downloads) and their events
   cudaStream_t s_up = nullptr, s_down = nullptr;
-  cudaEvent_t pev[4 * kMaxPipeBlocks + 2] = {};
+  cudaEvent_t pev[5 * kMaxPipeBlocks + 2] = {};
   DevBuf ci32;                         // narrowed column indices of C blocks
   // split mode: k_esc_warp runs on its own stream beside k_esc_plan/k_esc_block
   cudaStream_t s_aux = nullptr;
@@ -1113,22 +1113,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   uint64_t* d_arp = static_cast<uint64_t*>(c->a_rp.p);
   uint64_t* d_aci = static_cast<uint64_t*>(c->a_ci.p);
   double* d_av = static_cast<double*>(c->a_v.p);
-  // 1. structure (and B's values) up
-  CUDA_TRY(cudaMemcpyAsync(d_arp, a->row_ptr, rpb, cudaMemcpyHostToDevice, c->s_up));
-  if (a->nnz)
-    CUDA_TRY(cudaMemcpyAsync(d_aci, a->col_idx, a->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
-  // the count pass needs A's structure and B's row pointers only; B's columns
-  // and values follow it (every block needs all of B when A != B)
-  if (!same)
-    CUDA_TRY(cudaMemcpyAsync(c->b_rp.p, b->row_ptr, (b->rows + 1) * 8, cudaMemcpyHostToDevice,
-                             c->s_up));
-  CUDA_TRY(cudaEventRecord(*ev_struct, c->s_up));
-  if (!same && b->nnz) {
-    CUDA_TRY(cudaMemcpyAsync(c->b_ci.p, b->col_idx, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
-    CUDA_TRY(cudaMemcpyAsync(c->b_v.p, b->values, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
-  }
-  CUDA_TRY(cudaEventRecord(*ev_bv, c->s_up));
-  // row blocks of about equal nnz(A); A's values go up block by block
+  // row blocks of about equal nnz(A)
   uint64_t bound[kMaxPipeBlocks + 1];
   bound[0] = 0;
   for (int j = 1; j < G; ++j) {
@@ -1138,26 +1123,58 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     bound[j] = std::min<uint64_t>(bound[j], a->rows);
   }
   bound[G] = a->rows;
-  // the value uploads below trust these entries (k_count checks the rest)
+  // the uploads below trust these entries (each block's k_count checks the rest)
   for (int j = 0; j < G && a->rows; ++j)
     if (arp[bound[j]] > arp[bound[j + 1]] || arp[bound[j + 1]] > a->nnz)
       return fail(SPMMM_ERR_INVALID, "malformed a.row_ptr (decreasing or past nnz)");
+  // 1. uploads, in the order the blocks need them. A != B: all of B first
+  // (any A row may read any B row). Then A block by block — row pointers,
+  // columns, values — and for C = A·A each block's largest column as soon as
+  // its columns are up: it names the last row of B = A that the block reads.
+  // No global count pass: block 0 starts as soon as its inputs are resident
+  // (each block's own count validates it and sizes its part of C).
+  cudaEvent_t* ev_maxc = &c->pev[2 + 4 * kMaxPipeBlocks];
+  uint64_t* d_aux = static_cast<uint64_t*>(c->aux.p);
+  if (!same) {
+    CUDA_TRY(cudaMemcpyAsync(c->b_rp.p, b->row_ptr, (b->rows + 1) * 8, cudaMemcpyHostToDevice,
+                             c->s_up));
+    if (b->nnz) {
+      CUDA_TRY(cudaMemcpyAsync(c->b_ci.p, b->col_idx, b->nnz * 8, cudaMemcpyHostToDevice,
+                               c->s_up));
+      CUDA_TRY(cudaMemcpyAsync(c->b_v.p, b->values, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
+    }
+  }
+  CUDA_TRY(cudaEventRecord(*ev_bv, c->s_up));
   for (int j = 0; j < G; ++j) {
-    const uint64_t e0 = a->rows ? arp[bound[j]] : 0, e1 = a->rows ? arp[bound[j + 1]] : 0;
+    const uint64_t r0 = bound[j], r1 = bound[j + 1];
+    const uint64_t e0 = a->rows ? arp[r0] : 0, e1 = a->rows ? arp[r1] : 0;
+    CUDA_TRY(cudaMemcpyAsync(d_arp + r0, arp + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice,
+                             c->s_up));
+    if (e1 > e0)
+      CUDA_TRY(cudaMemcpyAsync(d_aci + e0, a->col_idx + e0, (e1 - e0) * 8,
+                               cudaMemcpyHostToDevice, c->s_up));
+    if (same && r1 > r0) {
+      PipeBounds pb;
+      pb.r[0] = r0;
+      pb.r[1] = r1;
+      k_zero_u64<<<1, 32, 0, c->s_up>>>(d_aux + j, 1);
+      k_block_maxcol<<<kPipeSplit, 256, 0, c->s_up>>>(
+          d_arp, d_aci, pb, reinterpret_cast<unsigned long long*>(d_aux + j));
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(readback(reinterpret_cast<const unsigned long long*>(d_aux + j), c->h_aux + j, 1,
+                        c->s_up));
+      CUDA_TRY(cudaEventRecord(ev_maxc[j], c->s_up));
+    }
     if (e1 > e0)
       CUDA_TRY(cudaMemcpyAsync(d_av + e0, a->values + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice,
                                c->s_up));
     CUDA_TRY(cudaEventRecord(ev_av[j], c->s_up));
   }
-  // 2. one count pass over all of A: validation, and the size of the result
-  CUDA_TRY(cudaStreamWaitEvent(c->stream, *ev_struct, 0));
-  DevCsr A{d_arp, d_aci, d_av, a->rows, a->cols, a->nnz};
-  DevCsr B = A;
+  DevCsr B{d_arp, d_aci, d_av, a->rows, a->cols, a->nnz};
   if (!same)
     B = DevCsr{static_cast<const uint64_t*>(c->b_rp.p), static_cast<const uint64_t*>(c->b_ci.p),
                static_cast<const double*>(c->b_v.p), b->rows, b->cols, b->nnz};
   B.cols = b->cols;
-  Timer tm0{c, false};
   auto drain = [&](int code) {
     cudaStreamSynchronize(c->s_up);
     cudaStreamSynchronize(c->s_down);
@@ -1165,39 +1182,12 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     return code;
   };
   tr.mark("pipe: uploads issued");
-  rc = run_count(c, A, B, tm0, false);
-  if (rc) return drain(rc);
-  tr.mark("pipe: count done");
-  const uint64_t total = c->h_ctrl[kCtrlTotal];
-  // 3. A·A: block j reads B rows up to its largest column
-  uint64_t need[kMaxPipeBlocks];
-  for (int j = 0; j < G; ++j) need[j] = uint64_t(j);
-  if (same && a->rows) {
-    uint64_t* d_aux = static_cast<uint64_t*>(c->aux.p);
-    // (bounds by value: a small memcpy would queue behind the uploads)
-    PipeBounds pb;
-    for (int j = 0; j <= G; ++j) pb.r[j] = bound[j];
-    k_zero_u64<<<1, 32, 0, c->stream>>>(d_aux, G);
-    k_block_maxcol<<<G * kPipeSplit, 256, 0, c->stream>>>(d_arp, d_aci, pb,
-                                             reinterpret_cast<unsigned long long*>(d_aux));
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(readback(reinterpret_cast<const unsigned long long*>(d_aux), c->h_aux, G, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    tr.mark("pipe: max columns read back");
-    for (int j = 0; j < G; ++j) {
-      const uint64_t row = c->h_aux[j];  // rows [0, row] of B = A must be resident
-      int u = int(std::upper_bound(bound, bound + G + 1, row) - bound) - 1;
-      u = std::min(std::max(u, j), G - 1);
-      need[j] = uint64_t(u);
-    }
-  }
-  // 4. the result, in pinned host memory from the pool. nnz(C) <= products,
-  // but stencil products compress ~6x (C4): reserve min(products, 8 nnz(A))
-  // and, should a block overflow that, redo the product in one shot (below).
+  // 4. the result, in pinned host memory from the pool: 8 nnz(A) entries
+  // (C2 2.6, C3 5, C4 4.6, C5 6 nnz(C) per A entry); should a block overflow
+  // that, the product is redone in one shot (below).
   const char* cap_knob = std::getenv("SPMMM_PIPE_CAP");  // test knob, read per call
   const uint64_t cap_env = cap_knob ? std::strtoull(cap_knob, nullptr, 10) : 0;
-  const uint64_t cap = cap_env ? std::min(total, cap_env)
-                               : std::min(total, std::max<uint64_t>(8 * a->nnz, 1ull << 20));
+  const uint64_t cap = cap_env ? cap_env : std::max<uint64_t>(8 * a->nnz, 1ull << 20);
   void *hrp = nullptr, *hci = nullptr, *hv = nullptr;
   rc = host_alloc_internal(rpb, &hrp);
   if (!rc) rc = host_alloc_internal(std::max<uint64_t>(cap, 1) * 8, &hci);
@@ -1224,7 +1214,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   static const bool no_narrow = std::getenv("SPMMM_NO_NARROW") != nullptr;
   static const int widen_threads = std::getenv("SPMMM_WIDEN_THREADS")
                                        ? std::atoi(std::getenv("SPMMM_WIDEN_THREADS")) : 0;
-  const bool narrow = total >= kNarrowMin && !no_narrow;
+  const bool narrow = cap >= kNarrowMin && !no_narrow;
   void* hci32 = nullptr;
   if (narrow) {
     CUDA_TRY(ensure(c->ci32, cap * 4, c->stream));
@@ -1311,7 +1301,14 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   for (int j = 0; j < G; ++j) {
     const uint64_t r0 = bound[j], r1 = bound[j + 1];
     if (r1 == r0) continue;
-    CUDA_TRY(cudaStreamWaitEvent(c->stream, ev_av[same ? need[j] : j], 0));
+    int u = j;  // the last A block this block needs resident
+    if (same && a->rows) {
+      CUDA_TRY(cudaEventSynchronize(ev_maxc[j]));
+      const uint64_t row = c->h_aux[j];  // rows [0, row] of B = A (row_ptr to row + 1)
+      const int uu = int(std::upper_bound(bound, bound + G + 1, row) - bound) - 1;
+      u = std::min(std::max(uu, j), G - 1);
+    }
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, ev_av[u], 0));
     if (!same) CUDA_TRY(cudaStreamWaitEvent(c->stream, *ev_bv, 0));
     spmmm_csr va{r1 - r0, a->cols, a->nnz, d_arp + r0, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
     spmmm_csr vb{B.rows, B.cols, B.nnz, B.rp, B.ci, B.v, SPMMM_MEM_DEVICE, 0};

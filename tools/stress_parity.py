@@ -49,7 +49,7 @@ def case(rng):
     kind = rng.choice(["uniform", "zipf", "wide", "dense", "narrow"])
     values = rng.choice(["uniform", "quantized", "zeros"])
     m = int(rng.integers(1, 20000))
-    k = int(rng.integers(1, 20000))
+    k = m if rng.random() < 0.3 else int(rng.integers(1, 20000))
     n = int(rng.integers(1, 30000))
     if kind == "uniform":
         la = rng.integers(0, 40, m)
@@ -84,6 +84,24 @@ def check(name, a, b):
                            (c.values, ref.values, "values")):
             if np.asarray(x).tobytes() != np.asarray(y).tobytes():
                 raise AssertionError(f"{name} [{tag}]: {what} differs")
+    # the pipelined host path directly, random block count (A·A when square)
+    ctx = _lib.default_context()
+    va = _lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values)
+    for bb, vb in ((b, _lib.csr_view(b.rows, b.cols, b.row_ptr, b.col_idx, b.values)),):
+        blocks = int(np.random.default_rng(a.rows).integers(1, 17))
+        rp, ci, v, m = _lib.multiply_host(ctx, va, vb, 6, 0, blocks)
+        for x, y, what in ((rp, ref.row_ptr, "row_ptr"), (ci, ref.col_idx, "col_idx"),
+                           (v, ref.values, "values")):
+            if np.asarray(x).tobytes() != np.asarray(y).tobytes():
+                raise AssertionError(f"{name} [pipelined, {blocks} blocks]: {what} differs")
+    if a.rows == a.cols == b.rows:
+        # C = A·A through the pipelined path (blocks wait for the rows they read)
+        ref2 = oracle.multiply_rowmajor(a, a, threads=8)
+        rp, ci, v, m = _lib.multiply_host(ctx, va, va, 6, 0, 1 + a.rows % 16)
+        for x, y, what in ((rp, ref2.row_ptr, "row_ptr"), (ci, ref2.col_idx, "col_idx"),
+                           (v, ref2.values, "values")):
+            if np.asarray(x).tobytes() != np.asarray(y).tobytes():
+                raise AssertionError(f"{name} [pipelined A·A]: {what} differs")
     ch = np.full(a.rows, -1, np.int8)
     for r, s in stats.row_choices:
         ch[r] = 0 if s == StrategyKind.MIN_MAX else 1
