@@ -508,13 +508,19 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   uint64_t distinct = std::min<uint64_t>(max_prod, std::max<uint64_t>(B.cols, 1));
   uint64_t slots = 64;
   while (slots < 2 * distinct) slots <<= 1;
-  const uint64_t words = std::max<uint64_t>((B.cols + 31) / 32, 1);
+  uint64_t words = std::max<uint64_t>((B.cols + 31) / 32, 1);
+  // grow-only: a bigger table or bitmap than this product needs works as well
+  // (k_long restores both after every row), and the row blocks of one
+  // pipelined product differ in their longest row
+  const bool grow = any_huge && (!c->ws.p || slots > c->ws_slots || words > c->ws_words);
+  slots = std::max<uint64_t>(slots, c->ws_slots);
+  words = std::max<uint64_t>(words, c->ws_words);
   const uint64_t swords = (words + 31) / 32;
   const uint64_t per_block = slots * (4 + 8 + 4) + (words + swords) * 4;
   int grid = 2 * c->sms;
   const uint64_t budget = 8ull << 30;  // cap the workspace at 8 GiB
   while (grid > 1 && uint64_t(grid) * per_block > budget) grid /= 2;
-  if (any_huge && (slots != c->ws_slots || words != c->ws_words || grid != c->ws_grid)) {
+  if (grow) {
     release(c->ws, c->stream);
     CUDA_TRY(ensure(c->ws, size_t(grid) * per_block, c->stream));
     char* base = static_cast<char*>(c->ws.p);

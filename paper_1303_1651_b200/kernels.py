@@ -47,7 +47,7 @@ _STRATEGY_IDS = {s.value: i for i, s in enumerate(StrategyKind)}
 
 # multiply_rowmajor without stats on operands of at least this many A entries
 # takes the block-pipelined host path (spmmm_multiply_host), in row blocks of
-# about PIPELINE_BLOCK_NNZ A entries (2..8 blocks). Below it the per-block
+# about PIPELINE_BLOCK_NNZ A entries (2..12 blocks). Below it the per-block
 # fixed costs (a count readback each) outweigh the overlap (C2 sweep: grid
 # 512, 1.3M entries, pipelined 2.2 ms vs one-shot ~1.6 ms).
 PIPELINE_MIN_NNZ = 1 << 22
@@ -55,7 +55,7 @@ PIPELINE_BLOCK_NNZ = 1 << 20
 
 
 def pipeline_blocks(nnz_a: int) -> int:
-    return max(2, min(8, nnz_a // PIPELINE_BLOCK_NNZ))
+    return max(2, min(12, nnz_a // PIPELINE_BLOCK_NNZ))
 
 
 @dataclass
