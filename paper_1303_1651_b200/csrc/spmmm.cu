@@ -137,7 +137,7 @@ struct spmmm_context {
   // spmmm_multiply_host: copy streams (uploads, downloads) and their events
   cudaStream_t s_up = nullptr, s_down = nullptr;
   cudaEvent_t pev[5 * kMaxPipeBlocks + 2] = {};
-  DevBuf ci32;                         // narrowed column indices of C blocks
+  DevBuf ci32, rp32;                   // narrowed column indices / row pointers of C blocks
   // split mode: k_esc_warp runs on its own stream beside k_esc_plan/k_esc_block
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1220,11 +1220,14 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   static const bool no_narrow = std::getenv("SPMMM_NO_NARROW") != nullptr;
   static const int widen_threads = std::getenv("SPMMM_WIDEN_THREADS")
                                        ? std::atoi(std::getenv("SPMMM_WIDEN_THREADS")) : 0;
-  const bool narrow = cap >= kNarrowMin && !no_narrow;
+  const bool narrow = cap >= kNarrowMin && cap < (1ull << 32) && !no_narrow;
   void* hci32 = nullptr;
+  void* hrp32 = nullptr;
   if (narrow) {
     CUDA_TRY(ensure(c->ci32, cap * 4, c->stream));
-    rc = host_alloc_internal(cap * 4, &hci32);
+    CUDA_TRY(ensure(c->rp32, (a->rows + 1) * 4, c->stream));
+    rc = host_alloc_internal((a->rows + 1) * 4, &hrp32);
+    if (!rc) rc = host_alloc_internal(cap * 4, &hci32);
     if (rc) {
       free_out();
       return drain(rc);
@@ -1232,7 +1235,11 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   }
   uint32_t* d_ci32 = static_cast<uint32_t*>(c->ci32.p);
   uint32_t* h_ci32 = static_cast<uint32_t*>(hci32);
+  uint32_t* d_rp32 = static_cast<uint32_t*>(c->rp32.p);
+  uint32_t* h_rp32 = static_cast<uint32_t*>(hrp32);
   uint64_t blk_off[kMaxPipeBlocks] = {}, blk_n[kMaxPipeBlocks] = {};
+  uint64_t blk_r0[kMaxPipeBlocks] = {}, blk_r1[kMaxPipeBlocks] = {};
+  bool blk_on[kMaxPipeBlocks] = {};
   std::atomic<int> issued{0};
   std::mutex issue_mu;
   std::condition_variable issue_cv;
@@ -1262,12 +1269,16 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
             });
           }
           if (abort_widen.load(std::memory_order_relaxed)) return;
-          const uint64_t n = blk_n[j];
-          if (!n) continue;
+          if (!blk_on[j]) continue;
           if (cudaEventSynchronize(ev_ci[j]) != cudaSuccess) return;
+          const uint64_t n = blk_n[j];
           const uint64_t i0 = blk_off[j] + n * uint64_t(w) / uint64_t(nthreads);
           const uint64_t i1 = blk_off[j] + n * uint64_t(w + 1) / uint64_t(nthreads);
           widen(h_ci32 + i0, out_ci + i0, i1 - i0);
+          const uint64_t nr = blk_r1[j] - blk_r0[j] + 1;  // row pointers r0..r1
+          const uint64_t q0 = blk_r0[j] + nr * uint64_t(w) / uint64_t(nthreads);
+          const uint64_t q1 = blk_r0[j] + nr * uint64_t(w + 1) / uint64_t(nthreads);
+          widen(h_rp32 + q0, out_rp + q0, q1 - q0);
         }
       });
     }
@@ -1278,7 +1289,8 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     for (auto& t : workers) t.join();
     workers.clear();
     if (hci32) host_free_internal(hci32);
-    hci32 = nullptr;
+    if (hrp32) host_free_internal(hrp32);
+    hci32 = hrp32 = nullptr;
   };
   spmmm_product* prods[kMaxPipeBlocks] = {};
   auto release_all = [&]() {
@@ -1330,27 +1342,47 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
                      256, 0, c->stream>>>(p->rp, r1 - r0 + 1, off);
       CUDA_TRY(cudaGetLastError());
     }
-    CUDA_TRY(cudaEventRecord(ev_comp[j], c->stream));
-    CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
-    CUDA_TRY(cudaMemcpyAsync(out_rp + r0, p->rp, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost,
-                             c->s_down));
-    if (p->nnz && narrow) {
-      k_narrow<<<std::min<unsigned>(unsigned((p->nnz + 255) / 256), unsigned(c->sms) * 8), 256, 0,
-                 c->stream>>>(p->ci, d_ci32 + off, p->nnz);
+    if (narrow) {
+      // row pointers and columns go down as u32 (the reservation is < 2^32
+      // entries), widened by the workers once ev_ci[j] has fired
+      k_narrow<<<std::max(1u, std::min<unsigned>(unsigned((r1 - r0 + 256) / 256),
+                                                  unsigned(c->sms) * 8)),
+                 256, 0, c->stream>>>(p->rp, d_rp32 + r0, r1 - r0 + 1);
       CUDA_TRY(cudaGetLastError());
+      if (p->nnz) {
+        k_narrow<<<std::min<unsigned>(unsigned((p->nnz + 255) / 256), unsigned(c->sms) * 8), 256,
+                   0, c->stream>>>(p->ci, d_ci32 + off, p->nnz);
+        CUDA_TRY(cudaGetLastError());
+      }
       CUDA_TRY(cudaEventRecord(ev_comp[j], c->stream));
       CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
-      CUDA_TRY(cudaMemcpyAsync(h_ci32 + off, d_ci32 + off, p->nnz * 4, cudaMemcpyDeviceToHost,
-                               c->s_down));
+      CUDA_TRY(cudaMemcpyAsync(h_rp32 + r0, d_rp32 + r0, (r1 - r0 + 1) * 4,
+                               cudaMemcpyDeviceToHost, c->s_down));
+      if (p->nnz)
+        CUDA_TRY(cudaMemcpyAsync(h_ci32 + off, d_ci32 + off, p->nnz * 4, cudaMemcpyDeviceToHost,
+                                 c->s_down));
       CUDA_TRY(cudaEventRecord(ev_ci[j], c->s_down));
-      CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
-    } else if (p->nnz) {
-      CUDA_TRY(cudaMemcpyAsync(out_ci + off, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
-      CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->s_down));
+      if (p->nnz)
+        CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost,
+                                 c->s_down));
+    } else {
+      CUDA_TRY(cudaEventRecord(ev_comp[j], c->stream));
+      CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
+      CUDA_TRY(cudaMemcpyAsync(out_rp + r0, p->rp, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost,
+                               c->s_down));
+      if (p->nnz) {
+        CUDA_TRY(cudaMemcpyAsync(out_ci + off, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost,
+                                 c->s_down));
+        CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost,
+                                 c->s_down));
+      }
     }
     CUDA_TRY(cudaEventRecord(ev_down[j], c->s_down));  // (arrays live until the end)
     blk_off[j] = off;
-    blk_n[j] = narrow ? p->nnz : 0;
+    blk_n[j] = p->nnz;
+    blk_r0[j] = r0;
+    blk_r1[j] = r1;
+    blk_on[j] = narrow;
     publish(j + 1);
     off += p->nnz;
     mults += p->mults;
@@ -1414,13 +1446,15 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   CUDA_TRY(cudaStreamSynchronize(c->s_up));
   tr.mark("pipe: downloads done");
   guard.f = nullptr;  // success: the result arrays are the caller's
+  if (hrp32) host_free_internal(hrp32);
+  hrp32 = nullptr;
   release_all();
   out->rows = a->rows;
   out->cols = b->cols;
   out->nnz = off;
   out->mults = mults;
   out->h2d_bytes = rpb + a->nnz * 16 + (same ? 0 : (b->rows + 1) * 8 + b->nnz * 16);
-  out->d2h_bytes = rpb + off * (narrow ? 12 : 16);
+  out->d2h_bytes = (narrow ? rpb / 2 + off * 12 : rpb + off * 16);
   out->row_ptr = out_rp;
   out->col_idx = out_ci;
   out->values = out_v;
@@ -1500,7 +1534,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
                     &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v, &c->parts, &c->part_off, &c->part_nnz,
-                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32})
+                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32, &c->rp32})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
   c->cache.clear();
