@@ -138,6 +138,7 @@ struct spmmm_context {
   cudaStream_t s_up = nullptr, s_down = nullptr;
   cudaEvent_t pev[5 * kMaxPipeBlocks + 2] = {};
   DevBuf ci32, rp32;                   // narrowed column indices / row pointers of C blocks
+  DevBuf d16, dbase;                   // u16 column deltas of C blocks and their chunk bases
   // split mode: k_esc_warp runs on its own stream beside k_esc_plan/k_esc_block
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1009,6 +1010,45 @@ __global__ void k_narrow(const uint64_t* __restrict__ src, uint32_t* __restrict_
     dst[i] = uint32_t(__ldcs(reinterpret_cast<const unsigned long long*>(src) + i));
 }
 
+// Stencil-like results: each 64-entry chunk of C's columns (chunks aligned
+// to the global entry index) spans < 2^16 columns, so the columns go down as
+// u16 deltas from a per-chunk base — half the bytes of u32. A block whose
+// chunks do not all fit clears *ok (mapped host word) and goes down as u32.
+// ci: the block's columns (global entries [off, off + n)); base: per chunk of
+// the block, from chunk off >> 6.
+__global__ void k_delta16(const uint64_t* __restrict__ ci, uint64_t off, uint64_t n,
+                          uint32_t* __restrict__ base, uint16_t* __restrict__ delta,
+                          unsigned int* __restrict__ ok) {
+  const uint64_t c0 = off >> 6, c1 = (off + n + 63) >> 6;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t c = c0 + uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); c < c1;
+       c += nw) {
+    const uint64_t lo = c * 64 > off ? c * 64 : off, hi = (c + 1) * 64 < off + n ? (c + 1) * 64 : off + n;
+    uint32_t v[2];
+    uint32_t mn = 0xffffffffu, mx = 0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t e = lo + lane + 32u * u;
+      v[u] = e < hi ? uint32_t(__ldcs(reinterpret_cast<const unsigned long long*>(ci) + (e - off)))
+                    : 0u;
+      if (e < hi) {
+        mn = v[u] < mn ? v[u] : mn;
+        mx = v[u] > mx ? v[u] : mx;
+      }
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (hi > lo && mx - mn >= 65536u && lane == 0) *reinterpret_cast<volatile unsigned int*>(ok) = 0;
+    if (lane == 0) base[c - c0] = mn;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t e = lo + lane + 32u * u;
+      if (e < hi) delta[e] = uint16_t(v[u] - mn);
+    }
+  }
+}
+
 __global__ void k_zero_u64(uint64_t* p, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
 }
@@ -1053,6 +1093,32 @@ __attribute__((target("avx2"))) void widen_avx2(const uint32_t* in, uint64_t* ou
   }
   for (; i < n; ++i) out[i] = in[i];
   _mm_sfence();
+}
+
+// out[i] = base[(i >> 6) - cb] + delta[i] for global entries i in [i0, i1)
+__attribute__((target("avx2"))) void widen16_avx2(const uint16_t* delta, const uint32_t* base,
+                                                   uint64_t cb, uint64_t* out, uint64_t i0,
+                                                   uint64_t i1) {
+  uint64_t i = i0;
+  for (; i < i1 && (i & 3); ++i) out[i] = uint64_t(base[(i >> 6) - cb]) + delta[i];
+  for (; i + 4 <= i1; i += 4) {  // 4 entries never straddle a 64-entry chunk
+    const __m256i b = _mm256_set1_epi64x(static_cast<long long>(base[(i >> 6) - cb]));
+    const __m128i d = _mm_loadl_epi64(reinterpret_cast<const __m128i*>(delta + i));
+    const __m256i w = _mm256_add_epi64(_mm256_cvtepu16_epi64(d), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + i), w);
+  }
+  for (; i < i1; ++i) out[i] = uint64_t(base[(i >> 6) - cb]) + delta[i];
+  _mm_sfence();
+}
+
+void widen16(const uint16_t* delta, const uint32_t* base, uint64_t cb, uint64_t* out,
+             uint64_t i0, uint64_t i1) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2 && (reinterpret_cast<uintptr_t>(out) & 31) == 0) {
+    widen16_avx2(delta, base, cb, out, i0, i1);
+    return;
+  }
+  for (uint64_t i = i0; i < i1; ++i) out[i] = uint64_t(base[(i >> 6) - cb]) + delta[i];
 }
 
 void widen(const uint32_t* in, uint64_t* out, uint64_t n) {
@@ -1223,10 +1289,17 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   const bool narrow = cap >= kNarrowMin && cap < (1ull << 32) && !no_narrow;
   void* hci32 = nullptr;
   void* hrp32 = nullptr;
+  void* hd16 = nullptr;
+  void* hbase = nullptr;
+  const uint64_t max_chunks = cap / 64 + 2 * uint64_t(G) + 16;
   if (narrow) {
     CUDA_TRY(ensure(c->ci32, cap * 4, c->stream));
     CUDA_TRY(ensure(c->rp32, (a->rows + 1) * 4, c->stream));
+    CUDA_TRY(ensure(c->d16, cap * 2, c->stream));
+    CUDA_TRY(ensure(c->dbase, max_chunks * 4, c->stream));
     rc = host_alloc_internal((a->rows + 1) * 4, &hrp32);
+    if (!rc) rc = host_alloc_internal(cap * 2, &hd16);
+    if (!rc) rc = host_alloc_internal(max_chunks * 4, &hbase);
     if (!rc) rc = host_alloc_internal(cap * 4, &hci32);
     if (rc) {
       free_out();
@@ -1237,9 +1310,16 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   uint32_t* h_ci32 = static_cast<uint32_t*>(hci32);
   uint32_t* d_rp32 = static_cast<uint32_t*>(c->rp32.p);
   uint32_t* h_rp32 = static_cast<uint32_t*>(hrp32);
+  uint16_t* d_d16 = static_cast<uint16_t*>(c->d16.p);
+  uint16_t* h_d16 = static_cast<uint16_t*>(hd16);
+  uint32_t* d_base = static_cast<uint32_t*>(c->dbase.p);
+  uint32_t* h_base = static_cast<uint32_t*>(hbase);
+  static const bool no_delta = std::getenv("SPMMM_NO_DELTA16") != nullptr;
   uint64_t blk_off[kMaxPipeBlocks] = {}, blk_n[kMaxPipeBlocks] = {};
   uint64_t blk_r0[kMaxPipeBlocks] = {}, blk_r1[kMaxPipeBlocks] = {};
-  bool blk_on[kMaxPipeBlocks] = {};
+  uint64_t blk_cb[kMaxPipeBlocks] = {};  // first chunk base of the block (u16 mode)
+  bool blk_on[kMaxPipeBlocks] = {}, blk_16[kMaxPipeBlocks] = {};
+  uint64_t cb_next = 0, d2h = 0;
   std::atomic<int> issued{0};
   std::mutex issue_mu;
   std::condition_variable issue_cv;
@@ -1274,7 +1354,10 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
           const uint64_t n = blk_n[j];
           const uint64_t i0 = blk_off[j] + n * uint64_t(w) / uint64_t(nthreads);
           const uint64_t i1 = blk_off[j] + n * uint64_t(w + 1) / uint64_t(nthreads);
-          widen(h_ci32 + i0, out_ci + i0, i1 - i0);
+          if (blk_16[j])
+            widen16(h_d16, h_base + blk_cb[j], blk_off[j] >> 6, out_ci, i0, i1);
+          else
+            widen(h_ci32 + i0, out_ci + i0, i1 - i0);
           const uint64_t nr = blk_r1[j] - blk_r0[j] + 1;  // row pointers r0..r1
           const uint64_t q0 = blk_r0[j] + nr * uint64_t(w) / uint64_t(nthreads);
           const uint64_t q1 = blk_r0[j] + nr * uint64_t(w + 1) / uint64_t(nthreads);
@@ -1290,7 +1373,9 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     workers.clear();
     if (hci32) host_free_internal(hci32);
     if (hrp32) host_free_internal(hrp32);
-    hci32 = hrp32 = nullptr;
+    if (hd16) host_free_internal(hd16);
+    if (hbase) host_free_internal(hbase);
+    hci32 = hrp32 = hd16 = hbase = nullptr;
   };
   spmmm_product* prods[kMaxPipeBlocks] = {};
   auto release_all = [&]() {
@@ -1349,7 +1434,22 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
                                                   unsigned(c->sms) * 8)),
                  256, 0, c->stream>>>(p->rp, d_rp32 + r0, r1 - r0 + 1);
       CUDA_TRY(cudaGetLastError());
-      if (p->nnz) {
+      const uint64_t nch = p->nnz ? ((off + p->nnz + 63) >> 6) - (off >> 6) : 0;
+      bool use16 = false;
+      if (p->nnz && !no_delta) {
+        // u16 deltas if every 64-entry chunk spans < 2^16 columns (stencils)
+        volatile unsigned long long* okw = c->h_aux + kMaxPipeBlocks + j;
+        *okw = 1;
+        k_delta16<<<std::max(1u, std::min<unsigned>(unsigned((nch + 7) / 8),
+                                                     unsigned(c->sms) * 8)),
+                    256, 0, c->stream>>>(p->ci, off, p->nnz, d_base + cb_next, d_d16,
+                                         reinterpret_cast<unsigned int*>(
+                                             const_cast<unsigned long long*>(okw)));
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        use16 = (*okw & 0xffffffffull) != 0;
+      }
+      if (p->nnz && !use16) {
         k_narrow<<<std::min<unsigned>(unsigned((p->nnz + 255) / 256), unsigned(c->sms) * 8), 256,
                    0, c->stream>>>(p->ci, d_ci32 + off, p->nnz);
         CUDA_TRY(cudaGetLastError());
@@ -1358,9 +1458,21 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
       CUDA_TRY(cudaStreamWaitEvent(c->s_down, ev_comp[j], 0));
       CUDA_TRY(cudaMemcpyAsync(h_rp32 + r0, d_rp32 + r0, (r1 - r0 + 1) * 4,
                                cudaMemcpyDeviceToHost, c->s_down));
-      if (p->nnz)
+      d2h += (r1 - r0 + 1) * 4 + p->nnz * 8;
+      if (use16) {
+        CUDA_TRY(cudaMemcpyAsync(h_base + cb_next, d_base + cb_next, nch * 4,
+                                 cudaMemcpyDeviceToHost, c->s_down));
+        CUDA_TRY(cudaMemcpyAsync(h_d16 + off, d_d16 + off, p->nnz * 2, cudaMemcpyDeviceToHost,
+                                 c->s_down));
+        d2h += nch * 4 + p->nnz * 2;
+      } else if (p->nnz) {
         CUDA_TRY(cudaMemcpyAsync(h_ci32 + off, d_ci32 + off, p->nnz * 4, cudaMemcpyDeviceToHost,
                                  c->s_down));
+        d2h += p->nnz * 4;
+      }
+      blk_16[j] = use16;
+      blk_cb[j] = cb_next;
+      if (use16) cb_next += nch;
       CUDA_TRY(cudaEventRecord(ev_ci[j], c->s_down));
       if (p->nnz)
         CUDA_TRY(cudaMemcpyAsync(out_v + off, p->v, p->nnz * 8, cudaMemcpyDeviceToHost,
@@ -1446,15 +1558,15 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   CUDA_TRY(cudaStreamSynchronize(c->s_up));
   tr.mark("pipe: downloads done");
   guard.f = nullptr;  // success: the result arrays are the caller's
-  if (hrp32) host_free_internal(hrp32);
-  hrp32 = nullptr;
+  for (void* hp : {hrp32, hd16, hbase}) host_free_internal(hp);
+  hrp32 = hd16 = hbase = nullptr;
   release_all();
   out->rows = a->rows;
   out->cols = b->cols;
   out->nnz = off;
   out->mults = mults;
   out->h2d_bytes = rpb + a->nnz * 16 + (same ? 0 : (b->rows + 1) * 8 + b->nnz * 16);
-  out->d2h_bytes = (narrow ? rpb / 2 + off * 12 : rpb + off * 16);
+  out->d2h_bytes = narrow ? d2h : rpb + off * 16;
   out->row_ptr = out_rp;
   out->col_idx = out_ci;
   out->values = out_v;
@@ -1534,7 +1646,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
                     &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v, &c->parts, &c->part_off, &c->part_nnz,
-                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32, &c->rp32})
+                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32, &c->rp32, &c->d16, &c->dbase})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
   c->cache.clear();
