@@ -109,8 +109,10 @@ int spmmm_product_download(spmmm_product* p, uint64_t* row_ptr, uint64_t* col_id
 
 /* Result of spmmm_multiply_host: C in page-locked host memory from the
  * library's pool (return each array with spmmm_host_free). col_idx / values
- * hold `nnz` entries (their blocks may be larger). Column indices travel
- * down as u32 for large results and are widened by host threads. */
+ * hold `nnz` entries (their blocks may be larger). For large results row
+ * pointers travel down as u32 and column indices as u32 or, when every
+ * 64-entry chunk spans < 2^16 columns, as u16 deltas; host threads widen them
+ * into the u64 arrays. h2d_bytes / d2h_bytes count what crossed PCIe. */
 typedef struct {
   uint64_t rows, cols, nnz, mults;
   uint64_t* row_ptr;
