@@ -151,6 +151,29 @@ int spmmm_estimate_nnz(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* 
 int spmmm_row_products_prefix(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b,
                               uint64_t* out);
 
+/* Multi-GPU row blocks (rows of C are independent,
+ * kernels.py:323-329). The product-balanced partition of A's rows into
+ * `parts` (<= 64) blocks, computed on the device: bounds[g] =
+ * lower_bound(P, g·T/parts) over the exclusive prefix P of per-row product
+ * counts (perfmodel.py:63-76 per row), bounds[0] = 0, bounds[parts] = rows;
+ * *total = T. Same result as distributed.partition_rows on the host prefix.
+ * Every rank holding A and B computes the same bounds, so no collective is
+ * needed to agree on them. */
+int spmmm_partition_rows(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b, int parts,
+                         uint64_t* bounds, uint64_t* total);
+/* spmmm_product_download with every row pointer shifted by `offset` (the nnz
+ * of the row blocks before this one): a block lands in its slice of one
+ * result, row_ptr at rp + r0, columns and values at ci/v + offset. The
+ * destination may be any host memory; registered (pinned) memory goes at
+ * DMA speed. */
+int spmmm_product_download_offset(spmmm_product* p, uint64_t offset, uint64_t* row_ptr,
+                                  uint64_t* col_idx, double* values);
+/* Page-lock caller memory (e.g. a shared-memory result every rank of a
+ * node maps) so downloads into it run at PCIe speed; cudaHostRegister /
+ * cudaHostUnregister with the portable flag. */
+int spmmm_host_register(void* ptr, uint64_t bytes);
+int spmmm_host_unregister(void* ptr);
+
 /* Storage-order conversion: the product holds the CSR of M^T for the CSR view
  * M, i.e. the arrays of csr_to_csc(M) (formats.py:302-329); a CSC matrix
  * passed as the CSR view of its transpose yields csc_to_csr (formats.py:332-357).

@@ -212,3 +212,105 @@ def multiply_colmajor(a_csc, b_csc, *, row_choices: bool = False) -> OracleResul
     bt = _Csr(b_csc.cols, b_csc.rows, b_csc.col_ptr, b_csc.row_idx, b_csc.values)
     at = _Csr(a_csc.cols, a_csc.rows, a_csc.col_ptr, a_csc.row_idx, a_csc.values)
     return multiply_rowmajor(bt, at, row_choices=row_choices)
+
+
+# ---------------------------------------------------------------------------
+# Operand generators (gen_oracle.c): the reference arm of bench.py builds its
+# operands here, so it never maps the product library.
+
+# BASELINE.json configs (labels and wording as SURVEY.md §8(d))
+CONFIGS = {
+    "C1": dict(family="fd", grid=100, desc="2D 5-pt Laplacian 100x100, C = A*A"),
+    "C2": dict(family="fd", grid=2048,
+               desc="2D 5-pt Laplacian sweep 32..2048 (grid {grid}x{grid}), C = A*A"),
+    "C3": dict(family="random", n=2_000_000, k=5, seeds=(0, 1),
+               desc="random 5 per row, N=2M, C = A*B"),
+    "C4": dict(family="fd3", grid=100, desc="3D 27-pt stencil 100^3, C = A*A"),
+    "C5": dict(family="zipf", n=2_000_000, seeds=(0, 1),
+               desc="Zipf(2) rows clipped to [1,4096], N=2M, C = A*B"),
+}
+
+
+def _gen_lib():
+    lib = _load()
+    if not getattr(lib, "_gen_declared", False):
+        vp = ctypes.c_void_p
+        u64 = ctypes.c_uint64
+        lib.oracle_splitmix64.argtypes = [u64, u64, vp]
+        lib.oracle_gen_fd_size.argtypes = [u64, _u64p, _u64p]
+        lib.oracle_gen_fd.argtypes = [u64, vp, vp, vp]
+        lib.oracle_gen_fd3_size.argtypes = [u64, _u64p, _u64p]
+        lib.oracle_gen_fd3.argtypes = [u64, vp, vp, vp]
+        lib.oracle_gen_random_k.argtypes = [u64, u64, u64, vp, vp, vp]
+        lib.oracle_gen_zipf.argtypes = [u64, u64, u64, _u64p, vp, vp, vp]
+        for f in (lib.oracle_splitmix64, lib.oracle_gen_fd, lib.oracle_gen_fd3,
+                  lib.oracle_gen_random_k, lib.oracle_gen_zipf):
+            f.restype = ctypes.c_int
+        lib._gen_declared = True
+    return lib
+
+
+def splitmix64(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.uint64)
+    _gen_lib().oracle_splitmix64(seed & (2**64 - 1), n, out.ctypes.data)
+    return out
+
+
+def _stencil(size_fn, fill_fn, grid):
+    rows, nnz = ctypes.c_uint64(), ctypes.c_uint64()
+    size_fn(grid, ctypes.byref(rows), ctypes.byref(nnz))
+    rp = np.empty(rows.value + 1, np.uint64)
+    ci = np.empty(nnz.value, np.uint64)
+    v = np.empty(nnz.value, np.float64)
+    fill_fn(grid, rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+    return _Csr(rows.value, rows.value, rp, ci, v)
+
+
+def gen_fd(grid: int):
+    lib = _gen_lib()
+    return _stencil(lib.oracle_gen_fd_size, lib.oracle_gen_fd, grid)
+
+
+def gen_fd3(grid: int):
+    lib = _gen_lib()
+    return _stencil(lib.oracle_gen_fd3_size, lib.oracle_gen_fd3, grid)
+
+
+def gen_random_k(n: int, k: int, seed: int):
+    rp = np.empty(n + 1, np.uint64)
+    ci = np.empty(n * k, np.uint64)
+    v = np.empty(n * k, np.float64)
+    if _gen_lib().oracle_gen_random_k(n, k, seed, rp.ctypes.data, ci.ctypes.data, v.ctypes.data):
+        raise ValueError("need 1 <= k <= n")
+    return _Csr(n, n, rp, ci, v)
+
+
+def gen_zipf(n: int, seed: int, lmax: int = 4096):
+    lib = _gen_lib()
+    nnz = ctypes.c_uint64()
+    lib.oracle_gen_zipf(n, lmax, seed, ctypes.byref(nnz), None, None, None)
+    rp = np.empty(n + 1, np.uint64)
+    ci = np.empty(nnz.value, np.uint64)
+    v = np.empty(nnz.value, np.float64)
+    lib.oracle_gen_zipf(n, lmax, seed, ctypes.byref(nnz), rp.ctypes.data, ci.ctypes.data,
+                        v.ctypes.data)
+    return _Csr(n, n, rp, ci, v)
+
+
+def config_operands(label: str, grid: int | None = None):
+    """(a, b, desc) of a BASELINE config; b is a for the A*A configs."""
+    cfg = dict(CONFIGS[label])
+    if grid:
+        cfg["grid"] = grid
+    fam = cfg["family"]
+    desc = cfg["desc"].format(**cfg)
+    if fam == "fd":
+        a = gen_fd(cfg["grid"])
+        return a, a, desc
+    if fam == "fd3":
+        a = gen_fd3(cfg["grid"])
+        return a, a, desc
+    s0, s1 = cfg["seeds"]
+    if fam == "random":
+        return gen_random_k(cfg["n"], cfg["k"], s0), gen_random_k(cfg["n"], cfg["k"], s1), desc
+    return gen_zipf(cfg["n"], s0), gen_zipf(cfg["n"], s1), desc

@@ -40,7 +40,8 @@ EXPORTS = (
     "spmmm_multiply", "spmmm_multiply_host", "spmmm_product_shape", "spmmm_product_device_arrays",
     "spmmm_product_download", "spmmm_product_copy_device", "spmmm_product_row_stats",
     "spmmm_product_destroy", "spmmm_estimate_nnz", "spmmm_row_products_prefix",
-    "spmmm_transpose",
+    "spmmm_transpose", "spmmm_partition_rows", "spmmm_product_download_offset",
+    "spmmm_host_register", "spmmm_host_unregister",
     "spmmm_last_timings", "spmmm_last_launch_count",
     "spmmm_host_alloc", "spmmm_host_free", "spmmm_host_pool_bytes",
     "spmmm_splitmix64", "spmmm_gen_fd_size", "spmmm_gen_fd", "spmmm_gen_fd3_size",
@@ -118,6 +119,11 @@ def _declare(lib):
         "spmmm_row_products_prefix": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr),
                                           vp]),
         "spmmm_transpose": (i, [vp, ctypes.POINTER(SpmmmCsr), pp]),
+        "spmmm_partition_rows": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr), i,
+                                     vp, p_u64]),
+        "spmmm_product_download_offset": (i, [vp, c_u64, vp, vp, vp]),
+        "spmmm_host_register": (i, [vp, c_u64]),
+        "spmmm_host_unregister": (i, [vp]),
         "spmmm_last_timings": (i, [vp, ctypes.POINTER(ctypes.c_char_p),
                                    ctypes.POINTER(ctypes.c_double), i, ctypes.POINTER(i)]),
         "spmmm_last_launch_count": (i, [vp, ctypes.POINTER(i)]),
@@ -288,6 +294,13 @@ class Product:
                                                 ctypes.byref(v)), "device arrays")
         return rp.value, ci.value, v.value
 
+    def download_offset(self, offset: int, rp_addr, ci_addr, v_addr):
+        """Into caller memory at raw addresses, row pointers shifted by
+        `offset` (spmmm_product_download_offset)."""
+        check(lib().spmmm_product_download_offset(self._h, int(offset), rp_addr,
+                                                  ci_addr if self.nnz else None,
+                                                  v_addr if self.nnz else None), "download")
+
     def copy_device(self, rp_addr, ci_addr, v_addr):
         check(lib().spmmm_product_copy_device(self._h, rp_addr, ci_addr, v_addr), "copy")
 
@@ -355,6 +368,25 @@ def multiply_host(ctx: Context, a: SpmmmCsr, b: SpmmmCsr, strategy_id: int, flag
 
 # PCIe bytes of the last multiply_host call (bench.py's e2e accounting)
 last_transfer = None
+
+
+def partition_rows(ctx: Context, a: SpmmmCsr, b: SpmmmCsr, parts: int):
+    """Product-balanced row bounds (parts+1) and the product total, computed on
+    the device (spmmm_partition_rows)."""
+    bounds = np.zeros(int(parts) + 1, np.uint64)
+    total = ctypes.c_uint64()
+    check(lib().spmmm_partition_rows(ctx.handle, ctypes.byref(a), ctypes.byref(b), int(parts),
+                                     bounds.ctypes.data, ctypes.byref(total)),
+          "spmmm_partition_rows")
+    return bounds.astype(np.int64), int(total.value)
+
+
+def host_register(addr: int, nbytes: int) -> None:
+    check(lib().spmmm_host_register(ctypes.c_void_p(int(addr)), int(nbytes)), "spmmm_host_register")
+
+
+def host_unregister(addr: int) -> None:
+    check(lib().spmmm_host_unregister(ctypes.c_void_p(int(addr))), "spmmm_host_unregister")
 
 
 def transpose_view(ctx: Context, m: SpmmmCsr) -> Product:

@@ -30,6 +30,7 @@
 #include "../../include/spmmm.h"
 #include "aux_kernels.cuh"
 #include "convert.cuh"
+#include "dist_kernels.cuh"
 #include "esc.cuh"
 #include "fused_launch.cuh"
 
@@ -144,6 +145,10 @@ struct spmmm_context {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf aux;                          // per-block max columns
   unsigned long long* h_aux = nullptr; // pinned mirror
+  // multi-GPU: partition scratch (chunk sums), its pinned result words, and
+  // the shifted row pointers of a download at an offset
+  DevBuf part_sums, dl_rp;
+  unsigned long long* h_part = nullptr;
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -1646,7 +1651,8 @@ int spmmm_context_destroy(spmmm_context* c) {
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
                     &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v, &c->parts, &c->part_off, &c->part_nnz,
-                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32, &c->rp32, &c->d16, &c->dbase})
+                    &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32, &c->rp32, &c->d16, &c->dbase,
+                    &c->part_sums, &c->dl_rp})
     release(*b, c->stream);
   for (auto& cb : c->cache) cudaFreeAsync(cb.first, c->stream);
   c->cache.clear();
@@ -1662,6 +1668,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->s_down) cudaStreamDestroy(c->s_down);
   if (c->h_aux) cudaFreeHost(c->h_aux);
+  if (c->h_part) cudaFreeHost(c->h_part);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1886,6 +1893,99 @@ int spmmm_row_products_prefix(spmmm_context* c, const spmmm_csr* a, const spmmm_
   }
   out[0] = 0;
   for (uint64_t r = 0; r < A.rows; ++r) out[r + 1] = out[r] + h[r];
+  return SPMMM_OK;
+}
+
+int spmmm_partition_rows(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int parts,
+                         uint64_t* bounds, uint64_t* total) {
+  if (!c || !bounds) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  if (parts < 1 || parts > kPartMaxParts)
+    return fail(SPMMM_ERR_INVALID, "parts=%d outside [1, %d]", parts, kPartMaxParts);
+  std::lock_guard<std::mutex> lock(c->mu);
+  int rc = check_view(a, "a");
+  if (!rc) rc = check_view(b, "b");
+  if (rc) return rc;
+  if (a->cols != b->rows)
+    return fail(SPMMM_ERR_DIMENSION, "dimension mismatch: %llu (cols of a) != %llu (rows of b)",
+                (unsigned long long)a->cols, (unsigned long long)b->rows);
+  if (a->rows >= 0xffffffffull)
+    return fail(SPMMM_ERR_UNSUPPORTED, "a.rows=%llu exceeds the 32-bit row range",
+                (unsigned long long)a->rows);
+  CUDA_TRY(cudaSetDevice(c->device));
+  DevCsr A, B;
+  rc = resolve(c, a, b, &A, &B);
+  if (rc) return rc;
+  Timer tm{c, false};
+  c->last_launches = 0;
+  rc = run_count(c, A, B, tm);  // validates A and B, per-row products in c->prod
+  if (rc) return rc;
+  if (!c->h_part) CUDA_TRY(cudaMallocHost(&c->h_part, (kPartMaxParts + 2) * 8));
+  const uint64_t rows = A.rows;
+  if (rows == 0) {
+    for (int g = 0; g <= parts; ++g) bounds[g] = 0;
+    if (total) *total = 0;
+    return SPMMM_OK;
+  }
+  uint64_t L = kPartChunkRows;
+  while ((rows + L - 1) / L > uint64_t(kPartMaxChunks)) L *= 2;
+  const uint32_t nchunks = uint32_t((rows + L - 1) / L);
+  CUDA_TRY(ensure(c->part_sums, nchunks * 8, c->stream));
+  auto* sums = static_cast<unsigned long long*>(c->part_sums.p);
+  k_part_chunk_sums<<<nchunks, 256, 0, c->stream>>>(static_cast<const uint32_t*>(c->prod.p), rows,
+                                                     uint32_t(L), sums);
+  CUDA_TRY(cudaGetLastError());
+  k_partition<<<1, 1024, 0, c->stream>>>(static_cast<const uint32_t*>(c->prod.p), rows,
+                                         uint32_t(L), sums, nchunks, parts, c->h_part);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->last_launches += 2;
+  uint64_t prev = 0;
+  for (int g = 0; g <= parts; ++g) {
+    uint64_t v = std::min<uint64_t>(c->h_part[g], rows);
+    prev = std::max(prev, v);
+    bounds[g] = prev;
+  }
+  bounds[0] = 0;
+  bounds[parts] = rows;
+  if (total) *total = c->h_part[parts + 1];
+  return SPMMM_OK;
+}
+
+int spmmm_product_download_offset(spmmm_product* p, uint64_t offset, uint64_t* rp, uint64_t* ci,
+                                  double* v) {
+  if (!p) return fail(SPMMM_ERR_INVALID, "product is NULL");
+  spmmm_context* c = p->ctx;
+  std::lock_guard<std::mutex> lock(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (rp) {
+    const uint64_t n = p->rows + 1;
+    const uint64_t* src = p->rp;
+    if (offset) {
+      CUDA_TRY(ensure(c->dl_rp, n * 8, c->stream));
+      k_copy_offset<<<unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(c->sms) * 8)), 256, 0,
+                      c->stream>>>(p->rp, static_cast<uint64_t*>(c->dl_rp.p), n, offset);
+      CUDA_TRY(cudaGetLastError());
+      src = static_cast<const uint64_t*>(c->dl_rp.p);
+    }
+    CUDA_TRY(cudaMemcpyAsync(rp, src, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (p->nnz) {
+    if (ci) CUDA_TRY(cudaMemcpyAsync(ci, p->ci, p->nnz * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (v) CUDA_TRY(cudaMemcpyAsync(v, p->v, p->nnz * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SPMMM_OK;
+}
+
+int spmmm_host_register(void* ptr, uint64_t bytes) {
+  if (!ptr || !bytes) return fail(SPMMM_ERR_INVALID, "NULL or empty range");
+  CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return SPMMM_OK;
+}
+
+int spmmm_host_unregister(void* ptr) {
+  if (!ptr) return fail(SPMMM_ERR_INVALID, "ptr is NULL");
+  CUDA_TRY(cudaHostUnregister(ptr));
   return SPMMM_OK;
 }
 

@@ -89,24 +89,31 @@ def _choice_enum(strategy):
     return StrategyKind
 
 
-def _record_row_choices(stats, product: _lib.Product, enum_cls, a_row_ptr) -> None:
-    if product.cols == 0:
+def choices_from_row_stats(row_stats, cols: int, a_row_ptr, row0: int = 0):
+    """[(row + row0, is_minmax)] for every row that touched a column: the
+    reference's combined_select(max - min + 1, len(touched)) per row
+    (kernels.py:186-191, 255-258), from the GPU's per-row stats."""
+    if cols == 0:
         # With zero result columns the accumulator's sentinels coincide
         # (min_idx = length = 0 = max_idx, kernels.py:82-83), so the reference
         # records combined_select(1, 0) = SORT for every non-empty A row
         # (kernels.py:255-258) although nothing was touched.
-        rows = np.nonzero(np.diff(a_row_ptr.astype(np.int64)))[0]
-        stats.row_choices.extend((int(r), enum_cls.SORT) for r in rows.tolist())
-        return
-    mn, mx, touched = product.row_stats()
+        rows = np.nonzero(np.diff(np.asarray(a_row_ptr).astype(np.int64)))[0]
+        return [(int(r) + row0, False) for r in rows.tolist()]
+    mn, mx, touched = row_stats
     rows = np.nonzero(touched)[0]
     if rows.size == 0:
-        return
+        return []
     span = (mx[rows] - mn[rows] + np.uint64(1)).astype(np.uint64)
     use_minmax = span < np.uint64(2) * touched[rows]
+    return list(zip((rows + row0).tolist(), use_minmax.tolist()))
+
+
+def _record_row_choices(stats, product: _lib.Product, enum_cls, a_row_ptr) -> None:
+    row_stats = product.row_stats() if product.cols else None
     mm, so = enum_cls.MIN_MAX, enum_cls.SORT
     stats.row_choices.extend(
-        (int(r), mm if m else so) for r, m in zip(rows.tolist(), use_minmax.tolist()))
+        (r, mm if m else so) for r, m in choices_from_row_stats(row_stats, product.cols, a_row_ptr))
 
 
 def multiply_rowmajor(a, b, strategy=StrategyKind.COMBINED, stats=None):

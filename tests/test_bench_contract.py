@@ -35,6 +35,10 @@ def test_reference_arm_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["config"]["workload"].startswith("C1")
+    # the reference arm never maps the product library (its operands come
+    # from oracle/gen_oracle.c)
+    assert not any("libspmmm" in p for p in d["native_libs_mapped"]), d["native_libs_mapped"]
+    assert "oracle/liboracle.so" in d["native_libs_mapped"]
 
 
 @pytest.mark.gpu
@@ -52,3 +56,22 @@ def test_our_arm_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     cb = d["cpu_baseline"]
     assert cb["cores"] == 1 and cb["value"] > 0 and cb["kind"] == "port"
+    assert d["e2e_pageable"]["value"] > 0
+    assert "paper_1303_1651_b200/libspmmm.so" in d["native_libs_mapped"]
+    # both arms print the same config for the same workload
+    ref = _run(["--impl", "reference", "--config", "C1", "--steps", "2", "--warmup", "3"])
+    assert ref["config"] == d["config"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not have_gpu(), reason="needs a CUDA device")
+def test_multi_rank_line_functional():
+    """`--gpus 2` launches two ranks itself (torch.distributed.run). With one
+    GPU the ranks share it over gloo: a functional run of the N>1 path."""
+    d = _run(["--gpus", "2", "--backend", "gloo", "--config", "C3", "--steps", "3",
+              "--warmup", "3", "--e2e-steps", "2"], timeout=900)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "strong"
+    assert len(d["rank_products"]) == 2 and sum(d["rank_products"]) == d["config"]["products"]
+    assert d["balance"] < 1.01
+    assert d["e2e"]["value"] > 0 and d["gather_ms"] > 0 and d["b_allgather_ms"] > 0
+    assert d["gpu_launches"] >= 2 * 2 * d["steps"]

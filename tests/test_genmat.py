@@ -99,3 +99,40 @@ def test_config_operands_c5_fingerprint():
     a, b, _ = genmat.config_operands("C5")
     assert genmat.digests(a)["fingerprint"] == fp["a"]["fingerprint"]
     assert genmat.digests(b)["fingerprint"] == fp["b"]["fingerprint"]
+
+
+# --- the oracle's generators (gen_oracle.c), used by bench.py's reference arm
+
+
+def test_oracle_splitmix64_matches_reference():
+    import oracle
+
+    for seed in (0, 1, 0xA5A5A5A5, 2**64 - 1):
+        assert np.array_equal(oracle.splitmix64(seed, 64), golden_splitmix(seed))
+
+
+@pytest.mark.parametrize("label", ["C1", "C3", "C4", "C5"])
+def test_oracle_config_operands_match_reference_fingerprints(label):
+    """The reference arm's operands are the reference's own (C1, C3) and the
+    same bytes as the product's generators (C4, C5; fingerprints the
+    reference computed over them)."""
+    import oracle
+
+    key = {"C1": "C1_fd100", "C3": "C3_random2M", "C4": "C4_fd3_100", "C5": "C5_zipf2M"}[label]
+    fp = fingerprints().get(key)
+    if fp is None:
+        pytest.skip("fingerprint missing")
+    a, b, _ = oracle.config_operands(label)
+    assert genmat.digests(a)["fingerprint"] == fp["a"]["fingerprint"]
+    assert genmat.digests(b)["fingerprint"] == fp["b"]["fingerprint"]
+
+
+def test_oracle_c2_sweep_operand_matches_reference():
+    import oracle
+
+    for g in (32, 512):
+        fp = fingerprints().get(f"C2_fd{g}")
+        if fp is None:
+            pytest.skip("fingerprint missing")
+        a, b, _ = oracle.config_operands("C2", grid=g)
+        assert b is a and genmat.digests(a)["fingerprint"] == fp["a"]["fingerprint"]

@@ -31,6 +31,7 @@ def full(rep, config, kernel, tag):
         except (KeyError, ValueError):
             return None
 
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     u = dict(zip(hdr, units))
     rd = num("dram__bytes_read.sum") * scale.get(u.get("dram__bytes_read.sum"), 1)
@@ -52,7 +53,8 @@ def full(rep, config, kernel, tag):
         "configs": {}}
     d["configs"].setdefault(config, {})[kernel] = {
         "dram_bytes": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
-        "duration_ms": num("gpu__time_duration.sum"), "report": name + ".txt"}
+        "duration_ms": num("gpu__time_duration.sum") * tscale.get(u.get("gpu__time_duration.sum"), 1.0),
+        "report": name + ".txt"}
     json.dump(d, open(tpath, "w"), indent=1)
     print(f"wrote {name}.txt and {tag}_traffic.json ({(rd + wr) / 1e9:.3f} GB)")
 
