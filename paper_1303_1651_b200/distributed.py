@@ -304,7 +304,8 @@ def _to_tensor(arr: np.ndarray) -> torch.Tensor:
         return torch.from_numpy(a)
 
 
-def _replicate(arr: np.ndarray, rank: int, world: int, device, group, nccl: bool) -> torch.Tensor:
+def _replicate(arr: np.ndarray, rank: int, world: int, device, group,
+               nccl: bool) -> torch.Tensor:
     """All of `arr` on this rank's device; this rank uploads only its chunk.
     Returns a tensor of arr.size elements (a prefix of the padded buffer)."""
     n = int(arr.size)
@@ -320,7 +321,11 @@ def _replicate(arr: np.ndarray, rank: int, world: int, device, group, nccl: bool
         # in place: this rank's chunk is already in its slot
         dist.all_gather_into_tensor(buf, mine, group=group)
         return buf[:n]
-    # gloo: gather on the host, then one copy to the device
+    if device.type == "cuda":
+        # gloo (ranks sharing a GPU: a functional run): no NVLink to all-gather
+        # over; every rank reads the whole node-wide shared operand itself
+        return src.to(device, non_blocking=True)
+    # gloo on CPU (tests): gather the chunks on the host
     mine = torch.zeros(chunk, dtype=dtype)
     if hi > lo:
         mine[:hi - lo].copy_(src[lo:hi])
@@ -359,9 +364,11 @@ def replicate_csr(m, group=None, device=None) -> ResidentCsr:
 
 
 def _device(group, device):
+    """This rank's device: the given one, else the current CUDA device (there
+    is no CPU product: only the tests inject one, with device="cpu")."""
     if device is not None:
         return torch.device(device)
-    if dist.get_backend(group) == "nccl":
+    if dist.get_backend(group) == "nccl" or torch.cuda.is_available():
         return torch.device("cuda", torch.cuda.current_device())
     return torch.device("cpu")
 
@@ -405,6 +412,8 @@ def _context(device):
 def _view(m: ResidentCsr, r0=None, r1=None):
     from . import _lib
 
+    if m.values.device.type != "cuda":
+        raise RuntimeError("libspmmm needs device-resident operands (there is no CPU product)")
     rp = m.row_ptr if r0 is None else m.row_ptr[r0:r1 + 1]
     rows = m.rows if r0 is None else r1 - r0
     return _lib.device_view(rows, m.cols, m.nnz, rp.data_ptr(), m.col_idx.data_ptr(),
