@@ -35,6 +35,7 @@ enum Ctrl : int {
   kCtrlParts = 23,      // column-range parts written by k_esc_plan
   kCtrlPlanTicket = 24, // k_esc_plan's dynamic row counter
   kCtrlScrCursor = 25,  // k_esc_plan's scratch allocator (slots)
+  kCtrlCfFlags = 26,    // count-free path: kCf* bits, then [27] longest A row, [28] longest B row
   kCtrlWords = 32
 };
 
@@ -264,6 +265,75 @@ __host__ __device__ inline bool ell_wanted(const unsigned long long* w, uint64_t
   // worth it when the referenced B rows (>= total / longest) are not much
   // fewer than the rows the copy spans
   return 10 * (total / (bmax ? bmax : 1)) >= 7 * (k1 - k0);
+}
+
+// ---------------------------------------------------------------------------
+// The count-free path. When every row of C is short by construction — A
+// rows of <= kEllEntries entries and B rows of <= kEllSlots (the ELL flavour:
+// B read through its ELL records), or A rows of na entries and B rows of nb
+// with na <= 32 and na·nb <= 32 (the CSR flavour, e.g. a row block of A
+// against a whole B) — the fused kernel needs neither the per-row product
+// counts nor the host decisions k_count feeds. This pass only measures the
+// longest A and B rows, checks both row_ptr arrays, packs B's ELL records
+// (ELL flavour) and zeroes the look-back counters; k_fused follows it on the
+// stream with no host round trip, checks the verdict itself (cf_applies) and
+// returns at once when it does not apply. The host then runs the counted
+// path, which also yields the reference's exact error for bad input.
+// (CfFlags and cf_applies: rows.cuh, beside the ELL layout)
+
+__global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
+                                              unsigned long long* __restrict__ ctrl,
+                                              unsigned long long* __restrict__ zero,
+                                              uint64_t nzero, uint4* __restrict__ ell) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t t0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (uint64_t i = t0; i < nzero; i += stride) zero[i] = 0;
+  unsigned f = 0;
+  unsigned long long ma = 0, mb = 0;
+  // C = A·A (A square, its rows are B's rows): one pass over the rows
+  // measures both and checks A's columns while packing them as B's records
+  const bool same = A.rp == B.rp && A.ci == B.ci && A.rows == B.rows && A.nnz == B.nnz;
+  if (!same) {
+    for (uint64_t r = t0; r < A.rows; r += stride) {
+      const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
+      if (hi < lo || hi > A.nnz) f |= kCfBadA;
+      else ma = hi - lo > ma ? hi - lo : ma;
+    }
+    // every column of A's rows must name a row of B (k_fused trusts them);
+    // coalesced over the entries of the rows' span
+    uint64_t e0 = ld_idx(A.rp), e1 = ld_idx(A.rp + A.rows);
+    e1 = e1 < A.nnz ? e1 : A.nnz;
+    for (uint64_t e = e0 + t0; e < e1; e += stride)
+      if (ld_idx(A.ci + e) >= B.rows) f |= kCfBadCol;
+  }
+  for (uint64_t r = t0; r < B.rows; r += stride) {
+    const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+    if (hi < lo || hi > B.nnz) {
+      f |= kCfBadB;
+      continue;
+    }
+    mb = hi - lo > mb ? hi - lo : mb;
+    if (same)
+      for (uint64_t e = lo; e < hi; ++e)
+        if (ld_idx(B.ci + e) >= B.rows) f |= kCfBadCol;  // (L1 hits: the record's loads)
+    if (ell) pack_ell_record(B, r, lo, hi, ell);  // (longer rows: truncated, never read)
+  }
+  if (same) {
+    ma = mb;
+    f |= (f & kCfBadB) ? kCfBadA : 0u;
+  }
+  f = __reduce_or_sync(kFull, f);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long oa = __shfl_xor_sync(kFull, ma, d), ob = __shfl_xor_sync(kFull, mb, d);
+    ma = oa > ma ? oa : ma;
+    mb = ob > mb ? ob : mb;
+  }
+  if (lane_id() == 0) {
+    if (f) atomicOr(ctrl + kCtrlCfFlags, (unsigned long long)f);
+    if (ma) atomicMax(ctrl + kCtrlCfFlags + 1, ma);
+    if (mb) atomicMax(ctrl + kCtrlCfFlags + 2, mb);
+  }
 }
 
 // Only the rows A references ([kmin, kmax], from k_count) are packed; rows in

@@ -46,6 +46,13 @@ struct FusedParams {
   uint32_t* st_min;
   uint32_t* st_max;
   uint32_t* st_touch;
+  // count-free path (k_prep instead of k_count; short variant only): prod is
+  // null, every row with entries is short, k_prep's verdict is read here and
+  // the multiplications are summed into *cf_total
+  const unsigned long long* cf_flags;
+  unsigned long long* cf_total;
+  unsigned long long* cf_err;
+  uint64_t c_cap;  // count-free: entries reserved for C (0: sized exactly by the count)
 };
 
 // Warps take tiles dynamically, a batch of kBatch consecutive tiles per
@@ -75,9 +82,10 @@ struct FusedSmem {
   }
 };
 
-template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS>
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false>
 __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k_fused(const FusedParams p_in) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
+  static_assert(!(MEDIUM && CF), "the count-free path is short rows only");
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   using SM = FusedSmem<R, MEDIUM>;
@@ -112,6 +120,14 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     st.clear();
   }
   const uint64_t rows = p.A.rows;
+  // count-free: k_prep found a row the short path cannot take (or bad input)
+  if constexpr (CF) {
+    const volatile unsigned long long* w = p.cf_flags;
+    const unsigned long long ma = w[1], mb = w[2];
+    if (!cf_applies(w[0], ma, mb)) return;
+    if (!cf_ell(ma, mb)) p.ell = nullptr;  // B rows past a record: read B as CSR
+  }
+  uint64_t cf_prods = 0;
 
   // the previous batch waits for its offsets; its metadata lives in s_meta*
   int nprev = 0;
@@ -133,7 +149,10 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     }
     if (tile == 0 && lane == 0) p.c_rp[0] = 0;
     const uint32_t ext = MEDIUM ? 0u : s_meta32[2 * b + 1];  // short variant: external rows
-    if (!MEDIUM && ext) {
+    if (CF && excl + agg > p.c_cap) {
+      // count-free reservation exceeded: write nothing past it, the host redoes it
+      if (lane == 0) atomicOr(p.cf_err, (unsigned long long)kCfOverflow);
+    } else if (!MEDIUM && ext) {
       // the tile mixes staged short rows with rows computed before k_fused
       // (copied into their slots by k_copy_long): place each short row alone
       uint64_t dst = excl;
@@ -188,7 +207,8 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     const uint64_t rpn = __shfl_down_sync(kFull, rpv, 1);
     if (lane < uint32_t(R) && r0 + lane < rows) {
       my_na = uint32_t(rpn - rpv);
-      my_cls = uint32_t(classify(p.prod[r0 + lane], rpn - rpv, p.medium_limit));
+      if constexpr (CF) my_cls = rpn > rpv ? uint32_t(kRowShort) : uint32_t(kRowZero);
+      else my_cls = uint32_t(classify(p.prod[r0 + lane], rpn - rpv, p.medium_limit));
     }
     // per-row results, lane i = row i; rows computed before this kernel
     // (long rows, and in split mode every non-short row) only report nnz
@@ -221,7 +241,8 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
           const uint32_t pcl = __shfl_sync(kFull, my_cls, src);
           if (pi < uint32_t(kLock) && pcl == kRowShort && pe < pna && pe < kEllEntries) {
             asm volatile("prefetch.global.L1 [%0];" ::"l"(p.A.v + plo + pe));
-            pf1 = p.ell + ld_idx(p.A.ci + plo + pe, p.A.pol) * kEllWords;
+            const uint64_t pk = ld_idx(p.A.ci + plo + pe, p.A.pol);
+            pf1 = p.ell + pk * kEllWords;
           }
         }
       }
@@ -241,8 +262,14 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
         for (int i = 0; i < kLock; ++i) any |= hon[i];
         if (!any) continue;
         ShortOut so[kLock];
-        short_rows<kLock, WIDE, STATS, !MEDIUM>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz, hmin,
-                                                hmax, htouch, h == 0 ? pf1 : nullptr);
+        uint32_t hprod[kLock];
+        short_rows<kLock, WIDE, STATS, !MEDIUM, CF>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz,
+                                                    hmin, hmax, htouch, hprod,
+                                                    h == 0 ? pf1 : nullptr);
+        if constexpr (CF) {
+#pragma unroll
+          for (int i = 0; i < kLock; ++i) cf_prods += hon[i] ? hprod[i] : 0u;
+        }
 #pragma unroll
         for (int i = 0; i < kLock; ++i) {
           if (!hon[i]) continue;
@@ -369,6 +396,9 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     nprev = ncur;
     half ^= 1;
   }
+  // count-free: the multiplications (KernelStats.multiplications), one
+  // atomic per warp (every lane holds the same sum)
+  if (CF && lane == 0 && cf_prods) atomicAdd(p.cf_total, (unsigned long long)cf_prods);
 }
 
 // ---------------------------------------------------------------------------

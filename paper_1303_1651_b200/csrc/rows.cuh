@@ -36,14 +36,35 @@ constexpr int kEllWords = 16;   // 64 B per record
 constexpr int kEllValOff = 6;   // values start after 6 column words (byte 24)
 constexpr uint32_t kEllEntries = 32 / kEllSlots;  // 6
 
-template <int R, bool WIDE, bool STATS, bool ELLOK>
+// The count-free path's verdict (k_prep in aux_kernels.cuh measures the rows).
+enum CfFlags : unsigned {
+  kCfBadA = 1,      // A.row_ptr decreasing or past nnz
+  kCfBadB = 2,      // B.row_ptr decreasing or past nnz
+  kCfBadCol = 4,    // an A column >= B.rows
+  kCfOverflow = 32  // C outgrew its reservation (found by k_fused; nothing past it written)
+};
+
+// ctrl + kCtrlCfFlags: [flags, longest A row, longest B row]. Every row of C
+// then has <= max_a * max_b <= 32 products: the short path takes them all.
+__host__ __device__ inline bool cf_applies(unsigned long long flags, unsigned long long max_a,
+                                           unsigned long long max_b) {
+  if (flags & (kCfBadA | kCfBadB | kCfBadCol)) return false;
+  return max_a <= 32 && max_a * max_b <= 32;
+}
+// ... and B is read through its ELL records (when k_prep packed them)
+__host__ __device__ inline bool cf_ell(unsigned long long max_a, unsigned long long max_b) {
+  return max_a <= uint64_t(kEllEntries) && max_b <= uint64_t(kEllSlots);
+}
+
+
+template <int R, bool WIDE, bool STATS, bool ELLOK, bool CF = false>
 __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
                                            const uint32_t* __restrict__ ell,
                                            const uint64_t (&lo)[R], const uint32_t (&na)[R],
                                            const bool (&on)[R], ShortOut (&out)[R],
                                            uint32_t (&nnz)[R], uint32_t (&smin)[R],
                                            uint32_t (&smax)[R], uint32_t (&stouch)[R],
-                                           const void* pf = nullptr) {
+                                           uint32_t (&prods)[R], const void* pf = nullptr) {
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   // narrow variant: every index and offset fits 32 bits (checked on the host)
   using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
@@ -69,6 +90,7 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
       if (on[i] && e < na[i]) {
         const uint64_t k = ld_idx(A.ci + lo[i] + e, A.pol);
         p[i] = ld_val(A.v + lo[i] + e, A.pol);
+        // (count-free path: k_prep has checked every A column against B.rows)
         const uint32_t* rec = ell + k * kEllWords;
         col[i] = ld_u32(rec + j, B.pol);
         bv[i] = ld_val(reinterpret_cast<const double*>(rec + kEllValOff) + j, B.pol);
@@ -205,6 +227,7 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
     out[i].keep = keep;
     out[i].rank = __popc(km & lanemask_lt());
     nnz[i] = __popc(km);
+    if (CF) prods[i] = tot[i];
     if (STATS && on[i]) {
       smin[i] = __shfl_sync(kFull, col[i], 0);
       smax[i] = __shfl_sync(kFull, col[i], (tot[i] - 1) & 31u);

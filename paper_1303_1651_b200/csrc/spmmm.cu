@@ -105,8 +105,8 @@ void release(DevBuf& b, cudaStream_t s) {
 
 const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
                                     "k_rows", "k_long_smem", "k_long_cluster", "k_pack_ell",
-                                    "k_esc_warp", "k_esc_block", "k_esc_plan"};
-constexpr int kNumKernels = 12;
+                                    "k_esc_warp", "k_esc_block", "k_esc_plan", "k_prep"};
+constexpr int kNumKernels = 13;
 constexpr int kMaxPipeBlocks = 16;  // spmmm_multiply_host row blocks
 constexpr uint64_t kNarrowMin = 1 << 20;  // results past this many products: u32 indices down
 
@@ -149,6 +149,8 @@ struct spmmm_context {
   // the shifted row pointers of a download at an offset
   DevBuf part_sums, dl_rp;
   unsigned long long* h_part = nullptr;
+  // operands the count-free path last declined (not retried for them)
+  uint64_t cf_skip[5] = {0, 0, 0, 0, 0};
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -388,10 +390,11 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
 // ---- fused-kernel launch: instantiations live in fused_short.cu / fused_medium.cu ----
 
 int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bool wide,
-               bool stats, unsigned grid, int* occ) {
+               bool stats, unsigned grid, int* occ, bool count_free = false) {
   FusedLaunchEnv env{c->device, c->sms, c->stream};
-  cudaError_t e = medium ? fused_medium(op, prm, env, wide, stats, grid, occ)
-                         : fused_short(op, prm, env, wide, stats, grid, occ);
+  cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ)
+                  : medium   ? fused_medium(op, prm, env, wide, stats, grid, occ)
+                             : fused_short(op, prm, env, wide, stats, grid, occ);
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
                 "k_fused<%s> %s: %s", medium ? "medium" : "short", op ? "launch" : "occupancy",
@@ -743,6 +746,181 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   return join_esc();
 }
 
+// ---- the count-free path (k_prep -> k_fused, one host round trip) ----------
+//
+// aux_kernels.cuh (k_prep) and rows.cuh (cf_applies) say when it applies:
+// every row of C is short by construction, so k_fused runs without k_count's
+// per-row products and without the host reading k_count's results first. C
+// is reserved at the bound that construction gives (30 or 32 entries per A
+// row, 5 per A entry) instead of the exact product count. When the verdict
+// is no (or the input is malformed) nothing was written and the counted path
+// runs; those operands are then not tried again.
+
+constexpr int kCfFallback = -1;
+
+uint64_t lookback_words(uint64_t rows) {
+  uint64_t words = 0, n = rows;
+  for (int l = 0; l < kLevels; ++l) {
+    words += n;
+    n = (n + 31) / 32;
+  }
+  return words;
+}
+
+// Look-back status words + counters for `rows` one-row tiles (the largest
+// layout); the counters are zeroed by k_count / k_prep.
+cudaError_t ensure_lookback(spmmm_context* c, uint64_t rows) {
+  bool grown = false;
+  cudaError_t e = ensure(c->status, (lookback_words(rows) + lb_counters_max(rows)) * 8, c->stream,
+                         &grown);
+  if (e != cudaSuccess) return e;
+  if (grown || c->epoch >= 0xffffu) {
+    e = cudaMemsetAsync(c->status.p, 0, c->status.cap, c->stream);
+    c->epoch = 0;
+  }
+  return e;
+}
+
+void fill_lookback(spmmm_context* c, uint64_t rows, uint64_t ntiles, FusedParams& fp) {
+  uint64_t nl[kLevels];
+  nl[0] = ntiles;
+  for (int l = 1; l < kLevels; ++l) nl[l] = (nl[l - 1] + 31) / 32;
+  c->epoch += 1;
+  unsigned long long* cnt = static_cast<unsigned long long*>(c->status.p);
+  uint64_t* w = reinterpret_cast<uint64_t*>(cnt + lb_counters_max(rows));
+  fp.lb.count[0] = nullptr;
+  for (int l = 0; l < kLevels; ++l) {
+    fp.lb.stat[l] = w;
+    fp.lb.n[l] = nl[l];
+    w += nl[l];
+    if (l > 0) {
+      fp.lb.count[l] = cnt;
+      cnt += nl[l];
+    }
+  }
+  fp.lb.epoch = c->epoch;
+  fp.lb.fault = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlFault;
+}
+
+// Operands the path declined are not retried: keyed by where the caller's
+// arrays are (host addresses for host operands — the upload buffers are
+// reused by every call — device addresses otherwise) and the shapes.
+void cf_key(const spmmm_csr* a, const spmmm_csr* b, uint64_t (&key)[5]) {
+  key[0] = reinterpret_cast<uint64_t>(a->row_ptr);
+  key[1] = reinterpret_cast<uint64_t>(a->col_idx);
+  key[2] = reinterpret_cast<uint64_t>(b->row_ptr);
+  key[3] = a->rows;
+  key[4] = b->rows;
+}
+
+bool cf_candidate(spmmm_context* c, const DevCsr& A, const DevCsr& B, const uint64_t (&key)[5]) {
+  static const bool off = std::getenv("SPMMM_NO_COUNT_FREE") != nullptr;
+  if (off || A.rows == 0 || B.rows == 0) return false;
+  if (B.nnz > 32 * B.rows + B.rows) return false;  // the longest B row is then > 32
+  return std::memcmp(key, c->cf_skip, sizeof key) != 0;
+}
+
+int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool stats, bool wide,
+                        const uint64_t (&key)[5], Timer& tm, spmmm_product** out) {
+  const uint64_t rows = A.rows;
+  // ELL flavour when A spans most of B (the pack covers all of B) and B's
+  // rows can fit records; else B is read as CSR
+  const bool use_ell = 2 * rows >= B.rows && B.nnz <= uint64_t(kEllSlots) * B.rows + B.rows / 8;
+  CUDA_TRY(ensure_lookback(c, rows));
+  if (use_ell) CUDA_TRY(ensure(c->ell, B.rows * 64, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
+  auto* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
+  const uint64_t ncnt = lb_counters_max(rows);
+  tm.begin(12);
+  k_prep<<<unsigned(std::min<uint64_t>((std::max(rows, B.rows) + 255) / 256, uint64_t(c->sms) * 8)),
+           256, 0, c->stream>>>(A, B, ctrl, static_cast<unsigned long long*>(c->status.p), ncnt,
+                                use_ell ? static_cast<uint4*>(c->ell.p) : nullptr);
+  CUDA_TRY(cudaGetLastError());
+  tm.end(12);
+  ++c->last_launches;
+
+  auto* p = new (std::nothrow) spmmm_product;
+  if (!p) return fail(SPMMM_ERR_OOM, "host allocation failed");
+  p->ctx = c;
+  p->rows = rows;
+  p->cols = B.cols;
+  auto cleanup = [&](int code) {
+    product_release(c, p);
+    delete p;
+    return code;
+  };
+  // the reservation: <= 32 products per row; with B rows of <= 5 entries,
+  // <= 5 per A entry. k_fused writes nothing past it (kCfOverflow: redone).
+  const uint64_t cap = use_ell ? std::min<uint64_t>(uint64_t(kEllSlots) * A.nnz, 32 * rows)
+                               : 32 * rows;
+  cudaError_t e = cache_alloc(c, (rows + 1) * 8, reinterpret_cast<void**>(&p->rp), &p->cap[0]);
+  if (e == cudaSuccess)
+    e = cache_alloc(c, std::max<uint64_t>(cap, 1) * 8, reinterpret_cast<void**>(&p->ci), &p->cap[1]);
+  if (e == cudaSuccess)
+    e = cache_alloc(c, std::max<uint64_t>(cap, 1) * 8, reinterpret_cast<void**>(&p->v), &p->cap[2]);
+  if (e == cudaSuccess && stats)
+    e = cache_alloc(c, rows * 3 * sizeof(uint32_t), reinterpret_cast<void**>(&p->st), &p->cap[3]);
+  if (e != cudaSuccess)
+    return cleanup(fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
+                        "allocating C (%llu entries): %s", (unsigned long long)cap,
+                        cudaGetErrorString(e)));
+  const uint64_t ntiles = (rows + kShortRowsPerTile - 1) / kShortRowsPerTile;
+  FusedParams fp{};
+  fill_lookback(c, rows, ntiles, fp);
+  fp.ticket = ctrl + kCtrlTicket;
+  fp.nnz_out = ctrl + kCtrlNnz;
+  fp.A = A;
+  fp.B = B;
+  fp.prod = nullptr;
+  fp.lmap = nullptr;
+  fp.l_nnz = nullptr;
+  fp.c_rp = p->rp;
+  fp.c_ci = p->ci;
+  fp.c_v = p->v;
+  fp.ntiles = ntiles;
+  fp.medium_limit = 0;
+  fp.a_is_b = (A.ci == B.ci && A.v == B.v) ? 1u : 0u;
+  fp.ell = use_ell ? static_cast<const uint32_t*>(c->ell.p) : nullptr;
+  fp.st_min = p->st;
+  fp.st_max = p->st ? p->st + rows : nullptr;
+  fp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+  fp.cf_flags = ctrl + kCtrlCfFlags;
+  fp.cf_total = ctrl + kCtrlTotal;
+  fp.cf_err = ctrl + kCtrlCfFlags;  // (kCfOverflow)
+  fp.c_cap = cap;
+  int occ = 0;
+  int rc = fused_call(c, false, 0, fp, wide, stats, 0, &occ, true);
+  if (rc) return cleanup(rc);
+  const unsigned grid = unsigned(std::min<uint64_t>((ntiles + kFusedWarps - 1) / kFusedWarps,
+                                                    uint64_t(occ) * uint64_t(c->sms)));
+  tm.begin(3);
+  rc = fused_call(c, false, 1, fp, wide, stats, grid, nullptr, true);
+  if (rc) return cleanup(rc);
+  tm.end(3);
+  ++c->last_launches;
+  // the one read-back: every ctrl word (verdict, multiplications, nnz, watchdog)
+  ++c->last_launches;
+  e = readback(ctrl, c->h_ctrl, kCtrlWords, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
+  const unsigned long long* h = c->h_ctrl;
+  if (!cf_applies(h[kCtrlCfFlags], h[kCtrlCfFlags + 1], h[kCtrlCfFlags + 2]) ||
+      (h[kCtrlCfFlags] & kCfOverflow)) {
+    std::memcpy(c->cf_skip, key, sizeof(c->cf_skip));
+    cleanup(0);
+    return kCfFallback;
+  }
+  if (h[kCtrlFault]) {
+    const unsigned long long f = h[kCtrlFault];
+    return cleanup(fail(SPMMM_ERR_CUDA, "k_fused look-back watchdog: site %llu tile %llu",
+                        (f >> 48) & 0x7fff, f & ((1ull << 48) - 1)));
+  }
+  p->nnz = h[kCtrlNnz];
+  p->mults = h[kCtrlTotal];
+  *out = p;
+  return SPMMM_OK;
+}
+
 int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
                   uint32_t flags, spmmm_product** out) {
   if (!out) return fail(SPMMM_ERR_INVALID, "out is NULL");
@@ -775,6 +953,27 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   const uint64_t rows = A.rows;
 
   const Trace tr;
+  uint64_t key[5];
+  cf_key(a, b, key);
+  if (cf_candidate(c, A, B, key)) {
+    const bool wide_s = B.cols > (1ull << 27) || B.nnz >= (1ull << 32) || A.nnz >= (1ull << 32) ||
+                        B.rows >= (1ull << 32);
+    rc = multiply_count_free(c, A, B, stats, wide_s, key, tm, out);
+    if (rc != kCfFallback) {
+      if (rc == SPMMM_OK && tm.on) {
+        for (int k = 0; k < kNumKernels; ++k) {
+          if (!c->ev_used[k]) continue;
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]);
+          c->last_ms[k] = ms;
+        }
+      }
+      tr.mark("count-free product done");
+      return rc;
+    }
+    // (k_prep's time and launches stay in the record: they were spent)
+    tr.mark("count-free path declined: counted path");
+  }
   rc = run_count(c, A, B, tm, true);
   if (rc) return rc;
   tr.mark("count done (host has totals)");
@@ -854,7 +1053,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     nl[0] = ntiles;
     for (int l = 1; l < kLevels; ++l) nl[l] = (nl[l - 1] + 31) / 32;
     c->epoch += 1;
-    FusedParams fp;
+    FusedParams fp{};
     {
       // counters at the front (zeroed by k_count), then the status words
       unsigned long long* cnt = static_cast<unsigned long long*>(c->status.p);
@@ -896,6 +1095,10 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.st_min = p->st;
     fp.st_max = p->st ? p->st + rows : nullptr;
     fp.st_touch = p->st ? p->st + 2 * rows : nullptr;
+    fp.cf_flags = nullptr;
+    fp.cf_total = nullptr;
+    fp.cf_err = nullptr;
+    fp.c_cap = 0;
     int occ = 0;
     rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ);
     if (rc) return fail_staged(rc);

@@ -211,7 +211,8 @@ def test_device_api_and_timings():
         rp, ci, v = p.download()
         assert p.multiplications == 100104
         t = ctx.last_timings()
-        assert "k_count" in t and "k_fused" in t and all(x > 0 for x in t.values())
+        assert ("k_count" in t or "k_prep" in t) and "k_fused" in t
+        assert all(x > 0 for x in t.values())
         assert ctx.last_launch_count() >= 2
         out = dev.product_tensors(p, d)
         assert np.array_equal(out.col_idx.cpu().numpy().view(np.uint64), ci)
