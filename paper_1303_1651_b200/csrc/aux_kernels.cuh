@@ -36,6 +36,7 @@ enum Ctrl : int {
   kCtrlPlanTicket = 24, // k_esc_plan's dynamic row counter
   kCtrlScrCursor = 25,  // k_esc_plan's scratch allocator (slots)
   kCtrlCfFlags = 26,    // count-free path: kCf* bits, then [27] longest A row, [28] longest B row
+  kCtrlDone = 29,       // count-free path: k_fused warps finished (the last one reports)
   kCtrlWords = 32
 };
 

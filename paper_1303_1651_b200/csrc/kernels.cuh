@@ -53,6 +53,12 @@ struct FusedParams {
   unsigned long long* cf_total;
   unsigned long long* cf_err;
   uint64_t c_cap;  // count-free: entries reserved for C (0: sized exactly by the count)
+  // count-free: the last warp to finish copies the ctrl words (ctrl) to the
+  // host's mapped mirror (host_ctrl), so no read-back kernel follows
+  const unsigned long long* ctrl;
+  unsigned long long* host_ctrl;
+  unsigned long long* done;
+  int ctrl_words;
 };
 
 // Warps take tiles dynamically, a batch of kBatch consecutive tiles per
@@ -121,10 +127,11 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
   }
   const uint64_t rows = p.A.rows;
   // count-free: k_prep found a row the short path cannot take (or bad input)
+  bool run = true;
   if constexpr (CF) {
     const volatile unsigned long long* w = p.cf_flags;
     const unsigned long long ma = w[1], mb = w[2];
-    if (!cf_applies(w[0], ma, mb)) return;
+    run = cf_applies(w[0], ma, mb);
     if (!cf_ell(ma, mb)) p.ell = nullptr;  // B rows past a record: read B as CSR
   }
   uint64_t cf_prods = 0;
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
 
   // A tile must be computed right after it is acquired (successors wait on
   // it), so tickets are taken when needed, never ahead.
-  while (true) {
+  while (run) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(p.ticket, (unsigned long long)kBatch);
     base = __shfl_sync(kFull, base, 0);
@@ -398,7 +405,22 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
   }
   // count-free: the multiplications (KernelStats.multiplications), one
   // atomic per warp (every lane holds the same sum)
-  if (CF && lane == 0 && cf_prods) atomicAdd(p.cf_total, (unsigned long long)cf_prods);
+  if constexpr (CF) {
+    if (lane == 0 && cf_prods) atomicAdd(p.cf_total, (unsigned long long)cf_prods);
+    // the last warp out reports every ctrl word to the host (the pattern of
+    // a last-block reduction: fence, count, fence, read through L2)
+    unsigned long long n = 0;
+    if (lane == 0) {
+      __threadfence();
+      n = atomicAdd(p.done, 1ull);
+    }
+    n = __shfl_sync(kFull, n, 0);
+    if (n + 1 == uint64_t(gridDim.x) * WARPS) {
+      __threadfence();
+      if (int(lane) < p.ctrl_words)
+        reinterpret_cast<volatile unsigned long long*>(p.host_ctrl)[lane] = __ldcg(p.ctrl + lane);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

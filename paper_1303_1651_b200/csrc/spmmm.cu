@@ -151,6 +151,8 @@ struct spmmm_context {
   unsigned long long* h_part = nullptr;
   // operands the count-free path last declined (not retried for them)
   uint64_t cf_skip[5] = {0, 0, 0, 0, 0};
+  // ctrl was zeroed behind the last count-free product (off the critical path)
+  bool ctrl_clean = false;
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -344,6 +346,7 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
   }
   if (pack) CUDA_TRY(ensure(c->ell, std::max<uint64_t>(B.rows, 1) * 64, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
+  c->ctrl_clean = false;
   // C = A·A with A's rows its own B rows: k_count writes the ELL copy itself
   const bool self_pack = pack && A.rows && A.rp == B.rp && A.ci == B.ci && A.v == B.v &&
                          A.rows == B.rows;
@@ -828,7 +831,9 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   const bool use_ell = 2 * rows >= B.rows && B.nnz <= uint64_t(kEllSlots) * B.rows + B.rows / 8;
   CUDA_TRY(ensure_lookback(c, rows));
   if (use_ell) CUDA_TRY(ensure(c->ell, B.rows * 64, c->stream));
-  CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
+  if (!c->ctrl_clean)
+    CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream));
+  c->ctrl_clean = false;
   auto* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
   const uint64_t ncnt = lb_counters_max(rows);
   tm.begin(12);
@@ -888,6 +893,10 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   fp.cf_total = ctrl + kCtrlTotal;
   fp.cf_err = ctrl + kCtrlCfFlags;  // (kCfOverflow)
   fp.c_cap = cap;
+  fp.ctrl = ctrl;
+  fp.host_ctrl = c->h_ctrl;
+  fp.done = ctrl + kCtrlDone;
+  fp.ctrl_words = kCtrlWords;
   int occ = 0;
   int rc = fused_call(c, false, 0, fp, wide, stats, 0, &occ, true);
   if (rc) return cleanup(rc);
@@ -898,11 +907,14 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   if (rc) return cleanup(rc);
   tm.end(3);
   ++c->last_launches;
-  // the one read-back: every ctrl word (verdict, multiplications, nnz, watchdog)
-  ++c->last_launches;
-  e = readback(ctrl, c->h_ctrl, kCtrlWords, c->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  // k_fused's last warp has copied every ctrl word (verdict, multiplications,
+  // nnz, watchdog) to h_ctrl: the one host round trip
+  e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
+  // zero ctrl for the next product now, behind this one (off its critical path)
+  if (cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream) ==
+      cudaSuccess)
+    c->ctrl_clean = true;
   const unsigned long long* h = c->h_ctrl;
   if (!cf_applies(h[kCtrlCfFlags], h[kCtrlCfFlags + 1], h[kCtrlCfFlags + 2]) ||
       (h[kCtrlCfFlags] & kCfOverflow)) {
@@ -2046,6 +2058,7 @@ int spmmm_transpose(spmmm_context* c, const spmmm_csr* m, spmmm_product** out) {
   if (e == cudaSuccess) e = ensure(c->tr_scratch, sb, c->stream);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream);
+  c->ctrl_clean = false;
   unsigned long long* err = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlError;
   if (e == cudaSuccess)
     e = transpose_csr(M, base, n, p->rp, p->ci, p->v, c->tr_scratch.p, c->tr_scratch.cap, err,
