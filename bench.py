@@ -374,6 +374,8 @@ def run_single(args):
         step()
         bare_step()
     mults, nnz_c, _, _ = step()
+    with _lib.multiply_views(ctx, va, vb, 6, 0) as p:
+        reserved = p.reserved_bytes()
     torch.cuda.synchronize()
     free0, total_mem = torch.cuda.mem_get_info(device)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -433,6 +435,7 @@ def run_single(args):
         "hbm_bytes": {"operands": int(16 * nnz_a + 8 * (a.rows + 1) +
                                       (0 if same else 16 * len(b.values) + 8 * (b.rows + 1))),
                       "result": int(16 * nnz_c + 8 * (a.rows + 1)),
+                      "result_reserved": int(reserved),
                       "device_used_between_steps": int(total_mem - free0)},
     }
 

@@ -100,6 +100,9 @@ int spmmm_multiply(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b, i
  * kernels.py:330-331 == perfmodel.count_mults). */
 int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
                         uint64_t* multiplications);
+/* Device bytes held by the product's arrays (their reservations: C's
+ * col_idx/values are reserved before nnz(C) is known). */
+int spmmm_product_reserved_bytes(const spmmm_product* p, uint64_t* bytes);
 /* Device pointers of C (valid until spmmm_product_destroy). */
 int spmmm_product_device_arrays(const spmmm_product* p, const uint64_t** row_ptr,
                                 const uint64_t** col_idx, const double** values);

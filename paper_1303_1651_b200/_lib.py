@@ -38,6 +38,7 @@ EXPORTS = (
     "spmmm_abi_version", "spmmm_last_error", "spmmm_device_count",
     "spmmm_context_create", "spmmm_context_destroy", "spmmm_synchronize",
     "spmmm_multiply", "spmmm_multiply_host", "spmmm_product_shape", "spmmm_product_device_arrays",
+    "spmmm_product_reserved_bytes",
     "spmmm_product_download", "spmmm_product_copy_device", "spmmm_product_row_stats",
     "spmmm_product_destroy", "spmmm_estimate_nnz", "spmmm_row_products_prefix",
     "spmmm_transpose", "spmmm_partition_rows", "spmmm_product_download_offset",
@@ -109,6 +110,7 @@ def _declare(lib):
                                ctypes.c_uint32, pp]),
         "spmmm_product_shape": (i, [vp, p_u64, p_u64, p_u64, p_u64]),
         "spmmm_product_device_arrays": (i, [vp, pp, pp, pp]),
+        "spmmm_product_reserved_bytes": (i, [vp, p_u64]),
         "spmmm_product_download": (i, [vp, vp, vp, vp]),
         "spmmm_multiply_host": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr), i,
                                     ctypes.c_uint32, i, ctypes.POINTER(SpmmmHostCsr)]),
@@ -172,6 +174,10 @@ def last_error() -> str:
     return msg.decode() if msg else ""
 
 
+class OutOfMemory(RuntimeError):
+    """SPMMM_ERR_OOM: a device or page-locked host allocation failed."""
+
+
 def check(rc: int, what: str) -> None:
     """Map a status code to the exception the reference raises."""
     if rc == OK:
@@ -179,6 +185,8 @@ def check(rc: int, what: str) -> None:
     msg = last_error() or f"status {rc}"
     if rc in (ERR_DIMENSION, ERR_INVALID):
         raise ValueError(msg)
+    if rc == ERR_OOM:
+        raise OutOfMemory(f"{what}: {msg}")
     raise RuntimeError(f"{what}: {msg}")
 
 
@@ -277,6 +285,11 @@ class Product:
                                         ctypes.byref(nnz), ctypes.byref(mults)), "shape")
         self.rows, self.cols, self.nnz, self.multiplications = (
             rows.value, cols.value, nnz.value, mults.value)
+
+    def reserved_bytes(self) -> int:
+        n = ctypes.c_uint64()
+        check(lib().spmmm_product_reserved_bytes(self._h, ctypes.byref(n)), "reserved bytes")
+        return int(n.value)
 
     def download(self, pinned: bool = True):
         alloc = pinned_empty if pinned else np.empty

@@ -734,6 +734,8 @@ struct CopyParams {
   const uint32_t* row_pbase;
   const uint64_t* part_off;
   const uint32_t* part_nnz;
+  uint64_t c_cap;                  // entries reserved for C: nothing is copied past it
+  unsigned long long* overflow;    // ctrl word: kCfOverflow when a run would pass it
 };
 
 // Copy the staged rows into their slots of C (after k_fused wrote row_ptr).
@@ -789,6 +791,10 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
       for (uint32_t j = 0; j < np; ++j) {
         const uint64_t so = p.part_off[pb + j];
         const uint32_t pc = p.part_nnz[pb + j];
+        if (d + pc > p.c_cap) {
+          if (threadIdx.x == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
+          break;
+        }
         copy_run<4>(cci + d, p.c_v + d, p.l_ci + so, p.l_v + so, pc, threadIdx.x, blockDim.x);
         d += pc;
       }
@@ -796,6 +802,10 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
     }
     const uint64_t src = p.l_off[li];
     const uint32_t cnt = p.l_nnz[li];
+    if (dst + cnt > p.c_cap) {
+      if (threadIdx.x == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
+      continue;
+    }
     copy_run<4>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, threadIdx.x, blockDim.x);
   }
   // the other listed rows (<= long_min products): one warp each, static
@@ -809,6 +819,10 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
     const uint64_t dst = p.c_rp[r];
     const uint64_t src = p.l_off[li];
     const uint32_t cnt = p.l_nnz[li];
+    if (dst + cnt > p.c_cap) {
+      if (lane == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
+      continue;
+    }
     copy_run<4>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, lane, 32);
   }
 }

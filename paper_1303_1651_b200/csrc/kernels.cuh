@@ -52,7 +52,7 @@ struct FusedParams {
   const unsigned long long* cf_flags;
   unsigned long long* cf_total;
   unsigned long long* cf_err;
-  uint64_t c_cap;  // count-free: entries reserved for C (0: sized exactly by the count)
+  uint64_t c_cap;  // entries reserved for C (count-free and medium variants check it)
   // count-free: the last warp to finish copies the ctrl words (ctrl) to the
   // host's mapped mirror (host_ctrl), so no read-back kernel follows
   const unsigned long long* ctrl;
@@ -156,8 +156,9 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     }
     if (tile == 0 && lane == 0) p.c_rp[0] = 0;
     const uint32_t ext = MEDIUM ? 0u : s_meta32[2 * b + 1];  // short variant: external rows
-    if (CF && excl + agg > p.c_cap) {
-      // count-free reservation exceeded: write nothing past it, the host redoes it
+    if ((CF || MEDIUM) && excl + agg > p.c_cap) {
+      // C's reservation exceeded (count-free bound, or the medium variant's
+      // 8·nnz(A)): write nothing past it, the host redoes it sized exactly
       if (lane == 0) atomicOr(p.cf_err, (unsigned long long)kCfOverflow);
     } else if (!MEDIUM && ext) {
       // the tile mixes staged short rows with rows computed before k_fused

@@ -24,6 +24,7 @@
 #include <mutex>
 #include <thread>
 #include <sched.h>
+#include <unistd.h>
 #include <string>
 #include <vector>
 
@@ -153,6 +154,10 @@ struct spmmm_context {
   uint64_t cf_skip[5] = {0, 0, 0, 0, 0};
   // ctrl was zeroed behind the last count-free product (off the critical path)
   bool ctrl_clean = false;
+  // the next counted product reserves C at the product count (an overflow redo)
+  bool exact_reserve = false;
+  // freed product arrays kept for reuse: at most this many bytes
+  size_t cache_limit = size_t(16) << 30;
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
   // of hundreds of MB can cost tens of milliseconds of pool growth)
   std::vector<std::pair<void*, size_t>> cache;
@@ -179,7 +184,6 @@ namespace {
 
 // ---- product array cache ----------------------------------------------------
 
-constexpr size_t kCacheLimit = size_t(48) << 30;
 
 // Best fit among cached blocks of [bytes, 2*bytes + 1 MiB], else a new one.
 cudaError_t cache_alloc(spmmm_context* c, size_t bytes, void** out, size_t* cap) {
@@ -209,7 +213,7 @@ void cache_free(spmmm_context* c, void* ptr, size_t cap) {
   if (!ptr) return;
   c->cache.emplace_back(ptr, cap);
   c->cache_bytes += cap;
-  while (c->cache_bytes > kCacheLimit && !c->cache.empty()) {
+  while (c->cache_bytes > c->cache_limit && !c->cache.empty()) {
     cudaFreeAsync(c->cache.front().first, c->stream);
     c->cache_bytes -= c->cache.front().second;
     c->cache.erase(c->cache.begin());
@@ -1025,13 +1029,24 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     delete p;
     return code;
   };
-  // C storage: one reservation of `total` entries (the reference's own
-  // capacity rule: CsrBuilder(..., estimate_nnz(a, b)), kernels.py:314)
+  // C storage: one reservation. The reference's own capacity rule is the
+  // product count (CsrBuilder(..., estimate_nnz(a, b)), kernels.py:314); on
+  // the device that is physical memory, not lazily touched pages
+  // (formats.py:161-163), and for long medium rows it is far above nnz(C)
+  // (C4: 705M products, 120.6M entries). The medium variant reserves
+  // min(products, 8 nnz(A)) entries (SPMMM_C_RESERVE overrides 8); a product
+  // that outgrows it writes nothing past it and is redone sized exactly.
+  static const uint64_t reserve_factor = std::getenv("SPMMM_C_RESERVE")
+                                             ? std::strtoull(std::getenv("SPMMM_C_RESERVE"), nullptr, 10)
+                                             : 8;
+  const uint64_t cap = (medium && !c->exact_reserve)
+                           ? std::min<uint64_t>(total, std::max<uint64_t>(reserve_factor * A.nnz, 1u << 20))
+                           : total;
   cudaError_t e = cache_alloc(c, (rows + 1) * 8, reinterpret_cast<void**>(&p->rp), &p->cap[0]);
   if (e == cudaSuccess)
-    e = cache_alloc(c, std::max<uint64_t>(total, 1) * 8, reinterpret_cast<void**>(&p->ci), &p->cap[1]);
+    e = cache_alloc(c, std::max<uint64_t>(cap, 1) * 8, reinterpret_cast<void**>(&p->ci), &p->cap[1]);
   if (e == cudaSuccess)
-    e = cache_alloc(c, std::max<uint64_t>(total, 1) * 8, reinterpret_cast<void**>(&p->v), &p->cap[2]);
+    e = cache_alloc(c, std::max<uint64_t>(cap, 1) * 8, reinterpret_cast<void**>(&p->v), &p->cap[2]);
   if (e == cudaSuccess && stats)
     e = cache_alloc(c, std::max<uint64_t>(rows, 1) * 3 * sizeof(uint32_t),
                     reinterpret_cast<void**>(&p->st), &p->cap[3]);
@@ -1109,8 +1124,8 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.st_touch = p->st ? p->st + 2 * rows : nullptr;
     fp.cf_flags = nullptr;
     fp.cf_total = nullptr;
-    fp.cf_err = nullptr;
-    fp.c_cap = 0;
+    fp.cf_err = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCfFlags;  // (kCfOverflow)
+    fp.c_cap = cap;
     int occ = 0;
     rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ);
     if (rc) return fail_staged(rc);
@@ -1152,6 +1167,8 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       cp.row_np = parts ? cp.row_pbase + (c->h_ctrl[kCtrlHugeProducts] / kHugeMin + 16) : nullptr;
       cp.part_off = parts ? static_cast<const uint64_t*>(c->part_off.p) : nullptr;
       cp.part_nnz = parts ? static_cast<const uint32_t*>(c->part_nnz.p) : nullptr;
+      cp.c_cap = cap;
+      cp.overflow = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCfFlags;
       k_copy_long<<<c->sms * 8, 256, 0, c->stream>>>(cp);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail_staged(fail(SPMMM_ERR_CUDA, "k_copy_long: %s",
@@ -1161,18 +1178,31 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     }
   }
   tr.mark("fused + copy launched");
-  // one read-back: the watchdog word through nnz(C) (rows == 0: nnz is 0)
-  static_assert(kCtrlNnz > kCtrlFault, "ctrl layout");
-  if (!rows) c->h_ctrl[kCtrlNnz] = 0;
+  // one read-back: the watchdog word through nnz(C) and the overflow word
+  // (rows == 0: nnz is 0)
+  static_assert(kCtrlNnz > kCtrlFault && kCtrlCfFlags > kCtrlNnz, "ctrl layout");
+  if (!rows) {
+    c->h_ctrl[kCtrlNnz] = 0;
+    c->h_ctrl[kCtrlCfFlags] = 0;
+  }
   ++c->last_launches;  // (k_readback)
   e = readback(static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlFault, c->h_ctrl + kCtrlFault,
-               rows ? kCtrlNnz - kCtrlFault + 1 : 1, c->stream);
+               rows ? kCtrlCfFlags - kCtrlFault + 1 : 1, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
   if (c->h_ctrl[kCtrlFault]) {
     const unsigned long long f = c->h_ctrl[kCtrlFault];
     return cleanup(fail(SPMMM_ERR_CUDA, "k_fused look-back watchdog: site %llu tile %llu",
                         (f >> 48) & 0x7fff, f & ((1ull << 48) - 1)));
+  }
+  if (c->h_ctrl[kCtrlCfFlags] & kCfOverflow) {
+    // C outgrew the reservation: once more, sized by the product count
+    cleanup(0);
+    tr.mark("C outgrew its reservation: redone sized exactly");
+    c->exact_reserve = true;
+    rc = multiply_impl(c, a, b, strategy, flags, out);
+    c->exact_reserve = false;
+    return rc;
   }
   p->nnz = c->h_ctrl[kCtrlNnz];
   tr.mark("done");
@@ -1591,6 +1621,11 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     publish(G + 1);
     for (auto& t : workers) t.join();
     workers.clear();
+    // the copy engines may still be writing into the staging blocks: drain
+    // both copy streams before they go back to the pool (another thread may
+    // be handed them by spmmm_host_alloc at once)
+    cudaStreamSynchronize(c->s_down);
+    cudaStreamSynchronize(c->s_up);
     if (hci32) host_free_internal(hci32);
     if (hrp32) host_free_internal(hrp32);
     if (hd16) host_free_internal(hd16);
@@ -1833,6 +1868,10 @@ int spmmm_context_create(int device, void* cuda_stream, spmmm_context** out) {
   if (!c) return fail(SPMMM_ERR_OOM, "host allocation failed");
   c->device = device;
   c->sms = prop.multiProcessorCount;
+  // product cache: a quarter of the device's memory unless
+  // SPMMM_DEVICE_CACHE_BYTES says otherwise
+  const char* dcl = std::getenv("SPMMM_DEVICE_CACHE_BYTES");
+  c->cache_limit = dcl ? size_t(std::strtoull(dcl, nullptr, 10)) : size_t(prop.totalGlobalMem / 4);
   // keep freed blocks in the pool: repeated products reuse their memory
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -1918,6 +1957,12 @@ int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, 
   if (cols) *cols = p->cols;
   if (nnz) *nnz = p->nnz;
   if (mults) *mults = p->mults;
+  return SPMMM_OK;
+}
+
+int spmmm_product_reserved_bytes(const spmmm_product* p, uint64_t* bytes) {
+  if (!p || !bytes) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  *bytes = p->cap[0] + p->cap[1] + p->cap[2] + p->cap[3];
   return SPMMM_OK;
 }
 
@@ -2239,7 +2284,15 @@ struct HostPool {
   std::multimap<uint64_t, void*> free_blocks;  // capacity -> block
   std::map<void*, uint64_t> live;              // block -> capacity
   uint64_t in_use = 0, cached = 0;
-  static constexpr uint64_t kCacheLimit = 64ull << 30;
+  // page-locked bytes kept for reuse: an eighth of the host's memory unless
+  // SPMMM_HOST_CACHE_BYTES says otherwise
+  uint64_t cache_limit = 0;
+  HostPool() {
+    const char* e = std::getenv("SPMMM_HOST_CACHE_BYTES");
+    const long pages = sysconf(_SC_PHYS_PAGES), page = sysconf(_SC_PAGESIZE);
+    cache_limit = e ? std::strtoull(e, nullptr, 10)
+                    : (pages > 0 && page > 0 ? uint64_t(pages) * uint64_t(page) / 8 : 8ull << 30);
+  }
 
   static uint64_t bucket(uint64_t bytes) {
     // round up to 1/8 steps of the next power of two to bound waste
@@ -2305,7 +2358,7 @@ int spmmm_host_free(void* ptr) {
   const uint64_t cap = it->second;
   hp.live.erase(it);
   hp.in_use -= cap;
-  if (hp.cached + cap > HostPool::kCacheLimit) {
+  if (hp.cached + cap > hp.cache_limit) {
     cudaFreeHost(ptr);
   } else {
     hp.free_blocks.emplace(cap, ptr);

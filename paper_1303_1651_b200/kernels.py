@@ -132,9 +132,14 @@ def multiply_rowmajor(a, b, strategy=StrategyKind.COMBINED, stats=None):
     ctx = _lib.default_context()
     if stats is None and len(av) >= PIPELINE_MIN_NNZ:
         # large host operands: uploads, kernels and downloads overlap in row
-        # blocks (spmmm_multiply_host); the same bytes as the path below
-        rp, ci, v, _ = _lib.multiply_host(ctx, va, vb, sid, 0, pipeline_blocks(len(av)))
-        return make_like(a, a.rows, b.cols, rp, ci, v)
+        # blocks (spmmm_multiply_host); the same bytes as the path below.
+        # Its result reservation is page-locked host memory (8 nnz(A)
+        # entries); if that cannot be had, the one-shot path below runs.
+        try:
+            rp, ci, v, _ = _lib.multiply_host(ctx, va, vb, sid, 0, pipeline_blocks(len(av)))
+            return make_like(a, a.rows, b.cols, rp, ci, v)
+        except _lib.OutOfMemory:
+            pass
     with _lib.multiply_views(ctx, va, vb, sid, flags) as product:
         rp, ci, v = product.download()
         if stats is not None:

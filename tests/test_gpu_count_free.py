@@ -181,3 +181,39 @@ def test_single_host_round_trip_launches():
         with _lib.multiply_views(ctx, va, va, 6, 0):
             assert ctx.last_launch_count() == 2
     ctx.close()
+
+
+def test_medium_reservation_overflow_is_redone_exactly():
+    """The medium variant reserves min(products, SPMMM_C_RESERVE x nnz(A))
+    entries (at least 2^20); with a factor of 1 the 40^3 27-point stencil's square (nnz(C) ~ 4.5
+    nnz(A)) outgrows it, writes nothing past it and is redone sized by the
+    product count: same bytes, and the redo's reservation is the exact one."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path[:0] = ['.', 'oracle']\n"
+        "import oracle\n"
+        "from paper_1303_1651_b200 import _lib, genmat\n"
+        "a = genmat.gen_fd3(40)\n"
+        "ctx = _lib.Context(0)\n"
+        "v = _lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values)\n"
+        "with _lib.multiply_views(ctx, v, v, 6, 0) as p:\n"
+        "    rp, ci, vv = p.download(); res = p.reserved_bytes(); m = p.multiplications\n"
+        "r = oracle.multiply_rowmajor(a, a, threads=8)\n"
+        "assert rp.tobytes() == r.row_ptr.tobytes() and ci.tobytes() == r.col_idx.tobytes()\n"
+        "assert vv.tobytes() == r.values.tobytes() and m == r.multiplications\n"
+        "print(res, len(vv), m)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for factor in ("1", "8"):
+        env = dict(os.environ, SPMMM_C_RESERVE=factor)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out[factor] = [int(x) for x in r.stdout.split()]
+    res1, nnz, mults = out["1"]
+    res8, _, _ = out["8"]
+    assert res1 >= 16 * mults  # redone at the product count
+    assert res8 < 16 * mults and res8 >= 16 * nnz  # the bounded reservation held

@@ -10,6 +10,7 @@ order exactly.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -490,3 +491,56 @@ def test_split_mode_hash_kernels_past_esc_key_range(values):
                              CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx, ref.values),
                              f"hash/{values}")
     assert np.array_equal(_choices_array(stats, a.rows), ref.row_choices)
+
+
+def _banded_then_random(n=200_000, seed=3):
+    """Top half: tridiagonal rows (C rows span a few columns: u16 deltas);
+    bottom half: 4 random columns over n > 2^16 (u32 fallback)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for r in range(n // 2):
+        rows.append(np.array([c for c in (r - 1, r, r + 1) if 0 <= c < n]))
+    for _ in range(n - n // 2):
+        rows.append(np.sort(rng.choice(n, 4, replace=False)))
+    lens = np.array([len(x) for x in rows])
+    rp = np.zeros(n + 1, np.uint64)
+    np.cumsum(lens, out=rp[1:])
+    ci = np.concatenate(rows).astype(np.uint64)
+    v = rng.integers(-3, 4, ci.size).astype(np.float64)
+    return CsrMatrix(n, n, rp, ci, v)
+
+
+@pytest.mark.parametrize("no_delta", [False, True])
+def test_pipelined_mixed_u16_and_u32_blocks(no_delta):
+    """One product whose first row blocks go down as u16 column deltas and
+    whose last blocks fall back to u32 (the cb_next / blk_cb bookkeeping
+    across mixed blocks), bitwise against the oracle; and the same with the
+    deltas off (SPMMM_NO_DELTA16, read once per process: a subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    if no_delta:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        code = ("import sys; sys.path[:0] = ['.', 'oracle', 'tests']\n"
+                "import test_gpu_parity as t\n"
+                "t.test_pipelined_mixed_u16_and_u32_blocks(False)\n")
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                           env=dict(os.environ, SPMMM_NO_DELTA16="1"), timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return
+    a = _banded_then_random()
+    ref = oracle.multiply_rowmajor(a, a, threads=8)
+    ctx = _lib.Context(0)
+    va, _ = _host_views(a, a)
+    for blocks in (4, 8, 13):
+        rp, ci, v, mults = _lib.multiply_host(ctx, va, va, 6, 0, blocks)
+        assert mults == ref.multiplications
+        assert_csr_bitwise_equal(CsrMatrix(a.rows, a.cols, rp, ci, v),
+                                 CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx,
+                                           ref.values), f"mixed/{blocks}")
+        # fewer bytes than u32 indices for all of C: some blocks went as u16
+        d2h = _lib.last_transfer["d2h_bytes"]
+        if os.environ.get("SPMMM_NO_DELTA16") is None:
+            assert d2h < 4 * (a.rows + 1) + 12 * len(v), (blocks, d2h)
+    ctx.close()
