@@ -113,6 +113,10 @@ constexpr uint64_t kNarrowMin = 1 << 20;  // results past this many products: u3
 
 }  // namespace
 
+namespace {
+struct Stager;
+}
+
 struct spmmm_context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -156,6 +160,8 @@ struct spmmm_context {
   bool ctrl_clean = false;
   // the next counted product reserves C at the product count (an overflow redo)
   bool exact_reserve = false;
+  // page-locked staging of pageable uploads (spmmm_multiply_host), lazily
+  Stager* stager = nullptr;
   // freed product arrays kept for reuse: at most this many bytes
   size_t cache_limit = size_t(16) << 30;
   // freed product arrays, reused by later products (a fresh cudaMallocAsync
@@ -1383,6 +1389,132 @@ void widen(const uint32_t* in, uint64_t* out, uint64_t n) {
 int host_alloc_internal(uint64_t bytes, void** ptr) { return spmmm_host_alloc(bytes, ptr); }
 int host_free_internal(void* ptr) { return ptr ? spmmm_host_free(ptr) : SPMMM_OK; }
 
+// ---- uploads from pageable host memory -------------------------------------
+//
+// cudaMemcpyAsync from pageable memory stages through the driver's own small
+// buffers at the speed of one host thread, serialised with the caller. The
+// reference's callers hand over ordinary numpy arrays (formats.py:35-58), so
+// the pipelined path stages them itself: a few page-locked slots, each chunk
+// copied into a slot by several host threads while the copy engine moves the
+// previous slots to the device.
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this, i]() { loop(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return int(th_.size()); }
+  // dst[0, n) = src[0, n), split over the pool's threads and the caller
+  void copy(void* dst, const void* src, size_t n) {
+    const int parts = size() + 1;
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    n_ = n;
+    parts_ = parts;
+    pending_ = size();
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    piece(parts - 1);
+    lk.lock();
+    done_cv_.wait(lk, [&]() { return pending_ == 0; });
+  }
+
+ private:
+  void piece(int i) {
+    const size_t a = n_ * size_t(i) / size_t(parts_), b = n_ * size_t(i + 1) / size_t(parts_);
+    if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
+  }
+  void loop(int i) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    while (true) {
+      cv_.wait(lk, [&]() { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      lk.unlock();
+      piece(i);
+      lk.lock();
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  bool stop_ = false;
+  uint64_t gen_ = 0;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t n_ = 0;
+  int parts_ = 1, pending_ = 0;
+};
+
+struct Stager {
+  static constexpr int kSlots = 4;
+  static constexpr size_t kSlotBytes = size_t(16) << 20;
+  void* slot[kSlots] = {};
+  cudaEvent_t done[kSlots] = {};
+  int next = 0;
+  CopyPool* pool = nullptr;
+  ~Stager() {
+    for (int k = 0; k < kSlots; ++k) {
+      if (done[k]) cudaEventSynchronize(done[k]);
+      if (slot[k]) spmmm_host_free(slot[k]);
+      if (done[k]) cudaEventDestroy(done[k]);
+    }
+    delete pool;
+  }
+  cudaError_t init() {
+    if (pool) return cudaSuccess;
+    for (int k = 0; k < kSlots; ++k) {
+      if (spmmm_host_alloc(kSlotBytes, &slot[k]) != SPMMM_OK) return cudaErrorMemoryAllocation;
+      cudaError_t e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    cpu_set_t cs;
+    const int ncpu = sched_getaffinity(0, sizeof(cs), &cs) == 0 ? CPU_COUNT(&cs) : 8;
+    static const int env = std::getenv("SPMMM_STAGE_THREADS")
+                               ? std::atoi(std::getenv("SPMMM_STAGE_THREADS")) : 0;
+    pool = new CopyPool(std::max(0, (env > 0 ? env : std::max(1, std::min(ncpu / 4, 4))) - 1));
+    return cudaSuccess;
+  }
+  // host (pageable) -> device on stream s, through the slots
+  cudaError_t copy(void* dst, const void* src, size_t bytes, cudaStream_t s,
+                   const std::atomic<bool>& abort) {
+    for (size_t off = 0; off < bytes && !abort.load(std::memory_order_relaxed);
+         off += kSlotBytes) {
+      const size_t n = std::min(kSlotBytes, bytes - off);
+      const int k = next++ % kSlots;
+      cudaError_t e = cudaEventSynchronize(done[k]);  // the slot's last copy has left
+      if (e != cudaSuccess) return e;
+      pool->copy(slot[k], static_cast<const char*>(src) + off, n);
+      e = cudaMemcpyAsync(static_cast<char*>(dst) + off, slot[k], n, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return e;
+      e = cudaEventRecord(done[k], s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+};
+
+bool host_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
                        uint32_t flags, int blocks, spmmm_host_csr* out) {
   if (!out) return fail(SPMMM_ERR_INVALID, "out is NULL");
@@ -1457,53 +1589,120 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   // (each block's own count validates it and sizes its part of C).
   cudaEvent_t* ev_maxc = &c->pev[2 + 4 * kMaxPipeBlocks];
   uint64_t* d_aux = static_cast<uint64_t*>(c->aux.p);
-  if (!same) {
-    CUDA_TRY(cudaMemcpyAsync(c->b_rp.p, b->row_ptr, (b->rows + 1) * 8, cudaMemcpyHostToDevice,
-                             c->s_up));
-    if (b->nnz) {
-      CUDA_TRY(cudaMemcpyAsync(c->b_ci.p, b->col_idx, b->nnz * 8, cudaMemcpyHostToDevice,
-                               c->s_up));
-      CUDA_TRY(cudaMemcpyAsync(c->b_v.p, b->values, b->nnz * 8, cudaMemcpyHostToDevice, c->s_up));
+  // Pageable operands (ordinary numpy arrays) go up through page-locked
+  // staging on an uploader thread; the compute loop below waits for each
+  // block's upload step to be issued (events must be recorded before a
+  // stream can wait on them). Pinned operands are issued right here.
+  const bool pageable = !host_pinned(a->row_ptr) || !host_pinned(a->col_idx) ||
+                        !host_pinned(a->values) ||
+                        (!same && (!host_pinned(b->row_ptr) || !host_pinned(b->col_idx) ||
+                                   !host_pinned(b->values)));
+  static const bool no_stage = std::getenv("SPMMM_NO_STAGE") != nullptr;
+  const bool staged = pageable && !no_stage;
+  if (staged) {
+    if (!c->stager) c->stager = new (std::nothrow) Stager;
+    if (!c->stager) return fail(SPMMM_ERR_OOM, "host allocation failed");
+    CUDA_TRY(c->stager->init());
+  }
+  std::atomic<bool> up_abort{false};
+  std::atomic<int> up_issued{0};  // upload steps issued: 1 (B) + one per A block
+  std::atomic<int> up_error{0};
+  std::string up_msg;
+  std::mutex up_mu;
+  std::condition_variable up_cv;
+  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!bytes) return cudaSuccess;
+    if (staged) return c->stager->copy(dst, src, bytes, c->s_up, up_abort);
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s_up);
+  };
+  auto issue_uploads = [&]() -> int {
+    cudaSetDevice(c->device);
+    auto step_done = [&](int n) {
+      {
+        std::lock_guard<std::mutex> lk(up_mu);
+        up_issued.store(n, std::memory_order_release);
+      }
+      up_cv.notify_all();
+    };
+    if (!same) {
+      CUDA_TRY(h2d(c->b_rp.p, b->row_ptr, (b->rows + 1) * 8));
+      CUDA_TRY(h2d(c->b_ci.p, b->col_idx, b->nnz * 8));
+      CUDA_TRY(h2d(c->b_v.p, b->values, b->nnz * 8));
+    }
+    CUDA_TRY(cudaEventRecord(*ev_bv, c->s_up));
+    step_done(1);
+    for (int j = 0; j < G && !up_abort.load(); ++j) {
+      const uint64_t r0 = bound[j], r1 = bound[j + 1];
+      const uint64_t e0 = a->rows ? arp[r0] : 0, e1 = a->rows ? arp[r1] : 0;
+      CUDA_TRY(h2d(d_arp + r0, arp + r0, (r1 - r0 + 1) * 8));
+      if (e1 > e0) CUDA_TRY(h2d(d_aci + e0, a->col_idx + e0, (e1 - e0) * 8));
+      if (same && r1 > r0) {
+        PipeBounds pb;
+        pb.r[0] = r0;
+        pb.r[1] = r1;
+        k_zero_u64<<<1, 32, 0, c->s_up>>>(d_aux + j, 1);
+        k_block_maxcol<<<kPipeSplit, 256, 0, c->s_up>>>(
+            d_arp, d_aci, pb, reinterpret_cast<unsigned long long*>(d_aux + j));
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(readback(reinterpret_cast<const unsigned long long*>(d_aux + j), c->h_aux + j, 1,
+                          c->s_up));
+        CUDA_TRY(cudaEventRecord(ev_maxc[j], c->s_up));
+      }
+      if (e1 > e0) CUDA_TRY(h2d(d_av + e0, a->values + e0, (e1 - e0) * 8));
+      CUDA_TRY(cudaEventRecord(ev_av[j], c->s_up));
+      step_done(j + 2);
+    }
+    return SPMMM_OK;
+  };
+  std::thread uploader;
+  if (staged) {
+    uploader = std::thread([&]() {
+      const int rc_up = issue_uploads();
+      if (rc_up) {
+        std::lock_guard<std::mutex> lk(up_mu);
+        up_msg = g_error;  // (thread-local: carried over to the caller's thread)
+        up_error.store(rc_up);
+      }
+      {
+        std::lock_guard<std::mutex> lk(up_mu);
+        up_issued.store(G + 2, std::memory_order_release);  // nothing more will come
+      }
+      up_cv.notify_all();
+    });
+  } else {
+    rc = issue_uploads();
+    if (rc) {
+      cudaStreamSynchronize(c->s_up);
+      return rc;
     }
   }
-  CUDA_TRY(cudaEventRecord(*ev_bv, c->s_up));
-  for (int j = 0; j < G; ++j) {
-    const uint64_t r0 = bound[j], r1 = bound[j + 1];
-    const uint64_t e0 = a->rows ? arp[r0] : 0, e1 = a->rows ? arp[r1] : 0;
-    CUDA_TRY(cudaMemcpyAsync(d_arp + r0, arp + r0, (r1 - r0 + 1) * 8, cudaMemcpyHostToDevice,
-                             c->s_up));
-    if (e1 > e0)
-      CUDA_TRY(cudaMemcpyAsync(d_aci + e0, a->col_idx + e0, (e1 - e0) * 8,
-                               cudaMemcpyHostToDevice, c->s_up));
-    if (same && r1 > r0) {
-      PipeBounds pb;
-      pb.r[0] = r0;
-      pb.r[1] = r1;
-      k_zero_u64<<<1, 32, 0, c->s_up>>>(d_aux + j, 1);
-      k_block_maxcol<<<kPipeSplit, 256, 0, c->s_up>>>(
-          d_arp, d_aci, pb, reinterpret_cast<unsigned long long*>(d_aux + j));
-      CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(readback(reinterpret_cast<const unsigned long long*>(d_aux + j), c->h_aux + j, 1,
-                        c->s_up));
-      CUDA_TRY(cudaEventRecord(ev_maxc[j], c->s_up));
+  auto join_uploader = [&]() {
+    if (uploader.joinable()) {
+      up_abort.store(true);
+      uploader.join();
     }
-    if (e1 > e0)
-      CUDA_TRY(cudaMemcpyAsync(d_av + e0, a->values + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice,
-                               c->s_up));
-    CUDA_TRY(cudaEventRecord(ev_av[j], c->s_up));
-  }
+  };
+  // until the uploader has issued step n (1: B, j + 2: A block j)
+  auto wait_upload = [&](int n) -> int {
+    if (!staged) return SPMMM_OK;
+    std::unique_lock<std::mutex> lk(up_mu);
+    up_cv.wait(lk, [&]() { return up_issued.load(std::memory_order_acquire) >= n; });
+    if (up_error.load()) return fail(up_error.load(), "%s", up_msg.c_str());
+    return SPMMM_OK;
+  };
   DevCsr B{d_arp, d_aci, d_av, a->rows, a->cols, a->nnz};
   if (!same)
     B = DevCsr{static_cast<const uint64_t*>(c->b_rp.p), static_cast<const uint64_t*>(c->b_ci.p),
                static_cast<const double*>(c->b_v.p), b->rows, b->cols, b->nnz};
   B.cols = b->cols;
   auto drain = [&](int code) {
+    join_uploader();
     cudaStreamSynchronize(c->s_up);
     cudaStreamSynchronize(c->s_down);
     cudaStreamSynchronize(c->stream);
     return code;
   };
-  tr.mark("pipe: uploads issued");
+  tr.mark(staged ? "pipe: staged uploads started" : "pipe: uploads issued");
   // 4. the result, in pinned host memory from the pool: 8 nnz(A) entries
   // (C2 2.6, C3 5, C4 4.6, C5 6 nnz(C) per A entry); should a block overflow
   // that, the product is redone in one shot (below).
@@ -1660,12 +1859,16 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     const uint64_t r0 = bound[j], r1 = bound[j + 1];
     if (r1 == r0) continue;
     int u = j;  // the last A block this block needs resident
+    rc = wait_upload(j + 2);
+    if (rc) return rc;  // (the guard cleans up)
     if (same && a->rows) {
       CUDA_TRY(cudaEventSynchronize(ev_maxc[j]));
       const uint64_t row = c->h_aux[j];  // rows [0, row] of B = A (row_ptr to row + 1)
       const int uu = int(std::upper_bound(bound, bound + G + 1, row) - bound) - 1;
       u = std::min(std::max(uu, j), G - 1);
     }
+    rc = wait_upload(u + 2);
+    if (rc) return rc;
     CUDA_TRY(cudaStreamWaitEvent(c->stream, ev_av[u], 0));
     if (!same) CUDA_TRY(cudaStreamWaitEvent(c->stream, *ev_bv, 0));
     spmmm_csr va{r1 - r0, a->cols, a->nnz, d_arp + r0, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
@@ -1759,6 +1962,8 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     // the reservation was too small: one product over the resident operands
     // into exact-size arrays (the operands are all up once s_up drains)
     stop_workers();
+    if (uploader.joinable()) uploader.join();  // every upload issued (no abort)
+    if (up_error.load()) return fail(up_error.load(), "%s", up_msg.c_str());
     CUDA_TRY(cudaStreamSynchronize(c->s_down));
     CUDA_TRY(cudaStreamSynchronize(c->s_up));
     release_all();
@@ -1805,6 +2010,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     tr.mark("pipe: downloads done (trace only: waits before joining)");
   }
   for (auto& t : workers) t.join();
+  if (uploader.joinable()) uploader.join();  // (its last step was waited for above)
   tr.mark("pipe: widening done");
   workers.clear();
   if (hci32) host_free_internal(hci32);
@@ -1923,6 +2129,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   if (c->s_down) cudaStreamDestroy(c->s_down);
   if (c->h_aux) cudaFreeHost(c->h_aux);
   if (c->h_part) cudaFreeHost(c->h_part);
+  delete c->stager;
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
