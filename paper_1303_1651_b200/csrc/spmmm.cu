@@ -250,6 +250,8 @@ int check_view(const spmmm_csr* m, const char* name) {
   return SPMMM_OK;
 }
 
+int stage_h2d(spmmm_context* c, void* dst, const void* src, size_t bytes);
+
 // Upload a host CSR view into context buffers; return a device view.
 int upload(spmmm_context* c, const spmmm_csr* m, DevBuf& rp, DevBuf& ci, DevBuf& v, DevCsr* out) {
   const size_t rpb = (m->rows + 1) * sizeof(uint64_t);
@@ -257,11 +259,10 @@ int upload(spmmm_context* c, const spmmm_csr* m, DevBuf& rp, DevBuf& ci, DevBuf&
   CUDA_TRY(ensure(rp, rpb, c->stream));
   CUDA_TRY(ensure(ci, cib, c->stream));
   CUDA_TRY(ensure(v, vb, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(rp.p, m->row_ptr, rpb, cudaMemcpyHostToDevice, c->stream));
-  if (m->nnz) {
-    CUDA_TRY(cudaMemcpyAsync(ci.p, m->col_idx, cib, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(v.p, m->values, vb, cudaMemcpyHostToDevice, c->stream));
-  }
+  int rc = stage_h2d(c, rp.p, m->row_ptr, rpb);
+  if (!rc && m->nnz) rc = stage_h2d(c, ci.p, m->col_idx, cib);
+  if (!rc && m->nnz) rc = stage_h2d(c, v.p, m->values, vb);
+  if (rc) return rc;
   out->rp = static_cast<const uint64_t*>(rp.p);
   out->ci = static_cast<const uint64_t*>(ci.p);
   out->v = static_cast<const double*>(v.p);
@@ -1405,61 +1406,68 @@ class CopyPool {
   ~CopyPool() {
     {
       std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
+      stop_.store(true);
     }
     cv_.notify_all();
     for (auto& t : th_) t.join();
   }
   int size() const { return int(th_.size()); }
-  // dst[0, n) = src[0, n), split over the pool's threads and the caller
+  // dst[0, n) = src[0, n), split over the pool's threads and the caller.
+  // Workers spin briefly before sleeping: chunks follow each other within
+  // microseconds and a condition-variable wake-up costs tens of them.
   void copy(void* dst, const void* src, size_t n) {
-    const int parts = size() + 1;
-    std::unique_lock<std::mutex> lk(mu_);
     dst_ = static_cast<char*>(dst);
     src_ = static_cast<const char*>(src);
     n_ = n;
-    parts_ = parts;
-    pending_ = size();
-    ++gen_;
-    lk.unlock();
+    pending_.store(size(), std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      gen_.fetch_add(1, std::memory_order_release);
+    }
     cv_.notify_all();
-    piece(parts - 1);
-    lk.lock();
-    done_cv_.wait(lk, [&]() { return pending_ == 0; });
+    piece(size());
+    while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
   }
 
  private:
   void piece(int i) {
-    const size_t a = n_ * size_t(i) / size_t(parts_), b = n_ * size_t(i + 1) / size_t(parts_);
+    const size_t parts = size_t(size()) + 1;
+    const size_t a = n_ * size_t(i) / parts, b = n_ * size_t(i + 1) / parts;
     if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
   }
   void loop(int i) {
     uint64_t seen = 0;
-    std::unique_lock<std::mutex> lk(mu_);
     while (true) {
-      cv_.wait(lk, [&]() { return stop_ || gen_ != seen; });
-      if (stop_) return;
-      seen = gen_;
-      lk.unlock();
+      uint64_t g = gen_.load(std::memory_order_acquire);
+      for (int spin = 0; g == seen && spin < 20000 && !stop_.load(); ++spin) {
+        _mm_pause();
+        g = gen_.load(std::memory_order_acquire);
+      }
+      if (g == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&]() { return stop_.load() || gen_.load() != seen; });
+        g = gen_.load(std::memory_order_acquire);
+      }
+      if (stop_.load()) return;
+      seen = g;
       piece(i);
-      lk.lock();
-      if (--pending_ == 0) done_cv_.notify_one();
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
   std::vector<std::thread> th_;
   std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  bool stop_ = false;
-  uint64_t gen_ = 0;
+  std::condition_variable cv_;
+  std::atomic<bool> stop_{false};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0};
   char* dst_ = nullptr;
   const char* src_ = nullptr;
   size_t n_ = 0;
-  int parts_ = 1, pending_ = 0;
 };
 
 struct Stager {
-  static constexpr int kSlots = 4;
-  static constexpr size_t kSlotBytes = size_t(16) << 20;
+  static constexpr int kSlots = 8;
+  static constexpr size_t kSlotBytes = size_t(4) << 20;
   void* slot[kSlots] = {};
   cudaEvent_t done[kSlots] = {};
   int next = 0;
@@ -1513,6 +1521,24 @@ bool host_pinned(const void* p) {
     return false;
   }
   return at.type == cudaMemoryTypeHost;
+}
+
+// One host->device copy on the context stream: pageable sources of 8 MiB and
+// more go through the page-locked staging slots (several host threads), the
+// rest straight to the copy engine.
+int stage_h2d(spmmm_context* c, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return SPMMM_OK;
+  static const bool no_stage = std::getenv("SPMMM_NO_STAGE") != nullptr;
+  if (bytes >= (size_t(8) << 20) && !no_stage && !host_pinned(src)) {
+    if (!c->stager) c->stager = new (std::nothrow) Stager;
+    if (!c->stager) return fail(SPMMM_ERR_OOM, "host allocation failed");
+    CUDA_TRY(c->stager->init());
+    const std::atomic<bool> no_abort{false};
+    CUDA_TRY(c->stager->copy(dst, src, bytes, c->stream, no_abort));
+    return SPMMM_OK;
+  }
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  return SPMMM_OK;
 }
 
 int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
