@@ -124,13 +124,18 @@ typedef struct {
   uint64_t h2d_bytes, d2h_bytes;  /* PCIe bytes this call moved each way */
 } spmmm_host_csr;
 
-/* C = A·B for HOST operands, block-pipelined: A's and B's structure go up
- * first and one count pass validates and sizes the product; then A's values go
- * up in `blocks` row blocks (<= 16) while each block is computed as soon as
- * the B rows it reads are resident, and its part of C streams down — uploads,
- * kernels and downloads overlap. Same bytes, errors and multiplication count
- * as spmmm_multiply + spmmm_product_download (kernels.py:302-332); row stats
- * are not available here (use spmmm_multiply). Replaces, like spmmm_multiply,
+/* C = A·B for HOST operands, block-pipelined: A goes up in `blocks` row
+ * blocks (<= 16) of about equal nnz — row pointers, columns, values — (for
+ * A != B all of B first); there is no global count pass: block j is computed
+ * as soon as the B rows it reads are resident (its own count validates it
+ * and sizes its part of C) and its part of C streams down while the next block
+ * computes — uploads, kernels and downloads overlap. Pageable operands go up
+ * through the library's page-locked staging (several host threads). The
+ * result is reserved at max(8 nnz(A), 2^20) entries of pooled page-locked
+ * memory; a product past that is redone in one shot into exact-size arrays.
+ * Same bytes, errors and multiplication count as spmmm_multiply +
+ * spmmm_product_download (kernels.py:302-332); row stats are not available
+ * here (use spmmm_multiply). Replaces, like spmmm_multiply,
  * sparsemm.kernels.multiply_rowmajor (kernels.py:302-332) for the drop-in. */
 int spmmm_multiply_host(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b, int strategy,
                         uint32_t flags, int blocks, spmmm_host_csr* out);

@@ -1,11 +1,13 @@
 // Host side of libspmmm.so: contexts, device memory, the launch sequence of
 // one C = A·B, and the C ABI declared in include/spmmm.h.
 //
-// One multiply (device-resident operands) is:
-//   memset(ctrl) -> k_count -> [D2H 64 B, sync]          (size C, pick the kernel)
-//   [k_collect -> k_long]            only when some row is too long for k_fused
-//   memset(C.row_ptr[0]) -> k_fused (cooperative, persistent)
-//   [D2H 8 B of C.row_ptr[rows], sync]                    (nnz(C) for the caller)
+// One multiply (device-resident operands) is either
+//   count-free (every row of C short by construction, aux_kernels.cuh k_prep):
+//     k_prep -> k_fused (its last warp reports to the host) -> [sync]
+//   or counted:
+//     memset(ctrl) -> k_count -> [read-back, sync]         (size C, pick the kernel)
+//     [k_collect -> ESC / long-row kernels]  only when some row is too long for k_fused
+//     k_fused (cooperative, persistent) [-> k_copy_long] -> [read-back, sync]
 // The reference does the same two steps host-side: estimate_nnz then one
 // reservation (kernels.py:314, formats.py:199-205), then the row loop.
 #include <cuda_runtime.h>
@@ -1229,15 +1231,19 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
 // ---- block-pipelined product of host operands (spmmm_multiply_host) ---------
 //
 // PCIe, not the kernels, bounds a product whose operands and result live on
-// the host (C2: 0.37 GB up, 0.91 GB down against ~1.5 ms of kernels). The
-// structure of A and B goes up first and one count pass sizes everything;
-// then A's values go up in G row blocks while block j is computed (as soon as
-// every B row it reads is resident) and block j's C streams down, so uploads,
-// kernels and downloads overlap (PCIe is full duplex). Each block is the
-// ordinary device product of a row block of A (rows are independent,
-// kernels.py:323-329); its row_ptr is shifted by the nnz before it on the
-// device and it lands at its offset in one result, so the bytes are those
-// of spmmm_multiply.
+// the host (C2: 0.37 GB up, 0.91 GB down against ~1.4 ms of kernels). A goes
+// up in G row blocks of about equal nnz — row pointers, columns, values —
+// (for A != B all of B first: any A row may read any B row); there is no
+// global count pass. Block j is computed as soon as every B row it reads is
+// resident (for C = A·A a small kernel on the upload stream finds the
+// block's largest column, which names the last row of B = A it reads), by
+// the ordinary device product of a row block of A (rows are independent,
+// kernels.py:323-329: its own count validates it and sizes its part of C),
+// and its part of C streams down while the next block computes, so uploads,
+// kernels and downloads overlap (PCIe is full duplex). Its row_ptr is
+// shifted by the nnz before it on the device and it lands at its offset in
+// one result, so the bytes are those of spmmm_multiply. Pageable operands go
+// up through page-locked staging on an uploader thread (Stager).
 
 constexpr int kPipeSplit = 64;
 

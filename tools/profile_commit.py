@@ -31,7 +31,8 @@ def full(rep, config, kernel, tag):
         except (KeyError, ValueError):
             return None
 
-    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+              "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     u = dict(zip(hdr, units))
     rd = num("dram__bytes_read.sum") * scale.get(u.get("dram__bytes_read.sum"), 1)
