@@ -315,10 +315,9 @@ def _replicate(arr: np.ndarray, rank: int, world: int, device, group,
     src = _to_tensor(arr)
     if nccl:
         buf = torch.empty(world * chunk, dtype=dtype, device=device)
-        mine = buf[rank * chunk:(rank + 1) * chunk]
+        mine = torch.empty(chunk, dtype=dtype, device=device)  # (the padding is never read)
         if hi > lo:
             mine[:hi - lo].copy_(src[lo:hi], non_blocking=True)
-        # in place: this rank's chunk is already in its slot
         dist.all_gather_into_tensor(buf, mine, group=group)
         return buf[:n]
     if device.type == "cuda":
