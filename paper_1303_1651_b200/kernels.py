@@ -48,10 +48,11 @@ _STRATEGY_IDS = {s.value: i for i, s in enumerate(StrategyKind)}
 # multiply_rowmajor without stats on operands of at least this many A entries
 # takes the block-pipelined host path (spmmm_multiply_host), in row blocks of
 # about PIPELINE_BLOCK_NNZ A entries (2..12 blocks). Below it the per-block
-# fixed costs (a count readback each) outweigh the overlap (C2 sweep: grid
-# 512, 1.3M entries, pipelined 2.2 ms vs one-shot ~1.6 ms).
-PIPELINE_MIN_NNZ = 1 << 22
-PIPELINE_BLOCK_NNZ = 1 << 20
+# fixed costs outweigh the overlap (tools/pipe_threshold.py, C2 sweep points,
+# pinned operands: 1.3M entries one-shot 1.59 ms vs pipelined >= 1.59; 2.6M
+# entries one-shot 3.09 vs 5 blocks 2.70; 5.2M entries 6.07 vs 10 blocks 4.68).
+PIPELINE_MIN_NNZ = 1 << 21
+PIPELINE_BLOCK_NNZ = 1 << 19
 
 
 def pipeline_blocks(nnz_a: int) -> int:

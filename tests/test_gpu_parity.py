@@ -446,7 +446,7 @@ def test_drop_in_pipelined_path_equals_stats_path():
 
 
 def test_pipelined_host_product_reservation_overflow(monkeypatch):
-    """The pipelined path reserves min(products, 8 nnz(A)) result entries; a
+    """The pipelined path reserves max(8 nnz(A), 2^20) result entries; a
     result past the reservation is redone in one shot — same bytes. Forced
     here with a tiny reservation (SPMMM_PIPE_CAP, read per call)."""
     monkeypatch.setenv("SPMMM_PIPE_CAP", "1000")
