@@ -1,6 +1,7 @@
 """Randomised parity stress: many seeded shapes and distributions through the
-drop-in (stats on and off, one-shot and pipelined paths) against the oracle,
-bit for bit. Usage: python tools/stress_parity.py SECONDS"""
+drop-in (stats on and off, one-shot and pipelined paths, count-free and
+counted, pageable operands through the staging) against the oracle, bit for
+bit. Usage: python tools/stress_parity.py SECONDS [SEED]"""
 import os
 import sys
 import time
@@ -46,7 +47,7 @@ def rand_csr(rng, rows, cols, lens, values):
 
 
 def case(rng):
-    kind = rng.choice(["uniform", "zipf", "wide", "dense", "narrow"])
+    kind = rng.choice(["uniform", "zipf", "wide", "dense", "narrow", "short", "shortcsr"])
     values = rng.choice(["uniform", "quantized", "zeros"])
     m = int(rng.integers(1, 20000))
     k = m if rng.random() < 0.3 else int(rng.integers(1, 20000))
@@ -65,6 +66,12 @@ def case(rng):
         n = int(rng.integers(1, 200))
         la = rng.integers(0, 60, m)
         lb = rng.integers(0, 60, k)
+    elif kind == "short":  # the count-free path, ELL flavour (rows <= 6 and <= 5 entries)
+        la = rng.integers(0, 7, m)
+        lb = rng.integers(0, 6, k)
+    elif kind == "shortcsr":  # the count-free path, CSR flavour (na * nb <= 32)
+        la = rng.integers(0, 5, m)
+        lb = rng.integers(0, 9, k)
     else:
         n = int(rng.integers(1, 3000))
         la = np.minimum(rng.zipf(1.7, m), 2000)
