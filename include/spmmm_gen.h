@@ -36,6 +36,17 @@ int spmmm_gen_fd(uint64_t grid, uint64_t* row_ptr, uint64_t* col_idx, double* va
 int spmmm_gen_fd3_size(uint64_t grid, uint64_t* rows, uint64_t* nnz);
 int spmmm_gen_fd3(uint64_t grid, uint64_t* row_ptr, uint64_t* col_idx, double* values);
 
+/* Device-side versions of the two stencil generators (gen_device.cu): the
+ * same bytes written straight into caller-owned DEVICE arrays (sizes from the
+ * *_size calls) on `stream` (a cudaStream_t, may be NULL); returns after the
+ * stream has finished them. 0 ok, 2 invalid argument, 3 CUDA error. The
+ * random families stay on the host: each is one sequential splitmix64 stream
+ * whose draws shift with every rejected duplicate (genmat.py:106-130). */
+int spmmm_gen_fd_device(uint64_t grid, uint64_t* row_ptr, uint64_t* col_idx, double* values,
+                        void* stream);
+int spmmm_gen_fd3_device(uint64_t grid, uint64_t* row_ptr, uint64_t* col_idx, double* values,
+                         void* stream);
+
 /* n x n, exactly k distinct uniform columns per row, values in (0,1]; nnz = n*k. */
 int spmmm_gen_random_k(uint64_t n, uint64_t k, uint64_t seed,
                        uint64_t* row_ptr, uint64_t* col_idx, double* values);

@@ -46,7 +46,8 @@ EXPORTS = (
     "spmmm_last_timings", "spmmm_last_launch_count",
     "spmmm_host_alloc", "spmmm_host_free", "spmmm_host_pool_bytes",
     "spmmm_splitmix64", "spmmm_gen_fd_size", "spmmm_gen_fd", "spmmm_gen_fd3_size",
-    "spmmm_gen_fd3", "spmmm_gen_random_k", "spmmm_gen_zipf",
+    "spmmm_gen_fd3", "spmmm_gen_random_k", "spmmm_gen_zipf", "spmmm_gen_fd_device",
+    "spmmm_gen_fd3_device",
     "spmmm_mtx_last_error", "spmmm_mtx_write", "spmmm_mtx_read", "spmmm_mtx_shape",
     "spmmm_mtx_copy", "spmmm_mtx_free",
 )
@@ -139,6 +140,8 @@ def _declare(lib):
         "spmmm_gen_fd3": (i, [c_u64, vp, vp, vp]),
         "spmmm_gen_random_k": (i, [c_u64, c_u64, c_u64, vp, vp, vp]),
         "spmmm_gen_zipf": (i, [c_u64, ctypes.c_double, c_u64, c_u64, p_u64, vp, vp, vp]),
+        "spmmm_gen_fd_device": (i, [c_u64, vp, vp, vp, vp]),
+        "spmmm_gen_fd3_device": (i, [c_u64, vp, vp, vp, vp]),
         "spmmm_mtx_last_error": (ctypes.c_char_p, []),
         "spmmm_mtx_write": (i, [ctypes.c_char_p, ctypes.POINTER(SpmmmCsr)]),
         "spmmm_mtx_read": (i, [ctypes.c_char_p, pp]),

@@ -81,6 +81,31 @@ def gen_zipf(n: int, seed: int, s: float = 2.0, lmax: int = 4096) -> CsrMatrix:
     return CsrMatrix(n, n, rp, ci, v)
 
 
+def gen_stencil_device(family: str, grid: int, device=None):
+    """The fd (5-point) or fd3 (27-point) stencil generated on the GPU
+    (spmmm_gen_fd_device / spmmm_gen_fd3_device): the bytes of gen_fd /
+    gen_fd3, written straight into HBM. Returns a device.DeviceCsr."""
+    import torch
+
+    from .device import DeviceCsr
+
+    lib = _lib.lib()
+    size_fn, fill_fn = {"fd": (lib.spmmm_gen_fd_size, lib.spmmm_gen_fd_device),
+                        "fd3": (lib.spmmm_gen_fd3_size, lib.spmmm_gen_fd3_device)}[family]
+    rows, nnz = ctypes.c_uint64(), ctypes.c_uint64()
+    _rc(size_fn(grid, ctypes.byref(rows), ctypes.byref(nnz)), "size")
+    device = torch.device(device or "cuda")
+    rp = torch.empty(rows.value + 1, dtype=torch.int64, device=device)
+    ci = torch.empty(max(nnz.value, 1), dtype=torch.int64, device=device)
+    v = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    rc = fill_fn(grid, rp.data_ptr(), ci.data_ptr(), v.data_ptr(), stream)
+    if rc == 3:
+        raise RuntimeError(f"gen_{family}_device: CUDA error")
+    _rc(rc, f"gen_{family}_device")
+    return DeviceCsr(rows.value, rows.value, rp, ci[:nnz.value], v[:nnz.value])
+
+
 def matrix_fingerprint(m) -> str:
     """genmat.py:154-165: sha256 over the canonical little-endian bytes."""
     h = hashlib.sha256()

@@ -544,3 +544,16 @@ def test_pipelined_mixed_u16_and_u32_blocks(no_delta):
         if os.environ.get("SPMMM_NO_DELTA16") is None:
             assert d2h < 4 * (a.rows + 1) + 12 * len(v), (blocks, d2h)
     ctx.close()
+
+
+@pytest.mark.parametrize("family,grids", [("fd", [1, 2, 3, 7, 64, 100, 1000]),
+                                          ("fd3", [1, 2, 3, 5, 17, 100])])
+def test_device_stencil_generators_match_host(family, grids):
+    """spmmm_gen_fd_device / spmmm_gen_fd3_device write the bytes of the host
+    generators (gen_fd restates the reference's genmat.py:79-103) into HBM."""
+    for g in grids:
+        host = genmat.gen_fd(g) if family == "fd" else genmat.gen_fd3(g)
+        dev = genmat.gen_stencil_device(family, g).to_host()
+        assert dev.row_ptr.tobytes() == np.asarray(host.row_ptr).tobytes(), (family, g)
+        assert dev.col_idx.tobytes() == np.asarray(host.col_idx).tobytes(), (family, g)
+        assert dev.values.tobytes() == np.asarray(host.values).tobytes(), (family, g)
