@@ -520,7 +520,8 @@ def run_distributed(args, rank, world, local_rank):
     ngpu = torch.cuda.device_count()
     backend = args.backend
     if backend == "nccl":
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the driver counts ranks in NCCL's log
+        # the driver counts ranks in NCCL's INFO log (the image may preset a quieter level)
+        os.environ["NCCL_DEBUG"] = "INFO"
         if world > ngpu:
             raise SystemExit(f"--gpus {world} needs {world} GPUs, this node has {ngpu} "
                              "(use --backend gloo to run oversubscribed ranks as a functional test)")
@@ -705,6 +706,8 @@ def main():
     ap.add_argument("--grid", type=int, default=None, help="another point of the stencil sweep")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="N > 1: NCCL (product); gloo runs oversubscribed ranks as a functional test")
+    ap.add_argument("--distributed", action="store_true",
+                    help="take the N-GPU path even at N = 1 (a one-rank NCCL run of its code)")
     ap.add_argument("--e2e-steps", type=int, default=7)
     ap.add_argument("--cpu-budget", type=float, default=8.0,
                     help="seconds of single-thread CPU work for cpu_baseline")
@@ -726,7 +729,7 @@ def main():
     local_rank = _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, rank, world)
-    if world > 1:
+    if world > 1 or args.distributed:
         return run_distributed(args, rank, world, local_rank)
     return run_single(args)
 

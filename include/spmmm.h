@@ -84,7 +84,9 @@ const char* spmmm_last_error(void);
 int spmmm_device_count(int* count);
 
 /* One context per (device, stream). cuda_stream may be NULL (the context
- * creates its own non-blocking stream) or a cudaStream_t owned by the caller. */
+ * creates its own non-blocking stream, unordered with the legacy default
+ * stream) or a cudaStream_t owned by the caller — cudaStreamLegacy (0x1)
+ * for the legacy default stream itself (torch's default stream). */
 int spmmm_context_create(int device, void* cuda_stream, spmmm_context** out);
 int spmmm_context_destroy(spmmm_context* ctx);
 int spmmm_synchronize(spmmm_context* ctx);

@@ -56,11 +56,18 @@ class DeviceCsr:
                          self.values[lo:hi].cpu().numpy().copy())
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream's handle
+
+
 def context_for_current_stream(device: torch.device) -> _lib.Context:
     """A libspmmm context bound to torch's current stream on `device`, so the
-    library's kernels are ordered with torch's copies and collectives."""
+    library's kernels are ordered with torch's copies and collectives. torch's
+    default stream has handle 0, which the C ABI reads as "make your own
+    stream" (one that does not wait for the default stream), so it is passed
+    as cudaStreamLegacy instead."""
     stream = torch.cuda.current_stream(device)
-    return _lib.Context(device.index if device.index is not None else 0, stream.cuda_stream)
+    handle = stream.cuda_stream or _CUDA_STREAM_LEGACY
+    return _lib.Context(device.index if device.index is not None else 0, handle)
 
 
 def multiply(ctx: _lib.Context, a: DeviceCsr, b: DeviceCsr, flags: int = 0,

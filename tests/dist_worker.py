@@ -122,8 +122,13 @@ def main():
     ap.add_argument("--stats", action="store_true")
     ap.add_argument("--expect", choices=["mismatch", "malformed"])
     ap.add_argument("--calls", type=int, default=1)
+    ap.add_argument("--backend", default="gloo", choices=["gloo", "nccl"])
     args = ap.parse_args()
-    dist.init_process_group("gloo")
+    if args.backend == "nccl":
+        torch.cuda.set_device(torch.device(args.device))
+        dist.init_process_group("nccl", device_id=torch.device(args.device))
+    else:
+        dist.init_process_group("gloo")
     rank = dist.get_rank()
     try:
         device = torch.device(args.device)

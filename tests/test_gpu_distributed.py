@@ -111,3 +111,40 @@ def test_full_size_two_ranks_match_reference_digests(label, config, tmp_path):
     assert d["digests"]["values"] == fp["c"]["values_sha256"]
     b = d["bounds"]
     assert b[0] == 0 and 0 < b[1] < b[2]
+
+
+@pytest.mark.parametrize("case", ["signed_k40", "long_rows", "empty_rows_mix"])
+def test_nccl_path_one_rank(case, tmp_path):
+    """The NCCL code path (chunked upload + all_gather_into_tensor, the gloo
+    control group beside it, the shared result) with the one rank a single
+    GPU allows: NCCL refuses two ranks on one device."""
+    out = str(tmp_path / "c.npz")
+    r = spawn(1, WORKER, ["--case", case, "--out", out, "--stats", "--calls", "2", "--device",
+                          "cuda:0", "--backend", "nccl"], timeout=600, capture=True)
+    assert r.returncode == 0, f"{r.stdout[-3000:]}\n{r.stderr[-6000:]}"
+    z = np.load(out)
+    _, _, c_ref, mults, choices = golden_case(case)
+    assert z["rp"].tobytes() == c_ref.row_ptr.tobytes()
+    assert z["ci"].tobytes() == c_ref.col_idx.tobytes()
+    assert z["v"].tobytes() == c_ref.values.tobytes()
+    assert int(z["mults"][0]) == mults and np.array_equal(z["choices"], choices)
+
+
+def test_bench_distributed_path_nccl_one_rank():
+    """bench.py's N-GPU path under torch.distributed.run with NCCL, one rank."""
+    import json
+    import subprocess
+    import sys
+
+    from paper_1303_1651_b200.launch import torchrun_argv
+
+    r = subprocess.run(torchrun_argv(1, os.path.join(ROOT, "bench.py"),
+                                     ["--distributed", "--config", "C3", "--steps", "3",
+                                      "--warmup", "3", "--e2e-steps", "2"]),
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and "nccl" in line["parallelism"]
+    assert line["e2e"]["value"] > 0 and line["b_allgather_ms"] > 0
+    assert sum(line["rank_products"]) == line["config"]["products"]
+    assert "NCCL INFO" in r.stdout + r.stderr  # NCCL_DEBUG=INFO stays on
