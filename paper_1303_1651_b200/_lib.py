@@ -280,14 +280,18 @@ def pinned_empty(n: int, dtype) -> np.ndarray:
 class Product:
     """Device-resident C returned by spmmm_multiply."""
 
+    _shape = threading.local()
+
     def __init__(self, ctx: Context, handle: ctypes.c_void_p):
         self.ctx = ctx
         self._h = handle
-        rows, cols, nnz, mults = (ctypes.c_uint64() for _ in range(4))
-        check(lib().spmmm_product_shape(handle, ctypes.byref(rows), ctypes.byref(cols),
-                                        ctypes.byref(nnz), ctypes.byref(mults)), "shape")
-        self.rows, self.cols, self.nnz, self.multiplications = (
-            rows.value, cols.value, nnz.value, mults.value)
+        # one reusable out-array per thread (this runs once per product)
+        vals = getattr(Product._shape, "vals", None)
+        if vals is None:
+            vals = Product._shape.vals = tuple(ctypes.c_uint64() for _ in range(4))
+            Product._shape.ptrs = tuple(ctypes.pointer(x) for x in vals)
+        check(lib().spmmm_product_shape(handle, *Product._shape.ptrs), "shape")
+        self.rows, self.cols, self.nnz, self.multiplications = (x.value for x in vals)
 
     def reserved_bytes(self) -> int:
         n = ctypes.c_uint64()

@@ -418,8 +418,11 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     n = __shfl_sync(kFull, n, 0);
     if (n + 1 == uint64_t(gridDim.x) * WARPS) {
       __threadfence();
-      if (int(lane) < p.ctrl_words)
+      if (int(lane) < p.ctrl_words) {
         reinterpret_cast<volatile unsigned long long*>(p.host_ctrl)[lane] = __ldcg(p.ctrl + lane);
+        // and leaves them zeroed for the next product (no memset before it)
+        __stcg(const_cast<unsigned long long*>(p.ctrl) + lane, 0ull);
+      }
     }
   }
 }

@@ -924,10 +924,8 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   // nnz, watchdog) to h_ctrl: the one host round trip
   e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cleanup(fail(SPMMM_ERR_CUDA, "multiply: %s", cudaGetErrorString(e)));
-  // zero ctrl for the next product now, behind this one (off its critical path)
-  if (cudaMemsetAsync(c->ctrl.p, 0, kCtrlWords * sizeof(unsigned long long), c->stream) ==
-      cudaSuccess)
-    c->ctrl_clean = true;
+  // the last warp also zeroed ctrl for the next product (no memset before it)
+  c->ctrl_clean = true;
   const unsigned long long* h = c->h_ctrl;
   if (!cf_applies(h[kCtrlCfFlags], h[kCtrlCfFlags + 1], h[kCtrlCfFlags + 2]) ||
       (h[kCtrlCfFlags] & kCfOverflow)) {
