@@ -37,6 +37,7 @@ enum Ctrl : int {
   kCtrlScrCursor = 25,  // k_esc_plan's scratch allocator (slots)
   kCtrlCfFlags = 26,    // count-free path: kCf* bits, then [27] longest A row, [28] longest B row
   kCtrlDone = 29,       // count-free path: k_fused warps finished (the last one reports)
+  kCtrlCfEll = 30,      // count-free path: B's referenced rows were packed into ELL records
   kCtrlWords = 32
 };
 
@@ -282,6 +283,13 @@ __host__ __device__ inline bool ell_wanted(const unsigned long long* w, uint64_t
 // path, which also yields the reference's exact error for bad input.
 // (CfFlags and cf_applies: rows.cuh, beside the ELL layout)
 
+// MODE 0, C = A·A (A square, its rows are B's rows): one pass over the rows
+// measures both and checks A's columns while packing them as B's records.
+// MODE 1, A spans most of B: A's rows and columns, then every B row (checked,
+// measured, packed). MODE 2, A a row block of a larger matrix: A only — its
+// rows, its columns against B.rows and their range [kmin, kmax] — and
+// k_prep_b takes the B rows in that range.
+template <int MODE>
 __global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
                                               unsigned long long* __restrict__ ctrl,
                                               unsigned long long* __restrict__ zero,
@@ -290,11 +298,8 @@ __global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
   const uint64_t t0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   for (uint64_t i = t0; i < nzero; i += stride) zero[i] = 0;
   unsigned f = 0;
-  unsigned long long ma = 0, mb = 0;
-  // C = A·A (A square, its rows are B's rows): one pass over the rows
-  // measures both and checks A's columns while packing them as B's records
-  const bool same = A.rp == B.rp && A.ci == B.ci && A.rows == B.rows && A.nnz == B.nnz;
-  if (!same) {
+  unsigned long long ma = 0, mb = 0, kmin = ~0ull, kmax1 = 0;
+  if (MODE != 0) {
     for (uint64_t r = t0; r < A.rows; r += stride) {
       const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
       if (hi < lo || hi > A.nnz) f |= kCfBadA;
@@ -304,24 +309,29 @@ __global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
     // coalesced over the entries of the rows' span
     uint64_t e0 = ld_idx(A.rp), e1 = ld_idx(A.rp + A.rows);
     e1 = e1 < A.nnz ? e1 : A.nnz;
-    for (uint64_t e = e0 + t0; e < e1; e += stride)
-      if (ld_idx(A.ci + e) >= B.rows) f |= kCfBadCol;
-  }
-  for (uint64_t r = t0; r < B.rows; r += stride) {
-    const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
-    if (hi < lo || hi > B.nnz) {
-      f |= kCfBadB;
-      continue;
+    for (uint64_t e = e0 + t0; e < e1; e += stride) {
+      const uint64_t k = ld_idx(A.ci + e);
+      if (k >= B.rows) f |= kCfBadCol;
+      if (MODE == 2) {
+        kmin = k < kmin ? k : kmin;
+        kmax1 = k + 1 > kmax1 ? k + 1 : kmax1;
+      }
     }
-    mb = hi - lo > mb ? hi - lo : mb;
-    if (same)
-      for (uint64_t e = lo; e < hi; ++e)
-        if (ld_idx(B.ci + e) >= B.rows) f |= kCfBadCol;  // (L1 hits: the record's loads)
-    if (ell) pack_ell_record(B, r, lo, hi, ell);  // (longer rows: truncated, never read)
   }
-  if (same) {
-    ma = mb;
-    f |= (f & kCfBadB) ? kCfBadA : 0u;
+  if (MODE != 2) {
+    for (uint64_t r = t0; r < B.rows; r += stride) {
+      const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+      if (hi < lo || hi > B.nnz) {
+        f |= MODE == 0 ? (kCfBadB | kCfBadA) : kCfBadB;
+        continue;
+      }
+      mb = hi - lo > mb ? hi - lo : mb;
+      if (MODE == 0)
+        for (uint64_t e = lo; e < hi; ++e)
+          if (ld_idx(B.ci + e) >= B.rows) f |= kCfBadCol;  // (L1 hits: the record's loads)
+      if (ell) pack_ell_record(B, r, lo, hi, ell);  // (longer rows: truncated, never read)
+    }
+    if (MODE == 0) ma = mb;
   }
   f = __reduce_or_sync(kFull, f);
 #pragma unroll
@@ -329,10 +339,54 @@ __global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
     const unsigned long long oa = __shfl_xor_sync(kFull, ma, d), ob = __shfl_xor_sync(kFull, mb, d);
     ma = oa > ma ? oa : ma;
     mb = ob > mb ? ob : mb;
+    if (MODE == 2) {
+      const unsigned long long o0 = __shfl_xor_sync(kFull, kmin, d);
+      const unsigned long long o1 = __shfl_xor_sync(kFull, kmax1, d);
+      kmin = o0 < kmin ? o0 : kmin;
+      kmax1 = o1 > kmax1 ? o1 : kmax1;
+    }
   }
   if (lane_id() == 0) {
     if (f) atomicOr(ctrl + kCtrlCfFlags, (unsigned long long)f);
     if (ma) atomicMax(ctrl + kCtrlCfFlags + 1, ma);
+    if (mb) atomicMax(ctrl + kCtrlCfFlags + 2, mb);
+    if (MODE == 2 && kmax1) {
+      atomicMax(ctrl + kCtrlKMinInv, ~kmin);
+      atomicMax(ctrl + kCtrlKMax1, kmax1);
+    }
+    if (MODE != 2 && ell && blockIdx.x == 0 && threadIdx.x == 0) ctrl[kCtrlCfEll] = 1;
+  }
+}
+
+// The B rows A references, [kmin, kmax] from k_prep: checked, measured and
+// (when A references most of them: at least 7/10 of the range, by A's entry
+// count) packed into ELL records — the counted path's rule (ell_wanted).
+// Rows outside the range are never read, like k_count leaves them unchecked.
+__global__ void __launch_bounds__(256) k_prep_b(DevCsr A, DevCsr B,
+                                                unsigned long long* __restrict__ ctrl,
+                                                uint4* __restrict__ ell) {
+  const uint64_t k0 = ~ctrl[kCtrlKMinInv], k1 = ctrl[kCtrlKMax1];
+  if (k1 <= k0) return;  // A has no entries
+  uint64_t e0 = ld_idx(A.rp), e1 = ld_idx(A.rp + A.rows);
+  e1 = e1 < A.nnz ? e1 : A.nnz;
+  const bool pack = ell != nullptr && e1 > e0 && 10 * (e1 - e0) >= 7 * (k1 - k0);
+  if (pack && blockIdx.x == 0 && threadIdx.x == 0) ctrl[kCtrlCfEll] = 1;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  unsigned f = 0;
+  unsigned long long mb = 0;
+  for (uint64_t r = k0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < k1; r += stride) {
+    const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+    if (hi < lo || hi > B.nnz) {
+      f |= kCfBadB;
+      continue;
+    }
+    mb = hi - lo > mb ? hi - lo : mb;
+    if (pack) pack_ell_record(B, r, lo, hi, ell);
+  }
+  f = __reduce_or_sync(kFull, f);
+  mb = __reduce_max_sync(kFull, uint32_t(mb > 0xffffffffull ? 0xffffffffull : mb));
+  if (lane_id() == 0) {
+    if (f) atomicOr(ctrl + kCtrlCfFlags, (unsigned long long)f);
     if (mb) atomicMax(ctrl + kCtrlCfFlags + 2, mb);
   }
 }

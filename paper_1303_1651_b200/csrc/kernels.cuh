@@ -50,6 +50,7 @@ struct FusedParams {
   // null, every row with entries is short, k_prep's verdict is read here and
   // the multiplications are summed into *cf_total
   const unsigned long long* cf_flags;
+  const unsigned long long* cf_ell_flag;  // B's ELL records were packed
   unsigned long long* cf_total;
   unsigned long long* cf_err;
   uint64_t c_cap;  // entries reserved for C (count-free and medium variants check it)
@@ -132,7 +133,10 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     const volatile unsigned long long* w = p.cf_flags;
     const unsigned long long ma = w[1], mb = w[2];
     run = cf_applies(w[0], ma, mb);
-    if (!cf_ell(ma, mb)) p.ell = nullptr;  // B rows past a record: read B as CSR
+    // B through its ELL records when k_prep(_b) packed them and every
+    // referenced row fits one; else as CSR
+    if (!cf_ell(ma, mb) || !*reinterpret_cast<const volatile unsigned long long*>(p.cf_ell_flag))
+      p.ell = nullptr;
   }
   uint64_t cf_prods = 0;
 

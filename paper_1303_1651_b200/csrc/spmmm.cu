@@ -839,9 +839,11 @@ bool cf_candidate(spmmm_context* c, const DevCsr& A, const DevCsr& B, const uint
 int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool stats, bool wide,
                         const uint64_t (&key)[5], Timer& tm, spmmm_product** out) {
   const uint64_t rows = A.rows;
-  // ELL flavour when A spans most of B (the pack covers all of B) and B's
-  // rows can fit records; else B is read as CSR
-  const bool use_ell = 2 * rows >= B.rows && B.nnz <= uint64_t(kEllSlots) * B.rows + B.rows / 8;
+  // B's rows may fit ELL records (on average they do); whether they all do,
+  // and whether A references enough of them to pay for the packing, is
+  // decided on the device (k_prep / k_prep_b)
+  const bool same = A.rp == B.rp && A.ci == B.ci && A.rows == B.rows && A.nnz == B.nnz;
+  const bool use_ell = B.nnz <= uint64_t(kEllSlots) * B.rows + B.rows / 8;
   CUDA_TRY(ensure_lookback(c, rows));
   if (use_ell) CUDA_TRY(ensure(c->ell, B.rows * 64, c->stream));
   if (!c->ctrl_clean)
@@ -850,12 +852,24 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   auto* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
   const uint64_t ncnt = lb_counters_max(rows);
   tm.begin(12);
-  k_prep<<<unsigned(std::min<uint64_t>((std::max(rows, B.rows) + 255) / 256, uint64_t(c->sms) * 8)),
-           256, 0, c->stream>>>(A, B, ctrl, static_cast<unsigned long long*>(c->status.p), ncnt,
-                                use_ell ? static_cast<uint4*>(c->ell.p) : nullptr);
+  uint4* ell = use_ell ? static_cast<uint4*>(c->ell.p) : nullptr;
+  // A spanning most of B: one pass packs all of B; a row block of A: its
+  // column range first, then only the B rows in it (k_prep_b)
+  const bool block = !same && 2 * rows < B.rows;
+  const unsigned pgrid = unsigned(std::min<uint64_t>((std::max(rows, B.rows) + 255) / 256,
+                                                     uint64_t(c->sms) * 8));
+  unsigned long long* zero = static_cast<unsigned long long*>(c->status.p);
+  if (same) k_prep<0><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, ell);
+  else if (!block) k_prep<1><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, ell);
+  else k_prep<2><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, nullptr);
   CUDA_TRY(cudaGetLastError());
-  tm.end(12);
   ++c->last_launches;
+  if (block) {  // the B rows A references
+    k_prep_b<<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, ell);
+    CUDA_TRY(cudaGetLastError());
+    ++c->last_launches;
+  }
+  tm.end(12);
 
   auto* p = new (std::nothrow) spmmm_product;
   if (!p) return fail(SPMMM_ERR_OOM, "host allocation failed");
@@ -898,11 +912,12 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   fp.ntiles = ntiles;
   fp.medium_limit = 0;
   fp.a_is_b = (A.ci == B.ci && A.v == B.v) ? 1u : 0u;
-  fp.ell = use_ell ? static_cast<const uint32_t*>(c->ell.p) : nullptr;
+  fp.ell = reinterpret_cast<const uint32_t*>(ell);
   fp.st_min = p->st;
   fp.st_max = p->st ? p->st + rows : nullptr;
   fp.st_touch = p->st ? p->st + 2 * rows : nullptr;
   fp.cf_flags = ctrl + kCtrlCfFlags;
+  fp.cf_ell_flag = ctrl + kCtrlCfEll;
   fp.cf_total = ctrl + kCtrlTotal;
   fp.cf_err = ctrl + kCtrlCfFlags;  // (kCfOverflow)
   fp.c_cap = cap;
