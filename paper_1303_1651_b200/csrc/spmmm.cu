@@ -773,6 +773,9 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
 // runs; those operands are then not tried again.
 
 constexpr int kCfFallback = -1;
+// internal multiply_impl flag: take the counted path (the pipelined host path's
+// blocks: measured faster there)
+constexpr uint32_t kFlagCounted = 1u << 30;
 
 uint64_t lookback_words(uint64_t rows) {
   uint64_t words = 0, n = rows;
@@ -993,7 +996,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
   const Trace tr;
   uint64_t key[5];
   cf_key(a, b, key);
-  if (cf_candidate(c, A, B, key)) {
+  if (!(flags & kFlagCounted) && cf_candidate(c, A, B, key)) {
     const bool wide_s = B.cols > (1ull << 27) || B.nnz >= (1ull << 32) || A.nnz >= (1ull << 32) ||
                         B.rows >= (1ull << 32);
     rc = multiply_count_free(c, A, B, stats, wide_s, key, tm, out);
@@ -1918,7 +1921,9 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
     if (!same) CUDA_TRY(cudaStreamWaitEvent(c->stream, *ev_bv, 0));
     spmmm_csr va{r1 - r0, a->cols, a->nnz, d_arp + r0, d_aci, d_av, SPMMM_MEM_DEVICE, 0};
     spmmm_csr vb{B.rows, B.cols, B.nnz, B.rp, B.ci, B.v, SPMMM_MEM_DEVICE, 0};
-    rc = multiply_impl(c, &va, &vb, strategy, flags & SPMMM_FLAG_TIMING, &prods[j]);
+    static const bool cf_blocks = std::getenv("SPMMM_PIPE_COUNT_FREE") != nullptr;
+    rc = multiply_impl(c, &va, &vb, strategy,
+                       (flags & SPMMM_FLAG_TIMING) | (cf_blocks ? 0u : kFlagCounted), &prods[j]);
     if (rc) return rc;  // (the guard cleans up)
     spmmm_product* p = prods[j];
     if (off + p->nnz > cap) {
@@ -2192,7 +2197,7 @@ int spmmm_multiply(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int
                    uint32_t flags, spmmm_product** out) {
   if (!c) return fail(SPMMM_ERR_INVALID, "context is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
-  return multiply_impl(c, a, b, strategy, flags, out);
+  return multiply_impl(c, a, b, strategy, flags & (SPMMM_FLAG_ROW_STATS | SPMMM_FLAG_TIMING), out);
 }
 
 int spmmm_multiply_host(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int strategy,
