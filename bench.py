@@ -520,8 +520,11 @@ def run_distributed(args, rank, world, local_rank):
     ngpu = torch.cuda.device_count()
     backend = args.backend
     if backend == "nccl":
-        # the driver counts ranks in NCCL's INFO log (the image may preset a quieter level)
+        # the driver counts ranks in NCCL's INFO log (the image may preset a
+        # quieter level); NCCL logs to stdout by default, where rank 0's one
+        # JSON line goes: send the log to stderr
         os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if world > ngpu:
             raise SystemExit(f"--gpus {world} needs {world} GPUs, this node has {ngpu} "
                              "(use --backend gloo to run oversubscribed ranks as a functional test)")

@@ -143,8 +143,10 @@ def test_bench_distributed_path_nccl_one_rank():
                                       "--warmup", "3", "--e2e-steps", "2"]),
                        cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-4000:]
-    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    # stdout is rank 0's one JSON line (NCCL's log goes to stderr)
+    assert len(r.stdout.strip().splitlines()) == 1, r.stdout[:2000]
+    line = json.loads(r.stdout)
     assert line["n_gpus"] == 1 and line["value"] > 0 and "nccl" in line["parallelism"]
     assert line["e2e"]["value"] > 0 and line["b_allgather_ms"] > 0
     assert sum(line["rank_products"]) == line["config"]["products"]
-    assert "NCCL INFO" in r.stdout + r.stderr  # NCCL_DEBUG=INFO stays on
+    assert "NCCL INFO" in r.stderr  # NCCL_DEBUG=INFO stays on

@@ -26,3 +26,9 @@ for spec in ${PROFILE:-C2:k_fused C2:k_prep C3:k_fused C4:k_fused C5:k_esc_block
   timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:$k \
       -s 3 -c 1 -o $OUT/${TAG}_${c}_$k -f $CMD > $OUT/ncu_full_${c}_$k.log 2>&1; echo "full $c $k rc=$?"
 done
+# the N > 1 path: one rank over NCCL (torchrun), and two ranks sharing the GPU over gloo
+timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=1 --master-addr=127.0.0.1 \
+   --master-port=29561 bench.py --distributed --config C2 --steps 20 --warmup 5 \
+   > $OUT/bench_${TAG}_dist1_nccl.json 2> $OUT/bench_${TAG}_dist1_nccl.err; echo "dist1 nccl rc=$?"
+timeout -s KILL 900 python bench.py --gpus 2 --backend gloo --config C2 --steps 20 --warmup 5 \
+   > $OUT/bench_${TAG}_dist2_gloo.json 2> $OUT/bench_${TAG}_dist2_gloo.err; echo "dist2 gloo rc=$?"
