@@ -514,47 +514,70 @@ def multiply_distributed(a, b, strategy="combined", stats=None, *, group=None, d
     total_nnz = int(offsets[-1])
     mults = sum(w[2] for w in words)
 
-    # 6. the result in the shared arena; each rank downloads its slice
-    key = ctrl
-    arena = _arenas.setdefault(key, _Arena())
+    # 6. the result in the shared arena; each rank downloads its slice. Every
+    # step that can fail on one rank is followed by a status exchange, so all
+    # ranks raise together instead of leaving the others in a collective.
+    arena = _arenas.setdefault(ctrl, _Arena())
     sizes = [8 * (a.rows + 1), 8 * total_nnz, 8 * total_nnz]
-    meta = [None]
+    plan, new_seg = None, None
     if rank == root:
-        got = arena.alloc(sizes)
-        grow = None
-        if got is None:
-            cur = arena.seg.size if arena.seg is not None else 0
-            want = max(2 * sum(_align(s) for s in sizes) + (1 << 20), cur + cur // 2)
-            grow = (_new_name(), want, arena.gen + 1)
-        meta = [(grow, got)]
-    dist.broadcast_object_list(meta, src=_global_rank(ctrl, root), group=ctrl)
-    grow, got = meta[0]
-    if grow is not None:
-        name, size, gen = grow
-        seg = SharedSegment(name, size, create=(rank == root))
-        dist.barrier(group=ctrl)
-        if rank == root:
-            seg.unlink()
-        if device.type == "cuda":
-            seg.register()
-        arena.install(gen, seg, rank == root)
-        if rank == root:
+        try:
             got = arena.alloc(sizes)
-        got = _bcast(ctrl, root, got)
+            if got is not None:
+                plan = ("fit", got)
+            else:
+                cur = arena.seg.size if arena.seg is not None else 0
+                want = max(2 * sum(_align(s) for s in sizes) + (1 << 20), cur + cur // 2)
+                new_seg = SharedSegment(_new_name(), want, create=True)
+                plan = ("grow", new_seg.name, new_seg.size, arena.gen + 1)
+        except OSError as e:
+            plan = ("error", f"result arena: {e}")
+    plan = _bcast(ctrl, root, plan)
+    if plan[0] == "error":
+        blk.close()
+        raise RuntimeError(plan[1])
+    if plan[0] == "grow":
+        _, name, size, gen = plan
+        err = None
+        try:
+            seg = new_seg if rank == root else SharedSegment(name, size, create=False)
+            if device.type == "cuda":
+                seg.register()
+        except (OSError, RuntimeError) as e:
+            err = e
+        failed = any(w[0] for w in _exchange_status(ctrl, [0 if err is None else 1]))
+        if rank == root:
+            new_seg.unlink()  # every rank has mapped it (or given up)
+        if failed:
+            blk.close()
+            _raise_collective(ctrl, err)
+        arena.install(gen, seg, rank == root)
+        got = _bcast(ctrl, root, arena.alloc(sizes) if rank == root else None)
+    else:
+        got = plan[1]
     offs, need = got
     seg, gen = arena.seg, arena.gen
     r0, r1 = bounds[rank], bounds[rank + 1]
     base = seg.addr
-    blk.download(int(offsets[rank]), base + offs[0] + 8 * r0, base + offs[1] + 8 * int(offsets[rank]),
-                 base + offs[2] + 8 * int(offsets[rank]))
+    err = None
+    try:
+        blk.download(int(offsets[rank]), base + offs[0] + 8 * r0,
+                     base + offs[1] + 8 * int(offsets[rank]),
+                     base + offs[2] + 8 * int(offsets[rank]))
+    except RuntimeError as e:
+        err = e
     mine = blk.choices or []
     blk.close()
+    # every slice has landed (this exchange is the barrier)
+    if any(w[0] for w in _exchange_status(ctrl, [0 if err is None else 1])):
+        if rank == root:
+            arena.release(gen, offs[0], need)
+        _raise_collective(ctrl, err)
     choices = None
     if stats is not None:
         gathered = [None] * world
         dist.all_gather_object(gathered, mine, group=ctrl)
         choices = [c for part in gathered for c in part]
-    dist.barrier(group=ctrl)  # every slice has landed
     t3 = time.perf_counter()
     if timings is not None:
         timings.update(replicate_ms=1e3 * (t1 - t0), compute_ms=1e3 * (t2 - t1),
