@@ -45,27 +45,6 @@ enum Ctrl : int {
 // (esc.cuh); k_count sums their products for the host
 constexpr uint32_t kHugeMin = 5120;
 
-// One ELL record: u32 col[6] (unused 0xffffffff) then f64 val[5] — B row r's
-// entries [lo, hi) (at most kEllSlots are stored).
-__device__ __forceinline__ void pack_ell_record(const DevCsr& B, uint64_t r, uint64_t lo,
-                                                uint64_t hi, uint4* __restrict__ ell) {
-  uint32_t c[kEllSlots + 1];
-  double v[kEllSlots];
-#pragma unroll
-  for (int j = 0; j < kEllSlots; ++j) {
-    const bool in = lo + j < hi;
-    c[j] = in ? uint32_t(ld_idx(B.ci + lo + j)) : kEmptyKey;
-    v[j] = in ? ld_val(B.v + lo + j) : 0.0;
-  }
-  c[kEllSlots] = kEmptyKey;
-  auto lo32 = [](double x) { return uint32_t(__double_as_longlong(x)); };
-  auto hi32 = [](double x) { return uint32_t(uint64_t(__double_as_longlong(x)) >> 32); };
-  uint4* rec = ell + r * 4;
-  rec[0] = make_uint4(c[0], c[1], c[2], c[3]);
-  rec[1] = make_uint4(c[4], c[5], lo32(v[0]), hi32(v[0]));
-  rec[2] = make_uint4(lo32(v[1]), hi32(v[1]), lo32(v[2]), hi32(v[2]));
-  rec[3] = make_uint4(lo32(v[3]), hi32(v[3]), lo32(v[4]), hi32(v[4]));
-}
 
 // ---------------------------------------------------------------------------
 // K1: per-row product counts. formats.py:276-289 per row. A warp takes 32
@@ -283,79 +262,16 @@ __host__ __device__ inline bool ell_wanted(const unsigned long long* w, uint64_t
 // path, which also yields the reference's exact error for bad input.
 // (CfFlags and cf_applies: rows.cuh, beside the ELL layout)
 
-// MODE 0, C = A·A (A square, its rows are B's rows): one pass over the rows
-// measures both and checks A's columns while packing them as B's records.
-// MODE 1, A spans most of B: A's rows and columns, then every B row (checked,
-// measured, packed). MODE 2, A a row block of a larger matrix: A only — its
-// rows, its columns against B.rows and their range [kmin, kmax] — and
-// k_prep_b takes the B rows in that range.
+// The count-free path's first pass (prep_pass in rows.cuh) as a kernel of its
+// own; small products run it inside k_fused instead (PREP instantiations).
 template <int MODE>
 __global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
                                               unsigned long long* __restrict__ ctrl,
                                               unsigned long long* __restrict__ zero,
                                               uint64_t nzero, uint4* __restrict__ ell) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t t0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (uint64_t i = t0; i < nzero; i += stride) zero[i] = 0;
-  unsigned f = 0;
-  unsigned long long ma = 0, mb = 0, kmin = ~0ull, kmax1 = 0;
-  if (MODE != 0) {
-    for (uint64_t r = t0; r < A.rows; r += stride) {
-      const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
-      if (hi < lo || hi > A.nnz) f |= kCfBadA;
-      else ma = hi - lo > ma ? hi - lo : ma;
-    }
-    // every column of A's rows must name a row of B (k_fused trusts them);
-    // coalesced over the entries of the rows' span
-    uint64_t e0 = ld_idx(A.rp), e1 = ld_idx(A.rp + A.rows);
-    e1 = e1 < A.nnz ? e1 : A.nnz;
-    for (uint64_t e = e0 + t0; e < e1; e += stride) {
-      const uint64_t k = ld_idx(A.ci + e);
-      if (k >= B.rows) f |= kCfBadCol;
-      if (MODE == 2) {
-        kmin = k < kmin ? k : kmin;
-        kmax1 = k + 1 > kmax1 ? k + 1 : kmax1;
-      }
-    }
-  }
-  if (MODE != 2) {
-    for (uint64_t r = t0; r < B.rows; r += stride) {
-      const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
-      if (hi < lo || hi > B.nnz) {
-        f |= MODE == 0 ? (kCfBadB | kCfBadA) : kCfBadB;
-        continue;
-      }
-      mb = hi - lo > mb ? hi - lo : mb;
-      if (MODE == 0)
-        for (uint64_t e = lo; e < hi; ++e)
-          if (ld_idx(B.ci + e) >= B.rows) f |= kCfBadCol;  // (L1 hits: the record's loads)
-      if (ell) pack_ell_record(B, r, lo, hi, ell);  // (longer rows: truncated, never read)
-    }
-    if (MODE == 0) ma = mb;
-  }
-  f = __reduce_or_sync(kFull, f);
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    const unsigned long long oa = __shfl_xor_sync(kFull, ma, d), ob = __shfl_xor_sync(kFull, mb, d);
-    ma = oa > ma ? oa : ma;
-    mb = ob > mb ? ob : mb;
-    if (MODE == 2) {
-      const unsigned long long o0 = __shfl_xor_sync(kFull, kmin, d);
-      const unsigned long long o1 = __shfl_xor_sync(kFull, kmax1, d);
-      kmin = o0 < kmin ? o0 : kmin;
-      kmax1 = o1 > kmax1 ? o1 : kmax1;
-    }
-  }
-  if (lane_id() == 0) {
-    if (f) atomicOr(ctrl + kCtrlCfFlags, (unsigned long long)f);
-    if (ma) atomicMax(ctrl + kCtrlCfFlags + 1, ma);
-    if (mb) atomicMax(ctrl + kCtrlCfFlags + 2, mb);
-    if (MODE == 2 && kmax1) {
-      atomicMax(ctrl + kCtrlKMinInv, ~kmin);
-      atomicMax(ctrl + kCtrlKMax1, kmax1);
-    }
-    if (MODE != 2 && ell && blockIdx.x == 0 && threadIdx.x == 0) ctrl[kCtrlCfEll] = 1;
-  }
+  const CfWords w{ctrl + kCtrlCfFlags, ctrl + kCtrlKMinInv, ctrl + kCtrlKMax1, ctrl + kCtrlCfEll};
+  prep_pass<MODE>(A, B, w, zero, nzero, ell, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x,
+                  uint64_t(gridDim.x) * blockDim.x);
 }
 
 // The B rows A references, [kmin, kmax] from k_prep: checked, measured and

@@ -24,7 +24,7 @@ struct FusedLaunchEnv {
   cudaStream_t stream;
 };
 
-template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false>
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0>
 struct FusedVariant {
   static constexpr size_t smem() {
     return FusedSmem<R, MEDIUM>::bytes(WARPS);
@@ -34,7 +34,7 @@ struct FusedVariant {
     static int cache[64] = {};
     int& c = cache[device & 63];
     if (c == 0) {
-      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF>;
+      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(smem()));
       if (e != cudaSuccess) return e;
@@ -50,7 +50,7 @@ struct FusedVariant {
     FusedParams prm = prm_in;
     void* args[] = {&prm};
     return cudaLaunchCooperativeKernel(
-        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF>), dim3(grid),
+        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP>), dim3(grid),
         dim3(WARPS * 32), args, smem(), env.stream);
   }
 };
@@ -60,16 +60,17 @@ cudaError_t fused_short(int op, const FusedParams& prm, const FusedLaunchEnv& en
                         bool stats, unsigned grid, int* occ);
 cudaError_t fused_medium(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                          bool stats, unsigned grid, int* occ);
-// the count-free short variant (fused_cf.cu)
+// the count-free short variant (fused_cf.cu); prep 1 / 2: with the prep pass
+// of mode 0 / 1 inside (small products)
 cudaError_t fused_cf(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
-                     bool stats, unsigned grid, int* occ);
+                     bool stats, unsigned grid, int* occ, int prep);
 
-template <int WARPS, int R, bool MEDIUM, bool CF = false>
+template <int WARPS, int R, bool MEDIUM, bool CF = false, int PREP = 0>
 cudaError_t fused_dispatch(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                            bool stats, unsigned grid, int* occ) {
 #define SPMMM_FUSED_CASE(W, S)                                                  \
   if (wide == W && stats == S) {                                                \
-    using V = FusedVariant<WARPS, R, MEDIUM, W, S, CF>;                         \
+    using V = FusedVariant<WARPS, R, MEDIUM, W, S, CF, PREP>;                   \
     return op == 0 ? V::occupancy(env.device, occ) : V::launch(prm, env, grid); \
   }
   SPMMM_FUSED_CASE(false, false)

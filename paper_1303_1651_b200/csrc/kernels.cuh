@@ -16,6 +16,8 @@
 // look-back cannot deadlock.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "rows.cuh"
 
 #ifndef SPMMM_SHORT_BLOCKS
@@ -60,6 +62,12 @@ struct FusedParams {
   unsigned long long* host_ctrl;
   unsigned long long* done;
   int ctrl_words;
+  // PREP instantiations (small count-free products): the prep pass runs in
+  // this kernel, before a grid barrier, instead of as k_prep
+  CfWords cf_words;
+  unsigned long long* cf_zero;
+  uint64_t cf_nzero;
+  uint4* cf_pack;
 };
 
 // Warps take tiles dynamically, a batch of kBatch consecutive tiles per
@@ -89,10 +97,20 @@ struct FusedSmem {
   }
 };
 
-template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false>
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0>
 __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k_fused(const FusedParams p_in) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(!(MEDIUM && CF), "the count-free path is short rows only");
+  static_assert(PREP == 0 || CF, "the fused prep pass belongs to the count-free path");
+  if constexpr (PREP != 0) {
+    // the prep pass (mode PREP - 1) by every thread of the grid, then a grid
+    // barrier: its verdict, maxima and ELL records are complete below
+    prep_pass<PREP - 1>(p_in.A, p_in.B, p_in.cf_words, p_in.cf_zero, p_in.cf_nzero, p_in.cf_pack,
+                        uint64_t(blockIdx.x) * blockDim.x + threadIdx.x,
+                        uint64_t(gridDim.x) * blockDim.x);
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+  }
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   using SM = FusedSmem<R, MEDIUM>;

@@ -36,6 +36,28 @@ constexpr int kEllWords = 16;   // 64 B per record
 constexpr int kEllValOff = 6;   // values start after 6 column words (byte 24)
 constexpr uint32_t kEllEntries = 32 / kEllSlots;  // 6
 
+// One ELL record: u32 col[6] (unused 0xffffffff) then f64 val[5] — B row r's
+// entries [lo, hi) (at most kEllSlots are stored).
+__device__ __forceinline__ void pack_ell_record(const DevCsr& B, uint64_t r, uint64_t lo,
+                                                uint64_t hi, uint4* __restrict__ ell) {
+  uint32_t c[kEllSlots + 1];
+  double v[kEllSlots];
+#pragma unroll
+  for (int j = 0; j < kEllSlots; ++j) {
+    const bool in = lo + j < hi;
+    c[j] = in ? uint32_t(ld_idx(B.ci + lo + j)) : kEmptyKey;
+    v[j] = in ? ld_val(B.v + lo + j) : 0.0;
+  }
+  c[kEllSlots] = kEmptyKey;
+  auto lo32 = [](double x) { return uint32_t(__double_as_longlong(x)); };
+  auto hi32 = [](double x) { return uint32_t(uint64_t(__double_as_longlong(x)) >> 32); };
+  uint4* rec = ell + r * 4;
+  rec[0] = make_uint4(c[0], c[1], c[2], c[3]);
+  rec[1] = make_uint4(c[4], c[5], lo32(v[0]), hi32(v[0]));
+  rec[2] = make_uint4(lo32(v[1]), hi32(v[1]), lo32(v[2]), hi32(v[2]));
+  rec[3] = make_uint4(lo32(v[3]), hi32(v[3]), lo32(v[4]), hi32(v[4]));
+}
+
 // The count-free path's verdict (k_prep in aux_kernels.cuh measures the rows).
 enum CfFlags : unsigned {
   kCfBadA = 1,      // A.row_ptr decreasing or past nnz
@@ -55,6 +77,88 @@ __host__ __device__ inline bool cf_applies(unsigned long long flags, unsigned lo
 __host__ __device__ inline bool cf_ell(unsigned long long max_a, unsigned long long max_b) {
   return max_a <= uint64_t(kEllEntries) && max_b <= uint64_t(kEllSlots);
 }
+
+// The count-free path's first pass. MODE 0, C = A·A (A square, its rows are
+// B's rows): one pass over the rows measures both and checks A's columns
+// while packing them as B's records. MODE 1, A spans most of B: A's rows and
+// columns, then every B row (checked, measured, packed). MODE 2, A a row
+// block of a larger matrix: A only — its rows, its columns against B.rows and
+// their range [kmin, kmax] — and k_prep_b takes the B rows in that range.
+// Runs as k_prep (aux_kernels.cuh) or as the prologue of k_fused (small
+// products). Also zeroes the look-back counters.
+struct CfWords {
+  unsigned long long* flags;     // [0] kCf* bits, [1] longest A row, [2] longest B row
+  unsigned long long* kmin_inv;  // ~(smallest column of A) (MODE 2)
+  unsigned long long* kmax1;     // largest column of A + 1 (MODE 2)
+  unsigned long long* ell;       // B's ELL records were packed
+};
+
+template <int MODE>
+__device__ __forceinline__ void prep_pass(const DevCsr& A, const DevCsr& B, const CfWords& w,
+                                          unsigned long long* __restrict__ zero, uint64_t nzero,
+                                          uint4* __restrict__ ell, uint64_t t0, uint64_t stride) {
+  for (uint64_t i = t0; i < nzero; i += stride) zero[i] = 0;
+  unsigned f = 0;
+  unsigned long long ma = 0, mb = 0, kmin = ~0ull, kmax1 = 0;
+  if (MODE != 0) {
+    for (uint64_t r = t0; r < A.rows; r += stride) {
+      const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
+      if (hi < lo || hi > A.nnz) f |= kCfBadA;
+      else ma = hi - lo > ma ? hi - lo : ma;
+    }
+    // every column of A's rows must name a row of B (k_fused trusts them);
+    // coalesced over the entries of the rows' span
+    uint64_t e0 = ld_idx(A.rp), e1 = ld_idx(A.rp + A.rows);
+    e1 = e1 < A.nnz ? e1 : A.nnz;
+    for (uint64_t e = e0 + t0; e < e1; e += stride) {
+      const uint64_t k = ld_idx(A.ci + e);
+      if (k >= B.rows) f |= kCfBadCol;
+      if (MODE == 2) {
+        kmin = k < kmin ? k : kmin;
+        kmax1 = k + 1 > kmax1 ? k + 1 : kmax1;
+      }
+    }
+  }
+  if (MODE != 2) {
+    for (uint64_t r = t0; r < B.rows; r += stride) {
+      const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+      if (hi < lo || hi > B.nnz) {
+        f |= MODE == 0 ? (kCfBadB | kCfBadA) : kCfBadB;
+        continue;
+      }
+      mb = hi - lo > mb ? hi - lo : mb;
+      if (MODE == 0)
+        for (uint64_t e = lo; e < hi; ++e)
+          if (ld_idx(B.ci + e) >= B.rows) f |= kCfBadCol;  // (L1 hits: the record's loads)
+      if (ell) pack_ell_record(B, r, lo, hi, ell);  // (longer rows: truncated, never read)
+    }
+    if (MODE == 0) ma = mb;
+  }
+  f = __reduce_or_sync(kFull, f);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long oa = __shfl_xor_sync(kFull, ma, d), ob = __shfl_xor_sync(kFull, mb, d);
+    ma = oa > ma ? oa : ma;
+    mb = ob > mb ? ob : mb;
+    if (MODE == 2) {
+      const unsigned long long o0 = __shfl_xor_sync(kFull, kmin, d);
+      const unsigned long long o1 = __shfl_xor_sync(kFull, kmax1, d);
+      kmin = o0 < kmin ? o0 : kmin;
+      kmax1 = o1 > kmax1 ? o1 : kmax1;
+    }
+  }
+  if (lane_id() == 0) {
+    if (f) atomicOr(w.flags, (unsigned long long)f);
+    if (ma) atomicMax(w.flags + 1, ma);
+    if (mb) atomicMax(w.flags + 2, mb);
+    if (MODE == 2 && kmax1) {
+      atomicMax(w.kmin_inv, ~kmin);
+      atomicMax(w.kmax1, kmax1);
+    }
+    if (MODE != 2 && ell && t0 == 0) *w.ell = 1;
+  }
+}
+
 
 
 template <int R, bool WIDE, bool STATS, bool ELLOK, bool CF = false>

@@ -406,9 +406,9 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
 // ---- fused-kernel launch: instantiations live in fused_short.cu / fused_medium.cu ----
 
 int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bool wide,
-               bool stats, unsigned grid, int* occ, bool count_free = false) {
+               bool stats, unsigned grid, int* occ, bool count_free = false, int prep = 0) {
   FusedLaunchEnv env{c->device, c->sms, c->stream};
-  cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ)
+  cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ, prep)
                   : medium   ? fused_medium(op, prm, env, wide, stats, grid, occ)
                              : fused_short(op, prm, env, wide, stats, grid, occ);
   if (e != cudaSuccess)
@@ -773,6 +773,10 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
 // runs; those operands are then not tried again.
 
 constexpr int kCfFallback = -1;
+// count-free products up to this many rows (of A and B) run the prep pass
+// inside k_fused (SPMMM_PREP_FUSED_ROWS overrides)
+// (C1 40.5 -> 38.4 us; at 65K rows the separate, wider k_prep is faster)
+constexpr uint64_t kPrepFusedRows = 1u << 14;
 // internal multiply_impl flag: take the counted path (the pipelined host path's
 // blocks: measured faster there)
 constexpr uint32_t kFlagCounted = 1u << 30;
@@ -854,7 +858,6 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   c->ctrl_clean = false;
   auto* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
   const uint64_t ncnt = lb_counters_max(rows);
-  tm.begin(12);
   uint4* ell = use_ell ? static_cast<uint4*>(c->ell.p) : nullptr;
   // A spanning most of B: one pass packs all of B; a row block of A: its
   // column range first, then only the B rows in it (k_prep_b)
@@ -862,17 +865,31 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   const unsigned pgrid = unsigned(std::min<uint64_t>((std::max(rows, B.rows) + 255) / 256,
                                                      uint64_t(c->sms) * 8));
   unsigned long long* zero = static_cast<unsigned long long*>(c->status.p);
-  if (same) k_prep<0><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, ell);
-  else if (!block) k_prep<1><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, ell);
-  else k_prep<2><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, nullptr);
-  CUDA_TRY(cudaGetLastError());
-  ++c->last_launches;
+  // small products: the prep pass inside k_fused (one launch, a grid barrier)
+  static const uint64_t prep_rows = std::getenv("SPMMM_PREP_FUSED_ROWS")
+                                        ? std::strtoull(std::getenv("SPMMM_PREP_FUSED_ROWS"), nullptr, 10)
+                                        : kPrepFusedRows;
+  const int prep = (!block && std::max(rows, B.rows) <= prep_rows) ? (same ? 1 : 2) : 0;
+  if (!prep) tm.begin(12);
+  if (prep) {
+    // (launched with k_fused below)
+  } else if (same) {
+    k_prep<0><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, ell);
+  } else if (!block) {
+    k_prep<1><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, ell);
+  } else {
+    k_prep<2><<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, zero, ncnt, nullptr);
+  }
+  if (!prep) {
+    CUDA_TRY(cudaGetLastError());
+    ++c->last_launches;
+  }
   if (block) {  // the B rows A references
     k_prep_b<<<pgrid, 256, 0, c->stream>>>(A, B, ctrl, ell);
     CUDA_TRY(cudaGetLastError());
     ++c->last_launches;
   }
-  tm.end(12);
+  if (!prep) tm.end(12);
 
   auto* p = new (std::nothrow) spmmm_product;
   if (!p) return fail(SPMMM_ERR_OOM, "host allocation failed");
@@ -928,13 +945,17 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   fp.host_ctrl = c->h_ctrl;
   fp.done = ctrl + kCtrlDone;
   fp.ctrl_words = kCtrlWords;
+  fp.cf_words = CfWords{ctrl + kCtrlCfFlags, ctrl + kCtrlKMinInv, ctrl + kCtrlKMax1, ctrl + kCtrlCfEll};
+  fp.cf_zero = zero;
+  fp.cf_nzero = ncnt;
+  fp.cf_pack = ell;
   int occ = 0;
-  int rc = fused_call(c, false, 0, fp, wide, stats, 0, &occ, true);
+  int rc = fused_call(c, false, 0, fp, wide, stats, 0, &occ, true, prep);
   if (rc) return cleanup(rc);
   const unsigned grid = unsigned(std::min<uint64_t>((ntiles + kFusedWarps - 1) / kFusedWarps,
                                                     uint64_t(occ) * uint64_t(c->sms)));
   tm.begin(3);
-  rc = fused_call(c, false, 1, fp, wide, stats, grid, nullptr, true);
+  rc = fused_call(c, false, 1, fp, wide, stats, grid, nullptr, true, prep);
   if (rc) return cleanup(rc);
   tm.end(3);
   ++c->last_launches;

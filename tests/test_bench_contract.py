@@ -52,7 +52,7 @@ def test_our_arm_line():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert d["gpu_launches"] >= 2 * d["steps"]
+    assert d["gpu_launches"] >= d["steps"]  # (C1: one count-free k_fused per product)
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     cb = d["cpu_baseline"]
     assert cb["cores"] == 1 and cb["value"] > 0 and cb["kind"] == "port"

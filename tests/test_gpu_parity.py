@@ -212,9 +212,9 @@ def test_device_api_and_timings():
         rp, ci, v = p.download()
         assert p.multiplications == 100104
         t = ctx.last_timings()
-        assert ("k_count" in t or "k_prep" in t) and "k_fused" in t
+        assert "k_fused" in t  # (4096 rows: the count-free prep pass runs inside k_fused)
         assert all(x > 0 for x in t.values())
-        assert ctx.last_launch_count() >= 2
+        assert ctx.last_launch_count() >= 1
         out = dev.product_tensors(p, d)
         assert np.array_equal(out.col_idx.cpu().numpy().view(np.uint64), ci)
     assert_csr_bitwise_equal(CsrMatrix(a.rows, a.cols, rp, ci, v), _oracle_csr(a, a), "fd64")
