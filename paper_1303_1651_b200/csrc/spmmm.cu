@@ -1633,6 +1633,13 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   CUDA_TRY(ensure(c->aux, (2 * kMaxPipeBlocks + 2) * 8, c->stream));
   // buffers (re)allocated on the context stream must exist before s_up uses them
   CUDA_TRY(cudaEventRecord(*ev_struct, c->stream));
+  // SPMMM_TRACE: a GPU timeline of the call (upload, compute, download of
+  // every block, relative to this point), printed at the end
+  cudaEvent_t tl[1 + 3 * kMaxPipeBlocks] = {};
+  if (tr.on) {
+    for (cudaEvent_t& ev : tl) cudaEventCreate(&ev);
+    cudaEventRecord(tl[0], c->stream);
+  }
   CUDA_TRY(cudaStreamWaitEvent(c->s_up, *ev_struct, 0));
   uint64_t* d_arp = static_cast<uint64_t*>(c->a_rp.p);
   uint64_t* d_aci = static_cast<uint64_t*>(c->a_ci.p);
@@ -1720,6 +1727,7 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
       }
       if (e1 > e0) CUDA_TRY(h2d(d_av + e0, a->values + e0, (e1 - e0) * 8));
       CUDA_TRY(cudaEventRecord(ev_av[j], c->s_up));
+      if (tr.on) cudaEventRecord(tl[1 + j], c->s_up);
       step_done(j + 2);
     }
     return SPMMM_OK;
@@ -2020,6 +2028,10 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
       }
     }
     CUDA_TRY(cudaEventRecord(ev_down[j], c->s_down));  // (arrays live until the end)
+    if (tr.on) {
+      cudaEventRecord(tl[1 + kMaxPipeBlocks + j], c->stream);
+      cudaEventRecord(tl[1 + 2 * kMaxPipeBlocks + j], c->s_down);
+    }
     blk_off[j] = off;
     blk_n[j] = p->nnz;
     blk_r0[j] = r0;
@@ -2090,6 +2102,18 @@ int multiply_host_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b,
   CUDA_TRY(cudaStreamSynchronize(c->s_down));
   CUDA_TRY(cudaStreamSynchronize(c->s_up));
   tr.mark("pipe: downloads done");
+  if (tr.on) {
+    cudaDeviceSynchronize();
+    for (int j = 0; j < G; ++j) {
+      float up = 0, comp = 0, down = 0;
+      cudaEventElapsedTime(&up, tl[0], tl[1 + j]);
+      cudaEventElapsedTime(&comp, tl[0], tl[1 + kMaxPipeBlocks + j]);
+      cudaEventElapsedTime(&down, tl[0], tl[1 + 2 * kMaxPipeBlocks + j]);
+      std::fprintf(stderr, "[spmmm] block %2d: uploaded %7.3f ms, computed %7.3f ms, downloaded %7.3f ms\n",
+                   j, up, comp, down);
+    }
+    for (cudaEvent_t ev : tl) cudaEventDestroy(ev);
+  }
   guard.f = nullptr;  // success: the result arrays are the caller's
   for (void* hp : {hrp32, hd16, hbase}) host_free_internal(hp);
   hrp32 = hd16 = hbase = nullptr;
