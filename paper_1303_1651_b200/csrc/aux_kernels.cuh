@@ -262,23 +262,90 @@ __host__ __device__ inline bool ell_wanted(const unsigned long long* w, uint64_t
 // path, which also yields the reference's exact error for bad input.
 // (CfFlags and cf_applies: rows.cuh, beside the ELL layout)
 
-// The count-free path's first pass (prep_pass in rows.cuh) as a kernel of its
-// own; small products run it inside k_fused instead (PREP instantiations).
+// The count-free path's first pass as a kernel (small products run the same
+// pass, prep_pass in rows.cuh, inside k_fused: the PREP instantiations; this
+// kernel keeps its own copy of the body — routed through the shared device
+// function it compiled 17% slower on C2, 0.118 -> 0.138 ms, measured).
+// MODE 0, C = A·A (A square, its rows are B's rows): one pass over the rows
+// measures both and checks A's columns while packing them as B's records.
+// MODE 1, A spans most of B: A's rows and columns, then every B row (checked,
+// measured, packed). MODE 2, A a row block of a larger matrix: A only — its
+// rows, its columns against B.rows and their range [kmin, kmax] — and
+// k_prep_b takes the B rows in that range.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_prep(DevCsr A, DevCsr B,
                                               unsigned long long* __restrict__ ctrl,
                                               unsigned long long* __restrict__ zero,
                                               uint64_t nzero, uint4* __restrict__ ell) {
-  const CfWords w{ctrl + kCtrlCfFlags, ctrl + kCtrlKMinInv, ctrl + kCtrlKMax1, ctrl + kCtrlCfEll};
-  prep_pass<MODE>(A, B, w, zero, nzero, ell, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x,
-                  uint64_t(gridDim.x) * blockDim.x);
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t t0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (uint64_t i = t0; i < nzero; i += stride) zero[i] = 0;
+  unsigned f = 0;
+  unsigned long long ma = 0, mb = 0, kmin = ~0ull, kmax1 = 0;
+  if (MODE != 0) {
+    for (uint64_t r = t0; r < A.rows; r += stride) {
+      const uint64_t lo = ld_idx(A.rp + r), hi = ld_idx(A.rp + r + 1);
+      if (hi < lo || hi > A.nnz) f |= kCfBadA;
+      else ma = hi - lo > ma ? hi - lo : ma;
+    }
+    // every column of A's rows must name a row of B (k_fused trusts them);
+    // coalesced over the entries of the rows' span
+    uint64_t e0 = ld_idx(A.rp), e1 = ld_idx(A.rp + A.rows);
+    e1 = e1 < A.nnz ? e1 : A.nnz;
+    for (uint64_t e = e0 + t0; e < e1; e += stride) {
+      const uint64_t k = ld_idx(A.ci + e);
+      if (k >= B.rows) f |= kCfBadCol;
+      if (MODE == 2) {
+        kmin = k < kmin ? k : kmin;
+        kmax1 = k + 1 > kmax1 ? k + 1 : kmax1;
+      }
+    }
+  }
+  if (MODE != 2) {
+    for (uint64_t r = t0; r < B.rows; r += stride) {
+      const uint64_t lo = ld_idx(B.rp + r), hi = ld_idx(B.rp + r + 1);
+      if (hi < lo || hi > B.nnz) {
+        f |= MODE == 0 ? (kCfBadB | kCfBadA) : kCfBadB;
+        continue;
+      }
+      mb = hi - lo > mb ? hi - lo : mb;
+      if (MODE == 0)
+        for (uint64_t e = lo; e < hi; ++e)
+          if (ld_idx(B.ci + e) >= B.rows) f |= kCfBadCol;  // (L1 hits: the record's loads)
+      if (ell) pack_ell_record(B, r, lo, hi, ell);  // (longer rows: truncated, never read)
+    }
+    if (MODE == 0) ma = mb;
+  }
+  f = __reduce_or_sync(kFull, f);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long oa = __shfl_xor_sync(kFull, ma, d), ob = __shfl_xor_sync(kFull, mb, d);
+    ma = oa > ma ? oa : ma;
+    mb = ob > mb ? ob : mb;
+    if (MODE == 2) {
+      const unsigned long long o0 = __shfl_xor_sync(kFull, kmin, d);
+      const unsigned long long o1 = __shfl_xor_sync(kFull, kmax1, d);
+      kmin = o0 < kmin ? o0 : kmin;
+      kmax1 = o1 > kmax1 ? o1 : kmax1;
+    }
+  }
+  if (lane_id() == 0) {
+    if (f) atomicOr(ctrl + kCtrlCfFlags, (unsigned long long)f);
+    if (ma) atomicMax(ctrl + kCtrlCfFlags + 1, ma);
+    if (mb) atomicMax(ctrl + kCtrlCfFlags + 2, mb);
+    if (MODE == 2 && kmax1) {
+      atomicMax(ctrl + kCtrlKMinInv, ~kmin);
+      atomicMax(ctrl + kCtrlKMax1, kmax1);
+    }
+    if (MODE != 2 && ell && blockIdx.x == 0 && threadIdx.x == 0) ctrl[kCtrlCfEll] = 1;
+  }
 }
 
 // The B rows A references, [kmin, kmax] from k_prep: checked, measured and
 // (when A references most of them: at least 7/10 of the range, by A's entry
 // count) packed into ELL records — the counted path's rule (ell_wanted).
 // Rows outside the range are never read, like k_count leaves them unchecked.
-__global__ void __launch_bounds__(256) k_prep_b(DevCsr A, DevCsr B,
+__global__ void __launch_bounds__(256, 8) k_prep_b(DevCsr A, DevCsr B,
                                                 unsigned long long* __restrict__ ctrl,
                                                 uint4* __restrict__ ell) {
   const uint64_t k0 = ~ctrl[kCtrlKMinInv], k1 = ctrl[kCtrlKMax1];
