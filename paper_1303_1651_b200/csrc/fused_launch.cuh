@@ -9,7 +9,10 @@
 
 namespace spmmm {
 
-constexpr int kFusedWarps = 8;
+#ifndef SPMMM_FUSED_WARPS
+#define SPMMM_FUSED_WARPS 8
+#endif
+constexpr int kFusedWarps = SPMMM_FUSED_WARPS;
 #ifndef SPMMM_SHORT_BLOCKS
 #define SPMMM_SHORT_BLOCKS 4  // resident blocks per SM the short variant is compiled for
 #endif
