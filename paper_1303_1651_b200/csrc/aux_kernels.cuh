@@ -25,8 +25,9 @@ enum Ctrl : int {
   kCtrlMidRows = 12,    // sub-list: rows for k_long_smem (one block per row)
   kCtrlHugeRows = 13,   // sub-list: rows for the cluster variant (8 blocks per row)
   kCtrlOvfRows = 14,    // sub-list: rows the cluster variant handed to k_long
-  kCtrlHugeTicket = 15, // cluster variant's dynamic row counter
-  kCtrlCopyTickets = 16, // k_copy_long: [16] block rows, [17] warp rows
+  kCtrlHugeTicket = 15, // cluster variant's dynamic row counter; ESC mode: k_esc_dom's
+  kCtrlCopyTickets = 16, // k_copy_long: block rows
+  kCtrlDomBigRows = 17, // sub-list: k_esc_dom's rows past the block-copy limit
   kCtrlBMaxLen = 18,    // longest B row referenced by A (entries)
   kCtrlKMinInv = 19,    // ~(smallest column of A), 0 if A has no entries
   kCtrlKMax1 = 20,      // largest column of A + 1, 0 if none
@@ -38,12 +39,27 @@ enum Ctrl : int {
   kCtrlCfFlags = 26,    // count-free path: kCf* bits, then [27] longest A row, [28] longest B row
   kCtrlDone = 29,       // count-free path: k_fused warps finished (the last one reports)
   kCtrlCfEll = 30,      // count-free path: B's referenced rows were packed into ELL records
+  kCtrlDomRows = 31,    // sub-list: rows dominated by one long B row (k_esc_dom)
   kCtrlWords = 32
 };
 
 // rows past this many products are split into column-range parts in ESC mode
 // (esc.cuh); k_count sums their products for the host
 constexpr uint32_t kHugeMin = 5120;
+
+// Rows dominated by one long B row (skewed inputs: a short A row that hits a
+// long B row — a third of C5's products sit in such rows): the longest B row
+// of the row, L entries, holds at least half of its P products and at most
+// kDomRCap products come from the other entries. Such a row is the dominant
+// run — already sorted, distinct columns — merged with the few sorted others
+// (esc.cuh k_esc_dom) instead of P keys sorted from scratch. k_count records
+// the dominant entry (its offset in the A row; the first of the longest).
+constexpr uint32_t kDomRCap = 256;
+constexpr uint32_t kDomMinRun = 64;
+constexpr uint32_t kNoDom = 0xffffffffu;
+__host__ __device__ inline bool dom_eligible(uint64_t P, uint64_t L) {
+  return L >= kDomMinRun && 2 * L >= P && P - L <= kDomRCap;
+}
 
 
 // ---------------------------------------------------------------------------
@@ -55,7 +71,8 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
                                                unsigned long long* __restrict__ ctrl,
                                                unsigned long long* __restrict__ zero,
                                                uint64_t nzero, uint4* __restrict__ ell_self,
-                                               uint4* __restrict__ ell_all) {
+                                               uint4* __restrict__ ell_all,
+                                               uint32_t* __restrict__ dom) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nzero;
        i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = 0;
@@ -77,6 +94,8 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       }
     }
     uint64_t p = 0;
+    uint64_t rl = 0;   // the row's longest B row and the (first) entry holding it
+    uint32_t re = 0;
     // rows past kSerial entries: the whole warp, one row at a time. When only
     // a few rows of the warp pass 8 entries (skewed inputs), those go to the
     // warp too, so 31 short rows do not wait on one lane's 30-entry loop.
@@ -103,6 +122,10 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
           if (b1[u] < b0[u] || b1[u] > B.nnz) { err |= 4u; continue; }
           const uint64_t l = b1[u] - b0[u];
           p += l;
+          if (l > rl) {
+            rl = l;
+            re = uint32_t(e0 + u - lo);
+          }
           bmax = l > bmax ? l : bmax;
           kmin = k[u] < kmin ? k[u] : kmin;
           kmax1 = k[u] + 1 > kmax1 ? k[u] + 1 : kmax1;
@@ -115,7 +138,8 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
       const uint32_t src = __ffs(big) - 1;
       big &= big - 1;
       const uint64_t blo = __shfl_sync(kFull, lo, src), bhi = __shfl_sync(kFull, hi, src);
-      uint64_t s = 0;
+      uint64_t s = 0, sl = 0;
+      uint32_t se = 0;
       // four entries per lane per round: a 4096-entry row is 32 rounds of two
       // dependent loads, not 128 (such rows set the kernel's tail)
       for (uint64_t e0 = blo + lane; e0 < bhi; e0 += 128) {
@@ -140,13 +164,31 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
           if (b1[u] < b0[u] || b1[u] > B.nnz) { err |= 4u; continue; }
           const uint64_t l = b1[u] - b0[u];
           s += l;
+          if (l > sl) {  // (a lane's entries ascend: its first longest)
+            sl = l;
+            se = uint32_t(e0 + 32u * u - blo);
+          }
           bmax = l > bmax ? l : bmax;
           kmin = k[u] < kmin ? k[u] : kmin;
           kmax1 = k[u] + 1 > kmax1 ? k[u] + 1 : kmax1;
         }
       }
       s = warp_sum64(s);
-      if (lane == src) p = s;
+      // longest, then lowest entry
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        const uint64_t ol = __shfl_xor_sync(kFull, sl, d);
+        const uint32_t oe = __shfl_xor_sync(kFull, se, d);
+        if (ol > sl || (ol == sl && oe < se)) {
+          sl = ol;
+          se = oe;
+        }
+      }
+      if (lane == src) {
+        p = s;
+        rl = sl;
+        re = se;
+      }
     }
     // C = A·A: row r of A is row r of B — its ELL record is written here, from
     // entries this lane has just read, instead of by a k_pack_ell pass
@@ -154,6 +196,7 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
     if (r < A.rows) {
       if (p > 0x7fffffffull) err |= 8u;
       prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
+      if (dom) dom[r] = (p <= 0x7fffffffull && dom_eligible(p, rl)) ? re : kNoDom;
       tot += p;
       huge += p > kHugeMin ? p : 0;
       mx = p > mx ? p : mx;
@@ -401,7 +444,10 @@ __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __res
                                                  uint32_t* __restrict__ lmap,
                                                  uint32_t* __restrict__ mid_list,
                                                  uint32_t* __restrict__ huge_list,
-                                                 unsigned long long* __restrict__ ctrl) {
+                                                 unsigned long long* __restrict__ ctrl,
+                                                 const uint32_t* __restrict__ dom,
+                                                 uint32_t* __restrict__ dom_list,
+                                                 uint32_t* __restrict__ dom_big) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   // warp-uniform trip count so the ballots are full-warp
@@ -417,15 +463,24 @@ __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __res
     }
     const uint32_t m = __ballot_sync(kFull, is_long);
     if (!m) continue;
-    uint32_t base = 0;
-    if (lane_id() == 0) base = uint32_t(atomicAdd(ctrl + kCtrlLongRows, (unsigned long long)__popc(m)));
+    const bool is_dom = is_long && dom && dom[r] != kNoDom;
+    const uint32_t md = __ballot_sync(kFull, is_dom);
+    uint32_t base = 0, dbase = 0;
+    if (lane_id() == 0) {
+      base = uint32_t(atomicAdd(ctrl + kCtrlLongRows, (unsigned long long)__popc(m)));
+      if (md) dbase = uint32_t(atomicAdd(ctrl + kCtrlDomRows, (unsigned long long)__popc(md)));
+    }
     base = __shfl_sync(kFull, base, 0);
+    dbase = __shfl_sync(kFull, dbase, 0);
     if (is_long) {
       const uint32_t idx = base + __popc(m & lanemask_lt());
       list[idx] = uint32_t(r);
       lmap[r] = idx;
-      // rows per computing kernel (few: plain atomics)
-      if (pr > huge_min) huge_list[atomicAdd(ctrl + kCtrlHugeRows, 1ull)] = idx;
+      // rows per computing kernel (the others are few: plain atomics)
+      if (is_dom) {
+        dom_list[dbase + __popc(md & lanemask_lt())] = idx;
+        if (pr > mid_min) dom_big[atomicAdd(ctrl + kCtrlDomBigRows, 1ull)] = idx;
+      } else if (pr > huge_min) huge_list[atomicAdd(ctrl + kCtrlHugeRows, 1ull)] = idx;
       else if (pr > mid_min) mid_list[atomicAdd(ctrl + kCtrlMidRows, 1ull)] = idx;
     }
   }
@@ -472,6 +527,7 @@ struct LongParams {
   const unsigned long long* n_sub;    // their count
   unsigned long long* ticket;         // dynamic row counter
   uint32_t* ovf;                      // cluster variant: rows handed on to k_long
+  const uint32_t* dom;                // k_esc_dom: the dominant entry of each of its rows
   // ESC mode (esc.cuh): column-range parts of the huge rows
   struct PartDesc* parts;             // [max parts]
   uint64_t* part_off;                 // staging offset per part
@@ -756,6 +812,7 @@ struct CopyParams {
   const uint32_t* list;      // pre-computed rows (k_collect)
   const uint32_t* prod;
   const uint32_t* big;       // mid then huge sub-lists (rows = A.rows apart)
+  const uint32_t* dom_big;   // k_esc_dom's rows past long_min (null: none)
   const unsigned long long* ctrl;
   unsigned long long* tickets;  // [0] big rows, [1] other rows
   const uint64_t* l_off;
@@ -813,12 +870,27 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
   unsigned long long* cci = reinterpret_cast<unsigned long long*>(p.c_ci);
   const uint32_t n_mid = uint32_t(p.ctrl[kCtrlMidRows]);
   const uint32_t n_big = n_mid + uint32_t(p.ctrl[kCtrlHugeRows]);
+  const uint32_t n_dom = p.dom_big ? uint32_t(p.ctrl[kCtrlDomBigRows]) : 0u;
   while (true) {
     if (threadIdx.x == 0) s_t = uint32_t(atomicAdd(p.tickets, 1ull));
     __syncthreads();
     const uint32_t t = s_t;
     __syncthreads();
-    if (t >= n_big) break;
+    if (t >= n_big + n_dom) break;
+    if (t >= n_big) {  // dominated rows past long_min (the shorter ones: warps, below)
+      const uint32_t dl = p.dom_big[t - n_big];
+      const uint32_t dr = p.list[dl];
+      const uint64_t ddst = p.c_rp[dr];
+      const uint32_t dcnt = p.l_nnz[dl];
+      if (ddst + dcnt > p.c_cap) {
+        if (threadIdx.x == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
+        continue;
+      }
+      const uint64_t dsrc = p.l_off[dl];
+      copy_run<4>(cci + ddst, p.c_v + ddst, p.l_ci + dsrc, p.l_v + dsrc, dcnt, threadIdx.x,
+                  blockDim.x);
+      continue;
+    }
     const uint32_t li = t < n_mid ? p.big[t] : p.big[p.rows + (t - n_mid)];
     const uint64_t dst = p.c_rp[p.list[li]];
     const uint32_t np = (t >= n_mid && p.row_np) ? p.row_np[t - n_mid] : 0u;

@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
     const uint32_t r = p.list[li];
     const uint32_t P = p.prod[r];
     if (P > kEscWarpLimit) continue;  // block kernel
+    if (p.dom && p.dom[r] != kNoDom) continue;  // k_esc_dom
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
     // ---- expand: product q -> skey[q] = col << 9 | q, sval[q] = a * b ----
     uint32_t base = 0;
@@ -290,6 +291,247 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
       if (STATS) {
         p.st_min[r] = skey[0] >> kEscQBits;
         p.st_max[r] = skey[P - 1] >> kEscQBits;
+        p.st_touch[r] = touches;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+
+// ---- k_esc_dom -------------------------------------------------------------------
+// Rows dominated by one long B row (aux_kernels.cuh dom_eligible): the
+// dominant entry's L products — a·(B row), columns ascending and distinct, the
+// storage contract of formats.py:40-46 — are streamed, 32 per step, straight
+// from B to the staged result, and merged on the way with the row's other
+// <= kDomRCap products, which are expanded and sorted as in k_esc_warp (key
+// col << 8 | qR, qR their product order). A column of the others is folded
+// left to right in product order from 0.0; where the dominant row has the
+// same column its product joins the fold at its place in the order: after the
+// products of earlier A entries (qR < n_before), before the later ones. So
+// C[r, x] keeps the reference's k order (kernels.py:163-180), exact zeros are
+// dropped (kernels.py:296-298), and a step's outputs are placed by counting:
+// a dominant column after the kept columns before it, a merged column after
+// the kept dominant columns below it. A B row whose columns do not ascend is
+// reported (kCfUnsorted) and the product redone without this kernel.
+constexpr int kDomWarps = 8;
+#ifndef SPMMM_DOM_BLOCKS
+#define SPMMM_DOM_BLOCKS 4
+#endif
+constexpr int kDomBlocks = SPMMM_DOM_BLOCKS;  // resident blocks per SM
+constexpr int kDomQBits = 8;
+static_assert((1u << kDomQBits) >= kDomRCap, "qR bits");
+
+__host__ __device__ constexpr size_t esc_dom_smem_bytes() {
+  return size_t(kDomWarps) * kDomRCap * (sizeof(uint32_t) + sizeof(double));
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(kDomWarps * 32, kDomBlocks) k_esc_dom(const LongParams p_in) {
+  extern __shared__ __align__(16) unsigned char esc_sm[];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  double* sval = reinterpret_cast<double*>(esc_sm) + warp * kDomRCap;
+  uint32_t* skey =
+      reinterpret_cast<uint32_t*>(esc_sm + kDomWarps * kDomRCap * sizeof(double)) + warp * kDomRCap;
+  LongParams p = p_in;
+  p.B.pol = policy_evict_last();
+  p.A.pol = policy_evict_first();
+  const uint32_t n_rows = uint32_t(*(volatile const unsigned long long*)p.n_sub);
+  constexpr uint32_t qmask = (1u << kDomQBits) - 1u;
+#pragma unroll 1
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.ticket, 1ull);
+    const uint32_t tr = uint32_t(__shfl_sync(kFull, t, 0));
+    if (tr >= n_rows) break;
+    const uint32_t li = p.sub[tr];
+    const uint32_t r = p.list[li];
+    const uint32_t P = p.prod[r];
+    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
+    const uint64_t ed = lo + p.dom[r];  // the dominant entry
+    const uint64_t kd = ld_idx(p.A.ci + ed, p.A.pol);
+    const double ad = ld_val(p.A.v + ed, p.A.pol);
+    const uint64_t bsd = ld_idx(p.B.rp + kd, p.B.pol);
+    const uint32_t L = uint32_t(ld_idx(p.B.rp + kd + 1, p.B.pol) - bsd);
+    const uint32_t nR = P - L;
+    // ---- expand the other entries: skey[qR] = col << 8 | qR, sval[qR] = a * b ----
+    uint32_t base = 0, n_before = 0;
+#pragma unroll 1
+    for (uint64_t ab = lo; ab < hi && nR; ab += 32) {
+      const uint32_t na = uint32_t(hi - ab < 32 ? hi - ab : 32);
+      uint64_t bs = 0;
+      uint32_t len = 0;
+      double av = 0.0;
+      if (lane < na && ab + lane != ed) {
+        const uint64_t k = ld_idx(p.A.ci + ab + lane, p.A.pol);
+        av = ld_val(p.A.v + ab + lane, p.A.pol);
+        bs = ld_idx(p.B.rp + k, p.B.pol);
+        len = uint32_t(ld_idx(p.B.rp + k + 1, p.B.pol) - bs);
+      }
+      n_before += __reduce_add_sync(kFull, ab + lane < ed ? len : 0u);
+      const uint32_t incl = warp_incl_scan(len);
+      const uint32_t excl = incl - len;
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+#pragma unroll 1
+      for (uint32_t c = 0; c < tot; c += 64) {
+        uint32_t col[2];
+        double bv[2], a[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t q = c + 32u * u + lane;
+          int i = 0;  // owner: the largest entry with excl <= q
+#pragma unroll
+          for (int st = 16; st > 0; st >>= 1) {
+            const uint32_t ex = __shfl_sync(kFull, excl, i + st);
+            if (ex <= q) i += st;
+          }
+          const uint64_t src = __shfl_sync(kFull, bs, i) + (q - __shfl_sync(kFull, excl, i));
+          a[u] = __shfl_sync(kFull, av, i);
+          col[u] = 0;
+          bv[u] = 0.0;
+          if (q < tot) {
+            col[u] = uint32_t(ld_idx(p.B.ci + src, p.B.pol));
+            bv[u] = ld_val(p.B.v + src, p.B.pol);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t q = c + 32u * u + lane;
+          if (q < tot) {
+            skey[base + q] = (col[u] << kDomQBits) | (base + q);
+            sval[base + q] = __dmul_rn(a[u], bv[u]);
+          }
+        }
+      }
+      base += tot;
+    }
+    __syncwarp();
+    if (nR > 1) sort_run(skey, nR);
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(p.ctrl + kCtrlStageCursor, (unsigned long long)P);  // upper bound
+    off = __shfl_sync(kFull, off, 0);
+    // ---- stream the dominant run, merging the others in ----
+    uint32_t out = 0, rpos = 0, touches = 0, prev_last = 0;
+    bool unsorted = false;
+    uint64_t ncol = 0;
+    double nval = 0.0;
+    if (lane < L) {
+      ncol = ld_idx(p.B.ci + bsd + lane, p.B.pol);
+      nval = ld_val(p.B.v + bsd + lane, p.B.pol);
+    }
+#pragma unroll 1
+    for (uint32_t j0 = 0; j0 < L; j0 += 32) {
+      const bool valid = j0 + lane < L;
+      const uint32_t cd = valid ? uint32_t(ncol) : kEmptyKey;
+      const double pd = __dmul_rn(ad, nval);
+      if (j0 + 32 + lane < L) {  // the next step's loads, in flight during this one
+        ncol = ld_idx(p.B.ci + bsd + j0 + 32 + lane, p.B.pol);
+        nval = ld_val(p.B.v + bsd + j0 + 32 + lane, p.B.pol);
+      }
+      uint32_t prevc = __shfl_up_sync(kFull, cd, 1);
+      if (lane == 0) prevc = prev_last;
+      unsorted |= valid && (j0 + lane) > 0 && cd <= prevc;
+      prev_last = __shfl_sync(kFull, cd, 31);
+      const bool last = j0 + 32 >= L;
+      const uint32_t limit = last ? kEmptyKey : prev_last;  // the others up to this column
+      const double accd = __dadd_rn(0.0, pd);
+      uint32_t km = __ballot_sync(kFull, valid && accd != 0.0);  // dominant-only columns kept
+      uint32_t rbefore = 0, rk = 0, absorbed = 0;
+      // the others up to `limit`, 32 per round, one per lane in sorted order
+#pragma unroll 1
+      while (rpos < nR) {
+        const uint32_t x = rpos + lane;
+        const uint32_t kx = x < nR ? skey[x] : kEmptyKey;
+        const uint32_t cx = kx >> kDomQBits;
+        const bool in = x < nR && cx <= limit;
+        const uint32_t inm = __ballot_sync(kFull, in);  // (a prefix of the lanes)
+        if (!inm) break;
+        const bool head = in && (x == 0 || (skey[x - 1] >> kDomQBits) != cx);
+        // jd: the step's dominant columns below cx (they ascend; lanes past L hold ~0)
+        uint32_t jd = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const uint32_t c = __shfl_sync(kFull, cd, jd + st - 1);
+          if (c < cx) jd += st;
+        }
+        const uint32_t cj = __shfl_sync(kFull, cd, jd);
+        const double pm = __shfl_sync(kFull, pd, jd);
+        if (jd == 31 && cj < cx) jd = 32;
+        const bool match = head && jd < 32 && cj == cx;
+        double acc = 0.0;
+        if (head) {
+          bool pend = match;
+          uint32_t t2 = x;
+          do {
+            const uint32_t kt = skey[t2];
+            if ((kt >> kDomQBits) != cx) break;
+            const uint32_t q = kt & qmask;
+            if (pend && q >= n_before) {
+              if (STATS && acc == 0.0) ++touches;
+              acc = __dadd_rn(acc, pm);
+              pend = false;
+            }
+            if (STATS && acc == 0.0) ++touches;
+            acc = __dadd_rn(acc, sval[q]);
+            ++t2;
+          } while (t2 < nR);
+          if (pend) {
+            if (STATS && acc == 0.0) ++touches;
+            acc = __dadd_rn(acc, pm);
+          }
+        }
+        const uint32_t ab = __reduce_or_sync(kFull, match ? (1u << jd) : 0u);
+        km &= ~ab;  // those columns are the merged ones' now
+        absorbed |= ab;
+        const bool keepx = head && acc != 0.0;
+        const uint32_t kmx = __ballot_sync(kFull, keepx);
+        if (keepx) {  // after the kept dominant-only columns below it and the kept merged before it
+          const uint32_t dbelow = jd >= 32 ? km : (km & ((1u << jd) - 1u));
+          const uint64_t pos = off + out + __popc(dbelow) + rk + __popc(kmx & lanemask_lt());
+          __stcs(p.l_ci + pos, cx);
+          __stcs(p.l_v + pos, acc);
+        }
+        // a dominant-only column: the kept merged columns below it (this round's:
+        // the others' columns ascend over the lanes)
+        {
+          const uint32_t ce = in ? cx : kEmptyKey;
+          uint32_t ix = 0;
+#pragma unroll
+          for (int st = 16; st > 0; st >>= 1) {
+            const uint32_t c = __shfl_sync(kFull, ce, ix + st - 1);
+            if (c < cd) ix += st;
+          }
+          const uint32_t c31 = __shfl_sync(kFull, ce, 31);
+          if (ix == 31 && c31 < cd) ix = 32;
+          rbefore += __popc(ix >= 32 ? kmx : (kmx & ((1u << ix) - 1u)));
+        }
+        rk += __popc(kmx);
+        const uint32_t cnt = __popc(inm);
+        rpos += cnt;
+        if (cnt < 32) break;
+      }
+      if ((km >> lane) & 1u) {
+        const uint64_t pos = off + out + __popc(km & lanemask_lt()) + rbefore;
+        __stcs(p.l_ci + pos, cd);
+        __stcs(p.l_v + pos, accd);
+      }
+      if (STATS && valid && !((absorbed >> lane) & 1u)) ++touches;
+      out += __popc(km) + rk;
+    }
+    if (__ballot_sync(kFull, unsorted) && lane == 0)
+      atomicOr(p.ctrl + kCtrlCfFlags, (unsigned long long)kCfUnsorted);
+    if (STATS) touches = __reduce_add_sync(kFull, touches);
+    if (lane == 0) {
+      p.l_off[li] = off;
+      p.l_nnz[li] = out;
+      if (STATS) {
+        // (touches: summed over the lanes below)
+        const uint32_t c0 = uint32_t(ld_idx(p.B.ci + bsd, p.B.pol));
+        const uint32_t c1 = uint32_t(ld_idx(p.B.ci + bsd + L - 1, p.B.pol));
+        const uint32_t r0 = nR ? skey[0] >> kDomQBits : c0;
+        const uint32_t r1 = nR ? skey[nR - 1] >> kDomQBits : c1;
+        p.st_min[r] = c0 < r0 ? c0 : r0;
+        p.st_max[r] = c1 > r1 ? c1 : r1;
         p.st_touch[r] = touches;
       }
     }

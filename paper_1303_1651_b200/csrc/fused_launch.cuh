@@ -27,7 +27,8 @@ struct FusedLaunchEnv {
   cudaStream_t stream;
 };
 
-template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0>
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0,
+          bool SPLIT = false>
 struct FusedVariant {
   static constexpr size_t smem() {
     return FusedSmem<R, MEDIUM>::bytes(WARPS);
@@ -37,7 +38,7 @@ struct FusedVariant {
     static int cache[64] = {};
     int& c = cache[device & 63];
     if (c == 0) {
-      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP>;
+      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP, SPLIT>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(smem()));
       if (e != cudaSuccess) return e;
@@ -53,13 +54,16 @@ struct FusedVariant {
     FusedParams prm = prm_in;
     void* args[] = {&prm};
     return cudaLaunchCooperativeKernel(
-        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP>), dim3(grid),
+        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP, SPLIT>), dim3(grid),
         dim3(WARPS * 32), args, smem(), env.stream);
   }
 };
 
 // op 0: occupancy query into *occ; op 1: launch with `grid`
 cudaError_t fused_short(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
+                        bool stats, unsigned grid, int* occ);
+// the split-mode short variant (fused_split.cu): packed passes, no ELL path
+cudaError_t fused_split(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                         bool stats, unsigned grid, int* occ);
 cudaError_t fused_medium(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                          bool stats, unsigned grid, int* occ);
@@ -68,12 +72,12 @@ cudaError_t fused_medium(int op, const FusedParams& prm, const FusedLaunchEnv& e
 cudaError_t fused_cf(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                      bool stats, unsigned grid, int* occ, int prep);
 
-template <int WARPS, int R, bool MEDIUM, bool CF = false, int PREP = 0>
+template <int WARPS, int R, bool MEDIUM, bool CF = false, int PREP = 0, bool SPLIT = false>
 cudaError_t fused_dispatch(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                            bool stats, unsigned grid, int* occ) {
 #define SPMMM_FUSED_CASE(W, S)                                                  \
   if (wide == W && stats == S) {                                                \
-    using V = FusedVariant<WARPS, R, MEDIUM, W, S, CF, PREP>;                   \
+    using V = FusedVariant<WARPS, R, MEDIUM, W, S, CF, PREP, SPLIT>;                   \
     return op == 0 ? V::occupancy(env.device, occ) : V::launch(prm, env, grid); \
   }
   SPMMM_FUSED_CASE(false, false)

@@ -23,6 +23,9 @@
 #ifndef SPMMM_SHORT_BLOCKS
 #define SPMMM_SHORT_BLOCKS 4
 #endif
+#ifndef SPMMM_LOCK
+#define SPMMM_LOCK 4
+#endif
 
 namespace spmmm {
 
@@ -97,7 +100,8 @@ struct FusedSmem {
   }
 };
 
-template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0>
+template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0,
+          bool SPLIT = false>
 __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k_fused(const FusedParams p_in) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(!(MEDIUM && CF), "the count-free path is short rows only");
@@ -112,6 +116,17 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     cooperative_groups::this_grid().sync();
   }
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
+  static_assert(!SPLIT || (!MEDIUM && !CF && PREP == 0), "split mode: the counted short variant");
+  // PACK: groups of tiny rows share one packed pass (skewed inputs such as
+  // C5, where most rows have a handful of products). In the counted short
+  // variant; the count-free path's rows are full-width. (A split-mode
+  // instantiation without the ELL path, SPLIT, measured slower on C5 with the
+  // packed passes than this one, 0.73 against 0.61 ms: kept for A/B builds.)
+#ifndef SPMMM_NO_PACK
+  constexpr bool PACK = !MEDIUM && !CF && !STATS && (SPMMM_LOCK <= (1 << kPackSlotBits));
+#else
+  constexpr bool PACK = false;
+#endif
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   using SM = FusedSmem<R, MEDIUM>;
   constexpr int EMAX = MEDIUM ? kSmemSlots / 32 : 1;  // register sort up to 256 keys
@@ -232,13 +247,17 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     const uint64_t r0 = tile * R;
     // ---- row bounds and classes of the tile: lane i owns row r0 + i ----
     uint64_t rpv = 0;
-    uint32_t my_cls = kRowZero, my_na = 0;
+    uint32_t my_cls = kRowZero, my_na = 0, my_prod = 0;
     if (lane <= uint32_t(R) && r0 + lane <= rows) rpv = ld_idx(p.A.rp + r0 + lane, p.A.pol);
     const uint64_t rpn = __shfl_down_sync(kFull, rpv, 1);
     if (lane < uint32_t(R) && r0 + lane < rows) {
       my_na = uint32_t(rpn - rpv);
-      if constexpr (CF) my_cls = rpn > rpv ? uint32_t(kRowShort) : uint32_t(kRowZero);
-      else my_cls = uint32_t(classify(p.prod[r0 + lane], rpn - rpv, p.medium_limit));
+      if constexpr (CF) {
+        my_cls = rpn > rpv ? uint32_t(kRowShort) : uint32_t(kRowZero);
+      } else {
+        my_prod = p.prod[r0 + lane];
+        my_cls = uint32_t(classify(my_prod, rpn - rpv, p.medium_limit));
+      }
     }
     // per-row results, lane i = row i; rows computed before this kernel
     // (long rows, and in split mode every non-short row) only report nnz
@@ -250,12 +269,21 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     if (__ballot_sync(kFull, my_cls == kRowShort)) {
       // short rows go through short_rows in lockstep groups of kLock; the
       // groups run in a loop (one copy of the code: instruction cache)
-#ifndef SPMMM_LOCK
-#define SPMMM_LOCK 4
-#endif
       constexpr int kLock = R < SPMMM_LOCK ? R : SPMMM_LOCK;
       int ngroups = R / kLock;
       asm volatile("" : "+r"(ngroups));  // opaque: keep one copy of the group body
+      // a group whose short rows have <= 32 A entries and <= 32 products in
+      // all goes through one packed pass (rows.cuh packed_rows) instead of a
+      // pass per row: its sums, products | entries << 16, in each of its lanes
+      // (both groups' packed passes in lockstep measured slower: the code
+      // outgrew the instruction cache)
+      uint32_t pack_sum = 0;
+      if constexpr (PACK) {
+        pack_sum = my_cls == kRowShort ? (my_prod | (my_na << 16)) : 0u;
+#pragma unroll
+        for (int d = 1; d < kLock; d <<= 1) pack_sum += __shfl_xor_sync(kFull, pack_sum, d);
+        if (!WIDE && p.B.cols > (1ull << kPackColBits)) pack_sum = ~0u;
+      }
       // ELL path, two groups: the second group's A entries are loaded now and
       // the B records they address are prefetched into L2 while the first
       // group waits on its own loads (one lane per (row, entry): 4 rows x 8
@@ -263,7 +291,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       // neutral on C5.)
       const void* pf1 = nullptr;
       if constexpr (!MEDIUM) {
-        if (p.ell && ngroups > 1) {
+        if (!SPLIT && p.ell && ngroups > 1) {
           const uint32_t pi = lane >> 3, pe = lane & 7;
           const uint32_t src = uint32_t(kLock) + (pi < uint32_t(kLock) ? pi : 0u);
           const uint64_t plo = __shfl_sync(kFull, rpv, src);
@@ -291,9 +319,37 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
 #pragma unroll
         for (int i = 0; i < kLock; ++i) any |= hon[i];
         if (!any) continue;
+        if constexpr (PACK) {
+          const uint32_t gs = __shfl_sync(kFull, pack_sum, h * kLock);
+          if ((gs & 0xffffu) <= 32u && (gs >> 16) <= 32u) {
+            uint64_t glo[1][kLock];
+            uint32_t gna[1][kLock], pn[1][kLock];
+            bool gon[1][kLock];
+#pragma unroll
+            for (int i = 0; i < kLock; ++i) {
+              glo[0][i] = hlo[i];
+              gna[0][i] = hna[i];
+              gon[0][i] = hon[i];
+            }
+            ShortOut po[1];
+            packed_rows<kLock, 1, WIDE>(p.A, p.B, glo, gna, gon, po, pn);
+            uint32_t gn = 0;
+#pragma unroll
+            for (int i = 0; i < kLock; ++i) {
+              if (hon[i] && lane == uint32_t(h * kLock + i)) my_nnz = pn[0][i];
+              gn += pn[0][i];
+            }
+            if (po[0].keep) {
+              s_col[buf * kStage + staged + po[0].rank] = po[0].col;
+              s_val[buf * kStage + staged + po[0].rank] = po[0].val;
+            }
+            staged += gn;
+            continue;
+          }
+        }
         ShortOut so[kLock];
         uint32_t hprod[kLock];
-        short_rows<kLock, WIDE, STATS, !MEDIUM, CF>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz,
+        short_rows<kLock, WIDE, STATS, !MEDIUM && !SPLIT, CF>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz,
                                                     hmin, hmax, htouch, hprod,
                                                     h == 0 ? pf1 : nullptr);
         if constexpr (CF) {
@@ -465,6 +521,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
 struct RowsParams {
   DevCsr A, B;
   const uint32_t* prod;
+  const uint32_t* dom;  // rows with a dominant entry are k_esc_dom's (null: none are)
   const uint32_t* list;
   const unsigned long long* n_list;
   unsigned long long* cursor;  // staging allocator

@@ -63,7 +63,8 @@ enum CfFlags : unsigned {
   kCfBadA = 1,      // A.row_ptr decreasing or past nnz
   kCfBadB = 2,      // B.row_ptr decreasing or past nnz
   kCfBadCol = 4,    // an A column >= B.rows
-  kCfOverflow = 32  // C outgrew its reservation (found by k_fused; nothing past it written)
+  kCfOverflow = 32,  // C outgrew its reservation (found by k_fused; nothing past it written)
+  kCfUnsorted = 64   // k_esc_dom met a B row whose columns do not ascend (redone without it)
 };
 
 // ctrl + kCtrlCfFlags: [flags, longest A row, longest B row]. Every row of C
@@ -340,6 +341,168 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
       for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(kFull, t, d);
       stouch[i] = t;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Several short rows in one pass (skewed inputs: most rows of C5 have a
+// handful of products, so a pass per row leaves the warp nearly empty). The
+// NR rows' A entries share the lanes (entry lane l belongs to the row whose
+// entry range holds l), their products share the lanes in row order, and the
+// sort key carries the row slot above the column: one expand -> sort -> fold
+// pass yields the rows' results back to back, in row order, each row's
+// columns folded in the reference's k order exactly as short_rows does.
+// Needs sum(na) <= 32 and sum(products) <= 32 over the rows that are on, and
+// columns < 2^kPackColBits in the narrow variant (the caller checks).
+constexpr int kPackSlotBits = 2;  // NR <= 4 rows per pass
+constexpr int kPackColBits = 32 - 5 - kPackSlotBits;
+
+template <int NR, int G, bool WIDE>
+__device__ __forceinline__ void packed_rows(const DevCsr& A, const DevCsr& B,
+                                            const uint64_t (&lo)[G][NR],
+                                            const uint32_t (&na)[G][NR], const bool (&on)[G][NR],
+                                            ShortOut (&out)[G], uint32_t (&nnz)[G][NR]) {
+  static_assert(NR <= (1 << kPackSlotBits), "row slots per packed pass");
+  using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
+  constexpr int kSlotShift = int(sizeof(K)) * 8 - kPackSlotBits;
+  const uint32_t lane = lane_id();
+  // G independent passes in lockstep (their dependent loads overlap).
+  // entry lane -> (row slot, entry of that row)
+  uint32_t slot[G], e[G];
+  uint64_t rlo[G];
+  bool ent[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    uint32_t eb = 0;
+    slot[g] = 0;
+    e[g] = 0;
+    rlo[g] = 0;
+    ent[g] = false;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const uint32_t n = on[g][i] ? na[g][i] : 0u;
+      if (lane >= eb && lane < eb + n) {
+        slot[g] = uint32_t(i);
+        e[g] = lane - eb;
+        rlo[g] = lo[g][i];
+        ent[g] = true;
+      }
+      eb += n;
+    }
+  }
+  Off kk[G], bs[G];
+  double av[G];
+  uint32_t len[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    kk[g] = 0;
+    av[g] = 0.0;
+    if (ent[g]) {
+      kk[g] = Off(ld_idx(A.ci + rlo[g] + e[g], A.pol));
+      av[g] = ld_val(A.v + rlo[g] + e[g], A.pol);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    bs[g] = 0;
+    len[g] = 0;
+    if (ent[g]) {
+      const uint64_t b0 = ld_idx(B.rp + kk[g], B.pol);
+      bs[g] = Off(b0);
+      len[g] = uint32_t(ld_idx(B.rp + kk[g] + 1, B.pol) - b0);
+    }
+  }
+  // products of a pass's rows, in (row, k, j) order, one per lane
+  uint32_t incl[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) incl[g] = len[g];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t = __shfl_up_sync(kFull, incl[g], d);
+      if (lane >= uint32_t(d)) incl[g] += t;
+    }
+  }
+  uint32_t excl[G], tot[G];
+  int src[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    excl[g] = incl[g] - len[g];  // lanes past the entries: == tot, never an owner
+    tot[g] = __shfl_sync(kFull, incl[g], 31);
+    src[g] = 0;
+  }
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t ex = __shfl_sync(kFull, excl[g], src[g] + st);
+      if (ex <= lane) src[g] += st;
+    }
+  }
+  uint32_t col[G];
+  double p[G];
+  K key[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const Off bsrc = __shfl_sync(kFull, bs[g], src[g]) + (lane - __shfl_sync(kFull, excl[g], src[g]));
+    col[g] = 0;
+    p[g] = 0.0;
+    if (lane < tot[g]) {
+      col[g] = uint32_t(ld_idx(B.ci + bsrc, B.pol));
+      p[g] = ld_val(B.v + bsrc, B.pol);  // multiplied below, after the loads are in flight
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const double a = __shfl_sync(kFull, av[g], src[g]);
+    const uint32_t pslot = __shfl_sync(kFull, slot[g], src[g]);
+    const bool valid = lane < tot[g];
+    p[g] = valid ? __dmul_rn(a, p[g]) : 0.0;
+    key[g] = valid ? ((K(pslot) << kSlotShift) | (K(col[g]) << 5) | K(lane)) : ~K(0);
+  }
+  bitonic32_multi<G>(key);
+  // sorted by (row slot, column, q): valid keys fill lanes [0, tot)
+  K ck[G];
+  double v[G], acc[G];
+  bool head[G];
+  uint32_t seg[G];
+  uint32_t max_seg = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    ck[g] = key[g] >> 5;  // slot and column
+    v[g] = __shfl_sync(kFull, p[g], uint32_t(key[g]) & 31u);
+    const K prev = __shfl_up_sync(kFull, ck[g], 1);
+    head[g] = lane < tot[g] && (lane == 0 || prev != ck[g]);
+    const uint32_t hm = __ballot_sync(kFull, head[g]);
+    const uint32_t above = hm & ~((2u << lane) - 1u);
+    const uint32_t nxt = above ? uint32_t(__ffs(above) - 1) : tot[g];
+    seg[g] = head[g] ? nxt - lane : 0u;
+    max_seg = seg[g] > max_seg ? seg[g] : max_seg;
+    acc[g] = v[g];
+  }
+  max_seg = __reduce_max_sync(kFull, max_seg);
+  for (uint32_t d = 1; d < max_seg; ++d) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double t = __shfl_down_sync(kFull, v[g], d);
+      if (d < seg[g]) acc[g] = __dadd_rn(acc[g], t);
+    }
+  }
+  constexpr K kColMask = WIDE ? K(0xffffffffu) : K((1u << kPackColBits) - 1u);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const bool keep = head[g] && (acc[g] != 0.0);  // kernels.py:296 drops exact zeros
+    const uint32_t km = __ballot_sync(kFull, keep);
+    out[g].col = uint32_t(ck[g] & kColMask);
+    out[g].val = acc[g];
+    out[g].keep = keep;
+    out[g].rank = __popc(km & lanemask_lt());
+    const uint32_t sid = uint32_t(key[g] >> kSlotShift);
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+      nnz[g][i] = __popc(km & __ballot_sync(kFull, lane < tot[g] && sid == uint32_t(i)));
   }
 }
 

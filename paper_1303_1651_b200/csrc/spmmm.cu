@@ -108,8 +108,14 @@ void release(DevBuf& b, cudaStream_t s) {
 
 const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused", "k_copy_long",
                                     "k_rows", "k_long_smem", "k_long_cluster", "k_pack_ell",
-                                    "k_esc_warp", "k_esc_block", "k_esc_plan", "k_prep"};
-constexpr int kNumKernels = 13;
+                                    "k_esc_warp", "k_esc_block", "k_esc_plan", "k_prep",
+                                    "k_esc_dom"};
+constexpr int kNumKernels = 14;
+#ifdef SPMMM_SPLIT_VARIANT
+constexpr bool kSplitVariant = true;  // split mode runs fused_split.cu's instantiation
+#else
+constexpr bool kSplitVariant = false;
+#endif
 constexpr int kMaxPipeBlocks = 16;  // spmmm_multiply_host row blocks
 constexpr uint64_t kNarrowMin = 1 << 20;  // results past this many products: u32 indices down
 
@@ -139,6 +145,8 @@ struct spmmm_context {
   bool esc_attr[2] = {false, false};        // k_esc_* opt-in smem set
   int long_clusters = 0;                     // resident kLongParts-block clusters
   DevBuf sub;                                // per-kernel row sub-lists
+  DevBuf dom;                                // per row: its dominant entry (k_count -> k_esc_dom)
+  bool no_dom = false;                       // the next counted product runs without k_esc_dom
   DevBuf ell;                                // ELL records of B (short rows)
   DevBuf tr_scratch;                         // storage-order conversion scratch
   DevBuf parts, part_off, part_nnz, row_parts, scr_col, scr_val;  // ESC parts of huge rows
@@ -342,6 +350,7 @@ uint64_t lb_counters_max(uint64_t rows) {
 
 int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, bool pack = false) {
   CUDA_TRY(ensure(c->prod, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(c->dom, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
   // status: counters + words for one row per tile (the medium layout, the largest)
   const uint64_t ncnt = pack ? lb_counters_max(A.rows) : 0;
   if (pack) {
@@ -376,7 +385,7 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
         A, B, static_cast<uint32_t*>(c->prod.p), static_cast<unsigned long long*>(c->ctrl.p),
         static_cast<unsigned long long*>(c->status.p), ncnt,
         self_pack ? static_cast<uint4*>(c->ell.p) : nullptr,
-        spec_pack ? static_cast<uint4*>(c->ell.p) : nullptr);
+        spec_pack ? static_cast<uint4*>(c->ell.p) : nullptr, static_cast<uint32_t*>(c->dom.p));
     CUDA_TRY(cudaGetLastError());
     tm.end(0);
     ++c->last_launches;
@@ -406,10 +415,12 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
 // ---- fused-kernel launch: instantiations live in fused_short.cu / fused_medium.cu ----
 
 int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bool wide,
-               bool stats, unsigned grid, int* occ, bool count_free = false, int prep = 0) {
+               bool stats, unsigned grid, int* occ, bool count_free = false, int prep = 0,
+               bool split = false) {
   FusedLaunchEnv env{c->device, c->sms, c->stream};
   cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ, prep)
                   : medium   ? fused_medium(op, prm, env, wide, stats, grid, occ)
+                  : split    ? fused_split(op, prm, env, wide, stats, grid, occ)  // (A/B builds)
                              : fused_short(op, prm, env, wide, stats, grid, occ);
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
@@ -514,10 +525,17 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   CUDA_TRY(ensure(c->list, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->l_off, rows * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(c->l_nnz, rows * sizeof(uint32_t), c->stream));
-  CUDA_TRY(ensure(c->sub, 3 * rows * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(c->sub, 5 * rows * sizeof(uint32_t), c->stream));
   uint32_t* mid_list = static_cast<uint32_t*>(c->sub.p);
   uint32_t* huge_list = mid_list + rows;
   uint32_t* ovf_list = mid_list + 2 * rows;
+  uint32_t* dom_list = mid_list + 3 * rows;
+  uint32_t* dom_big = mid_list + 4 * rows;
+  // ESC mode: rows dominated by one long B row go to k_esc_dom (SPMMM_NO_DOM=1,
+  // or a B row found unsorted by it: all of them through the other kernels)
+  static const bool env_no_dom = std::getenv("SPMMM_NO_DOM") != nullptr;
+  const uint32_t* dom = (esc && !env_no_dom && !c->no_dom) ? static_cast<const uint32_t*>(c->dom.p)
+                                                         : nullptr;
   // split mode: k_rows (k_esc_warp) takes rows up to kRowsLimit
   // (kEscWarpLimit); else k_fused up to kMediumLimit
   const uint32_t long_min = esc ? kEscWarpLimit : split ? kRowsLimit : kMediumLimit;
@@ -566,7 +584,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     k_collect<<<unsigned(blocks), 256, 0, c->stream>>>(
         A, static_cast<const uint32_t*>(c->prod.p), list_limit, long_min, huge_min,
         static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p), mid_list, huge_list,
-        static_cast<unsigned long long*>(c->ctrl.p));
+        static_cast<unsigned long long*>(c->ctrl.p), dom, dom_list, dom_big);
     CUDA_TRY(cudaGetLastError());
     tm.end(1);
     ++c->last_launches;
@@ -576,6 +594,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     rp.A = A;
     rp.B = B;
     rp.prod = static_cast<const uint32_t*>(c->prod.p);
+    rp.dom = dom;
     rp.list = static_cast<const uint32_t*>(c->list.p);
     rp.n_list = static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlLongRows;
     rp.cursor = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlStageCursor;
@@ -602,6 +621,34 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
       // the warp rows are independent of the block rows: their kernel runs on
       // a second stream, overlapping k_esc_plan / k_esc_block (all three are
       // latency bound); the context stream joins it before k_fused
+      if (dom) {
+        // the dominated rows first, with the whole GPU: a latency-bound stream of
+        // B rows to the staged result (behind the other ESC kernels' resident
+        // blocks it got one block per SM and took 1.3 ms instead of 0.3)
+        LongParams dp{};
+        dp.A = A;
+        dp.B = B;
+        dp.prod = rp.prod;
+        dp.list = rp.list;
+        dp.ctrl = static_cast<unsigned long long*>(c->ctrl.p);
+        dp.l_off = rp.l_off;
+        dp.l_nnz = rp.l_nnz;
+        dp.l_ci = rp.l_ci;
+        dp.l_v = rp.l_v;
+        dp.sub = dom_list;
+        dp.n_sub = dp.ctrl + kCtrlDomRows;
+        dp.ticket = dp.ctrl + kCtrlHugeTicket;  // (the cluster variant's: unused in ESC mode)
+        dp.dom = dom;
+        dp.st_min = rp.st_min;
+        dp.st_max = rp.st_max;
+        dp.st_touch = rp.st_touch;
+        tm.begin(13);
+        if (stats) k_esc_dom<true><<<unsigned(c->sms) * kDomBlocks, kDomWarps * 32, esc_dom_smem_bytes(), c->stream>>>(dp);
+        else k_esc_dom<false><<<unsigned(c->sms) * kDomBlocks, kDomWarps * 32, esc_dom_smem_bytes(), c->stream>>>(dp);
+        CUDA_TRY(cudaGetLastError());
+        tm.end(13);
+        ++c->last_launches;
+      }
       static const bool serial = std::getenv("SPMMM_SERIAL_ESC") != nullptr;
       cudaStream_t ws = c->stream;
       if (!serial) {
@@ -621,8 +668,8 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
       else k_esc_warp<false><<<grid_rows, kEscWarps * 32, smem, ws>>>(rp);
       CUDA_TRY(cudaGetLastError());
       tm.end(9, ws);
-      if (esc_forked) CUDA_TRY(cudaEventRecord(c->ev_join, c->s_aux));
       ++c->last_launches;
+      if (esc_forked) CUDA_TRY(cudaEventRecord(c->ev_join, c->s_aux));
       tr.mark("  run_long: k_esc_warp launched");
     } else {
     const size_t smem = rows_smem_bytes();
@@ -670,6 +717,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   lp.st_touch = p->st ? p->st + 2 * rows : nullptr;
   unsigned long long* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
   lp.ovf = ovf_list;
+  lp.dom = nullptr;
   lp.parts = nullptr;
   lp.part_off = nullptr;
   lp.part_nnz = nullptr;
@@ -1173,7 +1221,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.cf_err = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCfFlags;  // (kCfOverflow)
     fp.c_cap = cap;
     int occ = 0;
-    rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ);
+    rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ, false, 0, kSplitVariant && split);
     if (rc) return fail_staged(rc);
     const unsigned grid = unsigned(std::min<uint64_t>(
         (ntiles + kFusedWarps - 1) / kFusedWarps, uint64_t(occ) * uint64_t(c->sms)));
@@ -1187,7 +1235,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       fp.g_sval = gv.sval;
     }
     tm.begin(3);
-    rc = fused_call(c, medium, 1, fp, wide, stats, grid, nullptr);
+    rc = fused_call(c, medium, 1, fp, wide, stats, grid, nullptr, false, 0, kSplitVariant && split);
     if (rc) return fail_staged(rc);
     tm.end(3);
     ++c->last_launches;
@@ -1197,6 +1245,8 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       cp.list = static_cast<const uint32_t*>(c->list.p);
       cp.prod = static_cast<const uint32_t*>(c->prod.p);
       cp.big = static_cast<const uint32_t*>(c->sub.p);
+      static const bool env_no_dom = std::getenv("SPMMM_NO_DOM") != nullptr;
+      cp.dom_big = (esc && !env_no_dom && !c->no_dom) ? cp.big + 4 * rows : nullptr;
       cp.ctrl = static_cast<const unsigned long long*>(c->ctrl.p);
       cp.tickets = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCopyTickets;
       cp.l_off = static_cast<const uint64_t*>(c->l_off.p);
@@ -1240,6 +1290,17 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     const unsigned long long f = c->h_ctrl[kCtrlFault];
     return cleanup(fail(SPMMM_ERR_CUDA, "k_fused look-back watchdog: site %llu tile %llu",
                         (f >> 48) & 0x7fff, f & ((1ull << 48) - 1)));
+  }
+  if (c->h_ctrl[kCtrlCfFlags] & kCfUnsorted) {
+    // a B row whose columns do not ascend (outside the storage contract, but
+    // the other kernels sort whatever they are given): once more without
+    // k_esc_dom, which merges its dominant B row as it is stored
+    cleanup(0);
+    tr.mark("unsorted B row met by k_esc_dom: redone without it");
+    c->no_dom = true;
+    rc = multiply_impl(c, a, b, strategy, flags, out);
+    c->no_dom = false;
+    return rc;
   }
   if (c->h_ctrl[kCtrlCfFlags] & kCfOverflow) {
     // C outgrew the reservation: once more, sized by the product count
@@ -2205,7 +2266,7 @@ int spmmm_context_destroy(spmmm_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->ctrl, &c->prod, &c->lmap, &c->list, &c->status, &c->l_off, &c->l_nnz,
-                    &c->ws, &c->gtab, &c->sub, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
+                    &c->ws, &c->gtab, &c->sub, &c->dom, &c->ell, &c->tr_scratch, &c->stage_ci, &c->stage_v, &c->a_rp, &c->a_ci,
                     &c->a_v, &c->b_rp, &c->b_ci, &c->b_v, &c->parts, &c->part_off, &c->part_nnz,
                     &c->row_parts, &c->scr_col, &c->scr_val, &c->aux, &c->ci32, &c->rp32, &c->d16, &c->dbase,
                     &c->part_sums, &c->dl_rp})
