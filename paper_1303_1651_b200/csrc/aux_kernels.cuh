@@ -47,18 +47,30 @@ enum Ctrl : int {
 // (esc.cuh); k_count sums their products for the host
 constexpr uint32_t kHugeMin = 5120;
 
-// Rows dominated by one long B row (skewed inputs: a short A row that hits a
-// long B row — a third of C5's products sit in such rows): the longest B row
-// of the row, L entries, holds at least half of its P products and at most
-// kDomRCap products come from the other entries. Such a row is the dominant
-// run — already sorted, distinct columns — merged with the few sorted others
+// Rows with a dominant B row (skewed inputs: an A row that hits a long B
+// row — a third of C5's products sit in such rows): the longest B row of the
+// row has L >= kDomMinRun entries, at least half of the row's P products,
+// and at most kDomRCap products come from the other entries. Such a row is the dominant run —
+// already sorted, distinct columns — merged with the few sorted others
 // (esc.cuh k_esc_dom) instead of P keys sorted from scratch. k_count records
 // the dominant entry (its offset in the A row; the first of the longest).
-constexpr uint32_t kDomRCap = 256;
-constexpr uint32_t kDomMinRun = 64;
+// (measured on C5: cap 256 / run >= 64 / at least half of the row, the rule
+// below, 3.33 ms; cap 512 / run >= 32 / any share moves 9M more products here
+// and ties, 3.33 ms — the others cost about what they cost the block kernels)
+#ifndef SPMMM_DOM_RCAP
+#define SPMMM_DOM_RCAP 256
+#endif
+#ifndef SPMMM_DOM_MINRUN
+#define SPMMM_DOM_MINRUN 64
+#endif
+constexpr uint32_t kDomRCap = SPMMM_DOM_RCAP;
+constexpr uint32_t kDomMinRun = SPMMM_DOM_MINRUN;
 constexpr uint32_t kNoDom = 0xffffffffu;
 __host__ __device__ inline bool dom_eligible(uint64_t P, uint64_t L) {
-  return L >= kDomMinRun && 2 * L >= P && P - L <= kDomRCap;
+#ifndef SPMMM_DOM_ANY_SHARE
+  if (2 * L < P) return false;
+#endif
+  return L >= kDomMinRun && P - L <= kDomRCap;
 }
 
 
@@ -838,30 +850,38 @@ struct CopyParams {
 // one warp each. Both take rows dynamically.
 // One staged run to its slot of C: U loads in flight per thread (a plain
 // load -> store loop is one memory round trip per step).
+#ifndef SPMMM_COPY_U
+#define SPMMM_COPY_U 4
+#endif
 template <int U>
 __device__ __forceinline__ void copy_run(unsigned long long* __restrict__ dci,
                                          double* __restrict__ dv,
                                          const uint32_t* __restrict__ sci,
                                          const double* __restrict__ sv, uint32_t n,
                                          uint32_t t0, uint32_t step) {
-  uint32_t i = t0;
-  for (; i + (U - 1) * step < n; i += U * step) {
+  // U loads in flight per thread whatever n is (most staged rows are a few
+  // dozen entries: a loop that needs U * step of them to unroll never does)
+  for (uint32_t i = t0; i < n; i += U * step) {
     unsigned long long c[U];
     double v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      c[u] = (unsigned long long)__ldcs(sci + i + u * step);
-      v[u] = __ldcs(sv + i + u * step);
+      const uint32_t j = i + u * step;
+      c[u] = 0;
+      v[u] = 0.0;
+      if (j < n) {
+        c[u] = (unsigned long long)__ldcs(sci + j);
+        v[u] = __ldcs(sv + j);
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      __stcs(dci + i + u * step, c[u]);
-      __stcs(dv + i + u * step, v[u]);
+      const uint32_t j = i + u * step;
+      if (j < n) {
+        __stcs(dci + j, c[u]);
+        __stcs(dv + j, v[u]);
+      }
     }
-  }
-  for (; i < n; i += step) {
-    __stcs(dci + i, (unsigned long long)__ldcs(sci + i));
-    __stcs(dv + i, __ldcs(sv + i));
   }
 }
 
@@ -887,7 +907,7 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
         continue;
       }
       const uint64_t dsrc = p.l_off[dl];
-      copy_run<4>(cci + ddst, p.c_v + ddst, p.l_ci + dsrc, p.l_v + dsrc, dcnt, threadIdx.x,
+      copy_run<SPMMM_COPY_U>(cci + ddst, p.c_v + ddst, p.l_ci + dsrc, p.l_v + dsrc, dcnt, threadIdx.x,
                   blockDim.x);
       continue;
     }
@@ -904,7 +924,7 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
           if (threadIdx.x == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
           break;
         }
-        copy_run<4>(cci + d, p.c_v + d, p.l_ci + so, p.l_v + so, pc, threadIdx.x, blockDim.x);
+        copy_run<SPMMM_COPY_U>(cci + d, p.c_v + d, p.l_ci + so, p.l_v + so, pc, threadIdx.x, blockDim.x);
         d += pc;
       }
       continue;
@@ -915,7 +935,7 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
       if (threadIdx.x == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
       continue;
     }
-    copy_run<4>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, threadIdx.x, blockDim.x);
+    copy_run<SPMMM_COPY_U>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, threadIdx.x, blockDim.x);
   }
   // the other listed rows (<= long_min products): one warp each, static
   // assignment (their costs are alike; no ticket traffic)
@@ -932,7 +952,7 @@ __global__ void __launch_bounds__(256) k_copy_long(CopyParams p) {
       if (lane == 0) atomicOr(p.overflow, (unsigned long long)kCfOverflow);
       continue;
     }
-    copy_run<4>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, lane, 32);
+    copy_run<SPMMM_COPY_U>(cci + dst, p.c_v + dst, p.l_ci + src, p.l_v + src, cnt, lane, 32);
   }
 }
 

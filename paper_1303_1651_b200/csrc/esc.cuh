@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
 // storage contract of formats.py:40-46 — are streamed, 32 per step, straight
 // from B to the staged result, and merged on the way with the row's other
 // <= kDomRCap products, which are expanded and sorted as in k_esc_warp (key
-// col << 8 | qR, qR their product order). A column of the others is folded
+// col << kDomQBits | qR, qR their product order). A column of the others is folded
 // left to right in product order from 0.0; where the dominant row has the
 // same column its product joins the fold at its place in the order: after the
 // products of earlier A entries (qR < n_before), before the later ones. So
@@ -319,7 +319,8 @@ constexpr int kDomWarps = 8;
 #define SPMMM_DOM_BLOCKS 4
 #endif
 constexpr int kDomBlocks = SPMMM_DOM_BLOCKS;  // resident blocks per SM
-constexpr int kDomQBits = 8;
+constexpr int kDomQBits = kDomRCap <= 256 ? 8 : 9;
+static_assert(kDomRCap <= 512 && kDomQBits <= kEscQBits, "the others: one warp sort, ESC-mode column bits");
 static_assert((1u << kDomQBits) >= kDomRCap, "qR bits");
 
 __host__ __device__ constexpr size_t esc_dom_smem_bytes() {
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kDomWarps * 32, kDomBlocks) k_esc_dom(const Lo
     const uint64_t bsd = ld_idx(p.B.rp + kd, p.B.pol);
     const uint32_t L = uint32_t(ld_idx(p.B.rp + kd + 1, p.B.pol) - bsd);
     const uint32_t nR = P - L;
-    // ---- expand the other entries: skey[qR] = col << 8 | qR, sval[qR] = a * b ----
+    // ---- expand the other entries: skey[qR] = col << kDomQBits | qR, sval[qR] = a * b ----
     uint32_t base = 0, n_before = 0;
 #pragma unroll 1
     for (uint64_t ab = lo; ab < hi && nR; ab += 32) {
@@ -939,14 +940,17 @@ __global__ void __launch_bounds__(kEscThreads, 2) k_esc_block(LongParams p, uint
     }
     // buckets: nb (power of two) column ranges of 2^sh columns from cmin,
     // ~kEscBucketAvg keys each; in-bucket key = offset << qb | q
-    uint32_t nb = 2;
-    while (nb * kEscBucketAvg < P && nb < kEscMaxBuckets) nb <<= 1;
+    // nb: the smallest power of two >= max(2, P / kEscBucketAvg), at most kEscMaxBuckets
+    const uint32_t want = (P + kEscBucketAvg - 1) / kEscBucketAvg;
+    uint32_t nb = want <= 2 ? 2u : 1u << (32 - __clz(want - 1));
+    nb = nb < kEscMaxBuckets ? nb : kEscMaxBuckets;
     for (uint32_t b = tid; b < nb; b += NT) hist[b] = 0;
     if (tid == 0) s_bt = NT / 32;  // buckets below were taken statically
     __syncthreads();
     const uint32_t cmin = s_min, range = s_max - cmin;
-    uint32_t sh = 0;
-    while ((range >> sh) >= nb) ++sh;
+    // the smallest sh with (range >> sh) < nb: bits(range) - log2(nb), if positive
+    const int shs = (32 - __clz(range)) - (31 - __clz(nb));
+    const uint32_t sh = shs > 0 ? uint32_t(shs) : 0u;
     // ---- partition: histogram, bucket starts, scatter ----
     for (uint32_t q = tid; q < P; q += NT) atomicAdd(hist + ((scol[q] - cmin) >> sh), 1u);
     __syncthreads();

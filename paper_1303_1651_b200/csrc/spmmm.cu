@@ -618,9 +618,6 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
                      esc_block_smem_bytes(kEscBlockCap)));
         c->esc_attr[stats] = true;
       }
-      // the warp rows are independent of the block rows: their kernel runs on
-      // a second stream, overlapping k_esc_plan / k_esc_block (all three are
-      // latency bound); the context stream joins it before k_fused
       if (dom) {
         // the dominated rows first, with the whole GPU: a latency-bound stream of
         // B rows to the staged result (behind the other ESC kernels' resident
@@ -649,6 +646,9 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
         tm.end(13);
         ++c->last_launches;
       }
+      // the warp rows are independent of the block rows: their kernel runs on
+      // a second stream, overlapping k_esc_plan / k_esc_block (all three are
+      // latency bound); the context stream joins it before k_fused
       static const bool serial = std::getenv("SPMMM_SERIAL_ESC") != nullptr;
       cudaStream_t ws = c->stream;
       if (!serial) {

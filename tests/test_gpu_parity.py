@@ -338,6 +338,96 @@ def test_split_mode_esc_kernels(case, values):
     assert np.array_equal(_choices_array(stats, a.rows), ref.row_choices)
 
 
+def _dominated_operands(rng, values, window):
+    """A: many short rows, a few wider ones; B: one row in 25 is long
+    (64..3000 entries; non-short rows of C stay a minority: split mode). So many rows of C are one long B row plus a few other
+    products (k_esc_dom), with every tie-break shape: the dominant entry
+    first, last and in the middle of its A row, columns shared between the
+    dominant row and the others (`window` crowds them), exact cancellations."""
+    n = 20_000
+    cols = 60_000
+
+    def mk(rows, lens, span):
+        rp = np.zeros(rows + 1, np.uint64)
+        rp[1:] = np.cumsum(lens)
+        parts = [np.sort(rng.choice(span, int(k), replace=False)) for k in lens]
+        ci = np.concatenate(parts).astype(np.uint64)
+        if values == "quantized":
+            v = rng.choice([-2.0, -1.0, 1.0, 2.0], ci.size)
+        elif values == "zeros":
+            v = rng.choice([0.0, -0.0, 1.0, -1.0], ci.size)
+        else:
+            v = rng.uniform(-1.0, 1.0, ci.size)
+        return rp, ci, v
+
+    lb = np.where(rng.random(n) < 0.04, rng.integers(64, 3000, n), rng.integers(0, 6, n))
+    brp, bci, bv = mk(n, lb, window)
+    la = np.where(rng.random(n) < 0.03, rng.integers(20, 200, n), rng.integers(0, 5, n))
+    arp, aci, av = mk(n, la, n)
+    return CsrMatrix(n, n, arp, aci, av), CsrMatrix(n, cols, brp, bci, bv)
+
+
+@pytest.mark.parametrize("window", [60_000, 4_000])
+@pytest.mark.parametrize("values", ["uniform", "quantized", "zeros"])
+@pytest.mark.parametrize("with_stats", [False, True])
+def test_split_mode_dominant_rows(values, window, with_stats):
+    """Rows that are one long B row plus a few other products are merged by
+    k_esc_dom (the dominant run streamed from B, the others sorted and merged
+    in on the way): bitwise against the oracle, with the reference's row
+    choices, and the kernel must actually have run."""
+    rng = np.random.default_rng(17)
+    a, b = _dominated_operands(rng, values, window)
+    ref = oracle.multiply_rowmajor(a, b, row_choices=True, threads=8)
+    ctx = _lib.Context(0)
+    va, vb = (_lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values),
+              _lib.csr_view(b.rows, b.cols, b.row_ptr, b.col_idx, b.values))
+    flags = _lib.FLAG_TIMING | (_lib.FLAG_ROW_STATS if with_stats else 0)
+    with _lib.multiply_views(ctx, va, vb, 6, flags) as p:
+        rp, ci, v = p.download()
+        names = set(ctx.last_timings())
+        mults = p.multiplications
+        if with_stats:
+            stats = KernelStats()
+            from paper_1303_1651_b200.kernels import _record_row_choices
+            _record_row_choices(stats, p, StrategyKind, a.row_ptr)
+    ctx.close()
+    assert "k_esc_dom" in names, names
+    assert mults == ref.multiplications
+    assert_csr_bitwise_equal(CsrMatrix(a.rows, b.cols, rp, ci, v),
+                             CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx, ref.values),
+                             f"dom/{values}/{window}")
+    if with_stats:
+        assert np.array_equal(_choices_array(stats, a.rows), ref.row_choices)
+
+
+def test_dominant_row_with_unsorted_b_row_is_redone():
+    """k_esc_dom merges its dominant B row as it is stored. Ascending columns
+    are the storage contract (formats.py:40-46), but the reference's kernel
+    sorts whatever it is given and so do the other kernels: a B row whose
+    columns do not ascend is reported by k_esc_dom and the product redone
+    without it — the reference's bytes either way."""
+    rng = np.random.default_rng(23)
+    a, b = _dominated_operands(rng, "quantized", 60_000)
+    bci = b.col_idx.copy()
+    lens = np.diff(b.row_ptr.astype(np.int64))
+    for r in np.flatnonzero(lens >= 64)[:50]:  # swap two entries' columns inside long rows
+        s = int(b.row_ptr[r])
+        bci[s + 3], bci[s + 40] = bci[s + 40], bci[s + 3]
+    b2 = CsrMatrix(b.rows, b.cols, b.row_ptr.copy(), bci, b.values.copy())
+    ref = oracle.multiply_rowmajor(a, b2, threads=8)
+    ctx = _lib.Context(0)
+    va, vb = (_lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values),
+              _lib.csr_view(b2.rows, b2.cols, b2.row_ptr, b2.col_idx, b2.values))
+    with _lib.multiply_views(ctx, va, vb, 6, _lib.FLAG_TIMING) as p:
+        rp, ci, v = p.download()
+        names = set(ctx.last_timings())
+    ctx.close()
+    assert "k_esc_dom" not in names, names  # (the timings are the redo's)
+    assert_csr_bitwise_equal(CsrMatrix(a.rows, b2.cols, rp, ci, v),
+                             CsrMatrix(ref.rows, ref.cols, ref.row_ptr, ref.col_idx, ref.values),
+                             "dom/unsorted")
+
+
 def _host_views(a, b):
     return (_lib.csr_view(a.rows, a.cols, a.row_ptr, a.col_idx, a.values),
             _lib.csr_view(b.rows, b.cols, b.row_ptr, b.col_idx, b.values))
