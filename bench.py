@@ -347,10 +347,28 @@ def dominant_kernel(kernel_ms):
     return dom if dom in ("k_fused", "k_esc_block") else "k_fused"
 
 
-def esc_units(prod_per_row):
-    """k_esc_block's units: the products of the rows past kEscWarpLimit (512)
-    — the rows it computes (mid rows whole, huge rows as column-range parts)."""
-    return int(prod_per_row[prod_per_row > 512].sum())
+def esc_units(a, b, prod_per_row):
+    """k_esc_block's units: the products of the rows it computes — rows past
+    the warp-row limit (mid rows whole, huge rows as column-range parts) that
+    are not dominated by one long B row (those are k_esc_dom's). The limits
+    are the library's own (spmmm_row_classes)."""
+    import ctypes
+
+    from paper_1303_1651_b200 import _lib
+
+    lim = (ctypes.c_uint32 * 5)()
+    _lib.check(_lib.lib().spmmm_row_classes(lim), "spmmm_row_classes")
+    warp_limit, _, rcap, minrun, half = (int(x) for x in lim)
+    arp = a.row_ptr.astype(np.int64)
+    lens_b = np.diff(b.row_ptr.astype(np.int64))[a.col_idx.astype(np.int64)]
+    longest = np.zeros(a.rows, np.int64)
+    nz = np.flatnonzero(np.diff(arp) > 0)
+    if nz.size:
+        longest[nz] = np.maximum.reduceat(lens_b, arp[nz])
+    dominated = (longest >= minrun) & (prod_per_row - longest <= rcap)
+    if half:
+        dominated &= 2 * longest >= prod_per_row
+    return int(prod_per_row[(prod_per_row > warp_limit) & ~dominated].sum())
 
 
 # ---------------------------------------------------------------------------
@@ -430,7 +448,7 @@ def run_single(args):
     dom = dominant_kernel(kernel_ms)
     units = mults
     if dom == "k_esc_block":
-        units = esc_units(np.diff(row_products_prefix(a, b).astype(np.int64)))
+        units = esc_units(a, b, np.diff(row_products_prefix(a, b).astype(np.int64)))
     roof = roofline_entry(label, kernel_ms.get(dom, 0.0) / args.steps, dom, balg, units, mults,
                           nnz_c, a.rows, nnz_a, len(b.values), b.rows, ms_per_step, 1)
     line = {
@@ -660,7 +678,7 @@ def run_distributed(args, rank, world, local_rank):
         if dom == "k_esc_block":
             from paper_1303_1651_b200.kernels import row_products_prefix
 
-            units = esc_units(np.diff(row_products_prefix(a, b).astype(np.int64)))
+            units = esc_units(a, b, np.diff(row_products_prefix(a, b).astype(np.int64)))
         roof = roofline_entry(label, kmax.get(dom, 0.0), dom, balg, units, total_mults, total_nnz,
                               a.rows, nnz_a, len(b.values), b.rows, ms_per_step, world)
         roof["note"] = ("achieved = all ranks' algorithmic bytes / the slowest rank's kernel "

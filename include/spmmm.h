@@ -102,6 +102,14 @@ int spmmm_multiply(spmmm_context* ctx, const spmmm_csr* a, const spmmm_csr* b, i
  * kernels.py:330-331 == perfmodel.count_mults). */
 int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
                         uint64_t* multiplications);
+/* The split-mode row classes, for measurement tools (bench.py attributes the
+ * products of a skewed input to the kernels that compute them):
+ * out[0] products up to which a non-short row is one warp's (k_esc_warp),
+ * out[1] products past which a row is cut into column-range parts,
+ * out[2..4] the dominant-row rule (k_esc_dom): at most out[2] products outside
+ * the row's longest B row, which has at least out[3] entries and, if out[4],
+ * at least half of the row's products. */
+int spmmm_row_classes(uint32_t out[5]);
 /* Device bytes held by the product's arrays (their reservations: C's
  * col_idx/values are reserved before nnz(C) is known). */
 int spmmm_product_reserved_bytes(const spmmm_product* p, uint64_t* bytes);

@@ -38,7 +38,7 @@ EXPORTS = (
     "spmmm_abi_version", "spmmm_last_error", "spmmm_device_count",
     "spmmm_context_create", "spmmm_context_destroy", "spmmm_synchronize",
     "spmmm_multiply", "spmmm_multiply_host", "spmmm_product_shape", "spmmm_product_device_arrays",
-    "spmmm_product_reserved_bytes",
+    "spmmm_product_reserved_bytes", "spmmm_row_classes",
     "spmmm_product_download", "spmmm_product_copy_device", "spmmm_product_row_stats",
     "spmmm_product_destroy", "spmmm_estimate_nnz", "spmmm_row_products_prefix",
     "spmmm_transpose", "spmmm_partition_rows", "spmmm_product_download_offset",
@@ -112,6 +112,7 @@ def _declare(lib):
         "spmmm_product_shape": (i, [vp, p_u64, p_u64, p_u64, p_u64]),
         "spmmm_product_device_arrays": (i, [vp, pp, pp, pp]),
         "spmmm_product_reserved_bytes": (i, [vp, p_u64]),
+        "spmmm_row_classes": (i, [ctypes.POINTER(ctypes.c_uint32)]),
         "spmmm_product_download": (i, [vp, vp, vp, vp]),
         "spmmm_multiply_host": (i, [vp, ctypes.POINTER(SpmmmCsr), ctypes.POINTER(SpmmmCsr), i,
                                     ctypes.c_uint32, i, ctypes.POINTER(SpmmmHostCsr)]),

@@ -79,12 +79,63 @@ __host__ __device__ inline bool dom_eligible(uint64_t P, uint64_t L) {
 // consecutive rows (one per lane); rows with many A entries are summed by the
 // whole warp so a 4096-entry row does not stall its 31 neighbours.
 // Also zeroes k_fused's look-back counters (`zero`, `nzero` words) on the way.
-__global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
+// Split-mode row lists, built by k_count itself on the assumption that the
+// product will run in split mode with the ESC kernels (the host knows only
+// after reading k_count's totals; when it decides otherwise it resets the
+// counters and k_collect lists the rows by that mode's limits). Saves the
+// k_collect pass on skewed inputs (C5: 0.08 ms).
+struct RowLists {
+  uint32_t* list;       // every non-short row (null: k_count builds no lists)
+  uint32_t* lmap;       // row -> its index in list
+  uint32_t* mid_list;   // rows past mid_min products (one block each)
+  uint32_t* huge_list;  // rows past huge_min products (column-range parts)
+  uint32_t* dom_list;   // dominated rows (k_esc_dom), whatever their size
+  uint32_t* dom_big;    // ... those past mid_min (block copy)
+  uint32_t mid_min, huge_min;
+};
+
+// Append this warp's long rows (lane: row r, pr products, dominant entry dv)
+// to the lists; every lane of the warp calls it.
+__device__ __forceinline__ void list_rows(const RowLists& L, unsigned long long* ctrl, bool is_long,
+                                          uint64_t r, uint32_t pr, uint32_t dv) {
+  const uint32_t m = __ballot_sync(kFull, is_long);
+  if (!m) return;
+  const bool is_dom = is_long && dv != 0xffffffffu;
+  const uint32_t md = __ballot_sync(kFull, is_dom);
+  uint32_t base = 0, dbase = 0;
+  if (lane_id() == 0) {
+    base = uint32_t(atomicAdd(ctrl + kCtrlLongRows, (unsigned long long)__popc(m)));
+    if (md) dbase = uint32_t(atomicAdd(ctrl + kCtrlDomRows, (unsigned long long)__popc(md)));
+  }
+  base = __shfl_sync(kFull, base, 0);
+  dbase = __shfl_sync(kFull, dbase, 0);
+  if (is_long) {
+    const uint32_t idx = base + __popc(m & lanemask_lt());
+    L.list[idx] = uint32_t(r);
+    L.lmap[r] = idx;
+    // rows per computing kernel (the others are few: plain atomics)
+    if (is_dom) {
+      L.dom_list[dbase + __popc(md & lanemask_lt())] = idx;
+      if (pr > L.mid_min) L.dom_big[atomicAdd(ctrl + kCtrlDomBigRows, 1ull)] = idx;
+    } else if (pr > L.huge_min) {
+      L.huge_list[atomicAdd(ctrl + kCtrlHugeRows, 1ull)] = idx;
+    } else if (pr > L.mid_min) {
+      L.mid_list[atomicAdd(ctrl + kCtrlMidRows, 1ull)] = idx;
+    }
+  }
+}
+
+// (64 registers, 4 blocks per SM: with the per-row dominant-entry tracking the
+// kernel took 90 and ran 2; C5 0.30 -> 0.22 ms, C4 0.13 -> 0.10)
+#ifndef SPMMM_COUNT_BLOCKS
+#define SPMMM_COUNT_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, SPMMM_COUNT_BLOCKS) k_count(DevCsr A, DevCsr B, uint32_t* __restrict__ prod,
                                                unsigned long long* __restrict__ ctrl,
                                                unsigned long long* __restrict__ zero,
                                                uint64_t nzero, uint4* __restrict__ ell_self,
                                                uint4* __restrict__ ell_all,
-                                               uint32_t* __restrict__ dom) {
+                                               uint32_t* __restrict__ dom, const RowLists lists) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nzero;
        i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = 0;
@@ -205,10 +256,12 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
     // C = A·A: row r of A is row r of B — its ELL record is written here, from
     // entries this lane has just read, instead of by a k_pack_ell pass
     if (ell_self && r < A.rows && hi - lo <= uint64_t(kEllSlots)) pack_ell_record(A, r, lo, hi, ell_self);
+    uint32_t dv = kNoDom;
     if (r < A.rows) {
       if (p > 0x7fffffffull) err |= 8u;
       prod[r] = uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p);
-      if (dom) dom[r] = (p <= 0x7fffffffull && dom_eligible(p, rl)) ? re : kNoDom;
+      if (p <= 0x7fffffffull && dom_eligible(p, rl)) dv = re;
+      if (dom) dom[r] = dv;
       tot += p;
       huge += p > kHugeMin ? p : 0;
       mx = p > mx ? p : mx;
@@ -217,6 +270,9 @@ __global__ void __launch_bounds__(256) k_count(DevCsr A, DevCsr B, uint32_t* __r
         ++nonshort;
       }
     }
+    if (lists.list)
+      list_rows(lists, ctrl, r < A.rows && (p > 32 || (p > 0 && hi - lo > 32)), r,
+                uint32_t(p > 0x7fffffffull ? 0x7fffffffull : p), dv);
   }
   // speculative ELL copy of every B row (A != B, B rows of ~kEllSlots
   // entries): the bandwidth-bound copy interleaves with the latency-bound
@@ -451,15 +507,10 @@ __global__ void __launch_bounds__(256) k_pack_ell(DevCsr B, uint64_t a_rows,
 // ---------------------------------------------------------------------------
 // K2: list the long rows (warp-aggregated append; order is irrelevant).
 __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __restrict__ prod,
-                                                 uint32_t medium_limit, uint32_t mid_min,
-                                                 uint32_t huge_min, uint32_t* __restrict__ list,
-                                                 uint32_t* __restrict__ lmap,
-                                                 uint32_t* __restrict__ mid_list,
-                                                 uint32_t* __restrict__ huge_list,
+                                                 uint32_t medium_limit,
                                                  unsigned long long* __restrict__ ctrl,
                                                  const uint32_t* __restrict__ dom,
-                                                 uint32_t* __restrict__ dom_list,
-                                                 uint32_t* __restrict__ dom_big) {
+                                                 const RowLists lists) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t start = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   // warp-uniform trip count so the ballots are full-warp
@@ -473,28 +524,7 @@ __global__ void __launch_bounds__(256) k_collect(DevCsr A, const uint32_t* __res
       pr = prod[r];
       is_long = classify(pr, na, medium_limit) == kRowLong;
     }
-    const uint32_t m = __ballot_sync(kFull, is_long);
-    if (!m) continue;
-    const bool is_dom = is_long && dom && dom[r] != kNoDom;
-    const uint32_t md = __ballot_sync(kFull, is_dom);
-    uint32_t base = 0, dbase = 0;
-    if (lane_id() == 0) {
-      base = uint32_t(atomicAdd(ctrl + kCtrlLongRows, (unsigned long long)__popc(m)));
-      if (md) dbase = uint32_t(atomicAdd(ctrl + kCtrlDomRows, (unsigned long long)__popc(md)));
-    }
-    base = __shfl_sync(kFull, base, 0);
-    dbase = __shfl_sync(kFull, dbase, 0);
-    if (is_long) {
-      const uint32_t idx = base + __popc(m & lanemask_lt());
-      list[idx] = uint32_t(r);
-      lmap[r] = idx;
-      // rows per computing kernel (the others are few: plain atomics)
-      if (is_dom) {
-        dom_list[dbase + __popc(md & lanemask_lt())] = idx;
-        if (pr > mid_min) dom_big[atomicAdd(ctrl + kCtrlDomBigRows, 1ull)] = idx;
-      } else if (pr > huge_min) huge_list[atomicAdd(ctrl + kCtrlHugeRows, 1ull)] = idx;
-      else if (pr > mid_min) mid_list[atomicAdd(ctrl + kCtrlMidRows, 1ull)] = idx;
-    }
+    list_rows(lists, ctrl, is_long, r, pr, (is_long && dom) ? dom[r] : kNoDom);
   }
 }
 

@@ -147,6 +147,7 @@ struct spmmm_context {
   DevBuf sub;                                // per-kernel row sub-lists
   DevBuf dom;                                // per row: its dominant entry (k_count -> k_esc_dom)
   bool no_dom = false;                       // the next counted product runs without k_esc_dom
+  bool lists_from_count = false;             // k_count built the split-mode (ESC) row lists
   DevBuf ell;                                // ELL records of B (short rows)
   DevBuf tr_scratch;                         // storage-order conversion scratch
   DevBuf parts, part_off, part_nnz, row_parts, scr_col, scr_val;  // ESC parts of huge rows
@@ -348,9 +349,38 @@ uint64_t lb_counters_max(uint64_t rows) {
   return total;
 }
 
+// The row lists in the context's buffers (list, lmap; sub: mid, huge, overflow,
+// dominated, dominated past the block-copy limit — `rows` entries each).
+RowLists row_lists(spmmm_context* c, uint64_t rows, uint32_t mid_min, uint32_t huge_min) {
+  RowLists l{};
+  l.list = static_cast<uint32_t*>(c->list.p);
+  l.lmap = static_cast<uint32_t*>(c->lmap.p);
+  l.mid_list = static_cast<uint32_t*>(c->sub.p);
+  l.huge_list = l.mid_list + rows;
+  l.dom_list = l.mid_list + 3 * rows;
+  l.dom_big = l.mid_list + 4 * rows;
+  l.mid_min = mid_min;
+  l.huge_min = huge_min;
+  return l;
+}
+
 int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, bool pack = false) {
   CUDA_TRY(ensure(c->prod, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->dom, std::max<uint64_t>(A.rows, 1) * sizeof(uint32_t), c->stream));
+  // the product path: k_count also lists the non-short rows as split mode
+  // with the ESC kernels wants them (RowLists, aux_kernels.cuh)
+  RowLists lists{};
+  c->lists_from_count = false;
+  static const bool env_no_dom = std::getenv("SPMMM_NO_DOM") != nullptr;
+  static const bool env_no_esc = std::getenv("SPMMM_NO_ESC") != nullptr;
+  if (pack && A.rows && !env_no_dom && !env_no_esc && !c->no_dom &&
+      B.cols <= (1ull << kEscColBits)) {
+    CUDA_TRY(ensure(c->lmap, A.rows * sizeof(uint32_t), c->stream));
+    CUDA_TRY(ensure(c->list, A.rows * sizeof(uint32_t), c->stream));
+    CUDA_TRY(ensure(c->sub, 5 * A.rows * sizeof(uint32_t), c->stream));
+    lists = row_lists(c, A.rows, kEscWarpLimit, kEscBlockCap);
+    c->lists_from_count = true;
+  }
   // status: counters + words for one row per tile (the medium layout, the largest)
   const uint64_t ncnt = pack ? lb_counters_max(A.rows) : 0;
   if (pack) {
@@ -385,7 +415,8 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
         A, B, static_cast<uint32_t*>(c->prod.p), static_cast<unsigned long long*>(c->ctrl.p),
         static_cast<unsigned long long*>(c->status.p), ncnt,
         self_pack ? static_cast<uint4*>(c->ell.p) : nullptr,
-        spec_pack ? static_cast<uint4*>(c->ell.p) : nullptr, static_cast<uint32_t*>(c->dom.p));
+        spec_pack ? static_cast<uint4*>(c->ell.p) : nullptr, static_cast<uint32_t*>(c->dom.p),
+        lists);
     CUDA_TRY(cudaGetLastError());
     tm.end(0);
     ++c->last_launches;
@@ -529,8 +560,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   uint32_t* mid_list = static_cast<uint32_t*>(c->sub.p);
   uint32_t* huge_list = mid_list + rows;
   uint32_t* ovf_list = mid_list + 2 * rows;
-  uint32_t* dom_list = mid_list + 3 * rows;
-  uint32_t* dom_big = mid_list + 4 * rows;
+  uint32_t* dom_list = mid_list + 3 * rows;  // (+ 4 * rows: those past the block-copy limit)
   // ESC mode: rows dominated by one long B row go to k_esc_dom (SPMMM_NO_DOM=1,
   // or a B row found unsorted by it: all of them through the other kernels)
   static const bool env_no_dom = std::getenv("SPMMM_NO_DOM") != nullptr;
@@ -578,13 +608,21 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     c->ws_grid = grid;
   }
   tr.mark("  run_long: workspace");
-  {
+  if (!(c->lists_from_count && esc && dom)) {
+    // k_count's lists (if any) assumed split mode with every ESC kernel:
+    // list the rows by this mode's limits instead
+    unsigned long long* ctrl = static_cast<unsigned long long*>(c->ctrl.p);
+    if (c->lists_from_count) {
+      CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlLongRows, 0, 8, c->stream));
+      CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlMidRows, 0, 16, c->stream));  // (and kCtrlHugeRows)
+      CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlDomBigRows, 0, 8, c->stream));
+      CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlDomRows, 0, 8, c->stream));
+    }
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(1);
     k_collect<<<unsigned(blocks), 256, 0, c->stream>>>(
-        A, static_cast<const uint32_t*>(c->prod.p), list_limit, long_min, huge_min,
-        static_cast<uint32_t*>(c->list.p), static_cast<uint32_t*>(c->lmap.p), mid_list, huge_list,
-        static_cast<unsigned long long*>(c->ctrl.p), dom, dom_list, dom_big);
+        A, static_cast<const uint32_t*>(c->prod.p), list_limit, ctrl, dom,
+        row_lists(c, rows, long_min, huge_min));
     CUDA_TRY(cudaGetLastError());
     tm.end(1);
     ++c->last_launches;
@@ -2321,6 +2359,20 @@ int spmmm_product_shape(const spmmm_product* p, uint64_t* rows, uint64_t* cols, 
   if (cols) *cols = p->cols;
   if (nnz) *nnz = p->nnz;
   if (mults) *mults = p->mults;
+  return SPMMM_OK;
+}
+
+int spmmm_row_classes(uint32_t out[5]) {
+  if (!out) return fail(SPMMM_ERR_INVALID, "NULL argument");
+  out[0] = kEscWarpLimit;
+  out[1] = kHugeMin;
+  out[2] = kDomRCap;
+  out[3] = kDomMinRun;
+#ifndef SPMMM_DOM_ANY_SHARE
+  out[4] = 1;
+#else
+  out[4] = 0;
+#endif
   return SPMMM_OK;
 }
 
