@@ -578,19 +578,43 @@ __device__ __forceinline__ void plan_segment(const LongParams& pp, uint64_t es, 
                                              uint32_t* cnt) {
   const uint32_t lane = lane_id();
   const float inv_w = 1.0f / float(width);
-  // entries from es (whose first product is row product gq) until product qe
-#pragma unroll 1
-  for (uint64_t ab = es; ab < ehi && gq < qe; ab += 32) {
-    const uint32_t na = uint32_t(ehi - ab < 32 ? ehi - ab : 32);
-    uint64_t bs = 0;
-    uint32_t len = 0;
-    double av = 0.0;
-    if (lane < na) {
-      const uint64_t k = ld_idx(pp.A.ci + ab + lane, pp.A.pol);
+  // entries from es (whose first product is row product gq) until product qe.
+  // Two-deep software pipeline over the chunks of 32 entries: while chunk i's
+  // products are loaded and placed, chunk i+1's B.row_ptr pairs and chunk
+  // i+2's A entries are in flight (the walk is a chain of dependent loads:
+  // A.col_idx -> B.row_ptr -> B.col_idx; unpipelined it is four round trips
+  // per ~170 products)
+  constexpr uint64_t kNone = ~0ull;
+  auto load_a = [&](uint64_t ab, uint64_t& k, double& av) {
+    k = kNone;
+    av = 0.0;
+    if (ab < ehi && ab + lane < ehi) {
+      k = ld_idx(pp.A.ci + ab + lane, pp.A.pol);
       if (SCATTER) av = ld_val(pp.A.v + ab + lane, pp.A.pol);
+    }
+  };
+  auto load_b = [&](uint64_t k, uint64_t& bs, uint32_t& len) {
+    bs = 0;
+    len = 0;
+    if (k != kNone) {
       bs = ld_idx(pp.B.rp + k, pp.B.pol);
       len = uint32_t(ld_idx(pp.B.rp + k + 1, pp.B.pol) - bs);
     }
+  };
+  uint64_t k1, k2, bs_n;
+  uint32_t len_n;
+  double av_n, av2;
+  load_a(es, k1, av_n);          // chunk 0's entries
+  load_b(k1, bs_n, len_n);       // chunk 0's B rows
+  load_a(es + 32, k2, av2);      // chunk 1's entries
+#pragma unroll 1
+  for (uint64_t ab = es; ab < ehi && gq < qe; ab += 32) {
+    const uint64_t bs = bs_n;
+    const uint32_t len = len_n;
+    const double av = av_n;
+    av_n = av2;
+    load_b(k2, bs_n, len_n);          // chunk i+1's B rows
+    load_a(ab + 64, k2, av2);         // chunk i+2's entries
     const uint32_t incl = warp_incl_scan(len);
     const uint32_t excl = incl - len;
     const uint32_t tot = __shfl_sync(kFull, incl, 31);

@@ -14,7 +14,7 @@ timeout -s KILL 900 python bench.py --impl reference --steps 5 --warmup 3 \
 timeout -s KILL 900 python bench.py > $OUT/bench_${TAG}_default.json 2> $OUT/bench_${TAG}_default.err
 echo "default rc=$?"
 if [ -z "${NOSWEEP:-}" ]; then TAG=$TAG STEPS=200 bash tools/gpu_sweep.sh; fi
-for spec in ${PROFILE:-C2:k_fused C2:k_prep C3:k_fused C4:k_fused C5:k_esc_block}; do
+for spec in ${PROFILE:-C2:k_fused C2:k_prep C3:k_fused C4:k_fused C5:k_esc_block C5:k_esc_dom C5:k_esc_warp C5:k_esc_plan C5:k_fused C5:k_copy_long C5:k_count}; do
   c=${spec%%:*}; k=${spec##*:}
   CMD="python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
   if [ ! -f $OUT/launches_${TAG}_$c.csv ]; then
