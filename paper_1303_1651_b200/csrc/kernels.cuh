@@ -44,6 +44,7 @@ struct FusedParams {
   uint64_t ntiles;
   uint32_t medium_limit;
   uint32_t a_is_b;  // A and B are the same arrays
+  uint32_t self_ell;  // ... row for row (C = A·A, count-free): a row's A entries are its ELL record
   uint32_t* g_keys;  // [#warps][kGlobalSlots] overflow tables (medium kernel)
   double* g_vals;
   uint32_t* g_scol;  // [#warps][2][kMediumLimit] staging of overflowed rows
@@ -171,6 +172,12 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     if (!cf_ell(ma, mb) || !*reinterpret_cast<const volatile unsigned long long*>(p.cf_ell_flag))
       p.ell = nullptr;
   }
+  // C = A·A through the ELL records: rows are read from their own records
+  // (short_rows), so the tile needs no A.row_ptr at all
+  bool self = false;
+#ifndef SPMMM_NO_SELF
+  if constexpr (CF) self = p.self_ell != 0 && p.ell != nullptr;
+#endif
   uint64_t cf_prods = 0;
 
   // the previous batch waits for its offsets; its metadata lives in s_meta*
@@ -248,9 +255,15 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     // ---- row bounds and classes of the tile: lane i owns row r0 + i ----
     uint64_t rpv = 0;
     uint32_t my_cls = kRowZero, my_na = 0, my_prod = 0;
-    if (lane <= uint32_t(R) && r0 + lane <= rows) rpv = ld_idx(p.A.rp + r0 + lane, p.A.pol);
+    if (!self && lane <= uint32_t(R) && r0 + lane <= rows)
+      rpv = ld_idx(p.A.rp + r0 + lane, p.A.pol);
     const uint64_t rpn = __shfl_down_sync(kFull, rpv, 1);
-    if (lane < uint32_t(R) && r0 + lane < rows) {
+    if (self) {
+      if (lane < uint32_t(R) && r0 + lane < rows) {
+        my_cls = kRowShort;  // (an empty row's record is empty: no products)
+        my_na = kEllSlots;
+      }
+    } else if (lane < uint32_t(R) && r0 + lane < rows) {
       my_na = uint32_t(rpn - rpv);
       if constexpr (CF) {
         my_cls = rpn > rpv ? uint32_t(kRowShort) : uint32_t(kRowZero);
@@ -291,7 +304,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       // neutral on C5.)
       const void* pf1 = nullptr;
       if constexpr (!MEDIUM) {
-        if (!SPLIT && p.ell && ngroups > 1) {
+        if (!SPLIT && !self && p.ell && ngroups > 1) {
           const uint32_t pi = lane >> 3, pe = lane & 7;
           const uint32_t src = uint32_t(kLock) + (pi < uint32_t(kLock) ? pi : 0u);
           const uint64_t plo = __shfl_sync(kFull, rpv, src);
@@ -351,7 +364,8 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
         uint32_t hprod[kLock];
         short_rows<kLock, WIDE, STATS, !MEDIUM && !SPLIT, CF>(p.A, p.B, p.ell, hlo, hna, hon, so, hnnz,
                                                     hmin, hmax, htouch, hprod,
-                                                    h == 0 ? pf1 : nullptr);
+                                                    h == 0 ? pf1 : nullptr, self,
+                                                    r0 + uint64_t(h * kLock));
         if constexpr (CF) {
 #pragma unroll
           for (int i = 0; i < kLock; ++i) cf_prods += hon[i] ? hprod[i] : 0u;

@@ -169,7 +169,8 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
                                            const bool (&on)[R], ShortOut (&out)[R],
                                            uint32_t (&nnz)[R], uint32_t (&smin)[R],
                                            uint32_t (&smax)[R], uint32_t (&stouch)[R],
-                                           uint32_t (&prods)[R], const void* pf = nullptr) {
+                                           uint32_t (&prods)[R], const void* pf = nullptr,
+                                           bool self = false, uint64_t row0 = 0) {
   using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   // narrow variant: every index and offset fits 32 bits (checked on the host)
   using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
@@ -180,8 +181,10 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
   bool fast = false;
   if constexpr (ELLOK) {
     fast = ell != nullptr;
+    if (!self) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) fast &= !on[i] || na[i] <= kEllEntries;
+      for (int i = 0; i < R; ++i) fast &= !on[i] || na[i] <= kEllEntries;
+    }
   }
   if (fast) {
     const uint32_t e = lane / kEllSlots, j = lane - e * kEllSlots;
@@ -192,7 +195,20 @@ __device__ __forceinline__ void short_rows(const DevCsr& A, const DevCsr& B,
       col[i] = kEmptyKey;
       p[i] = 0.0;
       bv[i] = 0.0;
-      if (on[i] && e < na[i]) {
+      if (self) {
+        // C = A·A, row for row: row r's A entries are its own record — no
+        // A.row_ptr / A.col_idx / A.values loads, one dependent level less
+        if (on[i] && e < uint32_t(kEllSlots)) {
+          const uint32_t* mine = ell + (row0 + uint64_t(i)) * kEllWords;
+          const uint32_t k = ld_u32(mine + e, B.pol);
+          p[i] = ld_val(reinterpret_cast<const double*>(mine + kEllValOff) + e, B.pol);
+          if (k != kEmptyKey) {
+            const uint32_t* rec = ell + uint64_t(k) * kEllWords;
+            col[i] = ld_u32(rec + j, B.pol);
+            bv[i] = ld_val(reinterpret_cast<const double*>(rec + kEllValOff) + j, B.pol);
+          }
+        }
+      } else if (on[i] && e < na[i]) {
         const uint64_t k = ld_idx(A.ci + lo[i] + e, A.pol);
         p[i] = ld_val(A.v + lo[i] + e, A.pol);
         // (count-free path: k_prep has checked every A column against B.rows)

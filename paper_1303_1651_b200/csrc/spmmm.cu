@@ -1018,6 +1018,7 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   fp.ntiles = ntiles;
   fp.medium_limit = 0;
   fp.a_is_b = (A.ci == B.ci && A.v == B.v) ? 1u : 0u;
+  fp.self_ell = (same && A.v == B.v && use_ell) ? 1u : 0u;
   fp.ell = reinterpret_cast<const uint32_t*>(ell);
   fp.st_min = p->st;
   fp.st_max = p->st ? p->st + rows : nullptr;

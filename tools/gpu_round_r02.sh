@@ -21,10 +21,14 @@ for spec in ${PROFILE:-C2:k_fused C2:k_prep C3:k_fused C4:k_fused C5:k_esc_block
     timeout -s KILL 300 $CMD > $OUT/plain_$c.log 2>&1 && \
     timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $OUT/launches_${TAG}_$c.csv $CMD > $OUT/ncu_launch_$c.log 2>&1; echo "launch list $c rc=$?"
+    SPMMM_PROFILE_DIR=$OUT/profiles python tools/profile_commit.py launches $OUT/launches_${TAG}_$c.csv $c $TAG > /dev/null
   fi
   timeout -s KILL 300 $CMD > $OUT/plain2_$c.log 2>&1 && \
   timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:$k \
       -s 3 -c 1 -o $OUT/${TAG}_${c}_$k -f $CMD > $OUT/ncu_full_${c}_$k.log 2>&1; echo "full $c $k rc=$?"
+  # the summaries are made on the box (the reports together pass gpurun_out's 64 MiB)
+  SPMMM_PROFILE_DIR=$OUT/profiles python tools/profile_commit.py full $OUT/${TAG}_${c}_$k.ncu-rep $c $k $TAG \
+      && rm -f $OUT/${TAG}_${c}_$k.ncu-rep
 done
 # the N > 1 path: one rank over NCCL (torchrun), and two ranks sharing the GPU over gloo
 timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=1 --master-addr=127.0.0.1 \

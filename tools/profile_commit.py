@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PDIR = os.path.join(ROOT, "profiles")
+PDIR = os.environ.get("SPMMM_PROFILE_DIR", os.path.join(ROOT, "profiles"))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
