@@ -3,8 +3,10 @@
 # default line, the C2 sweep, launch lists and ncu --set full captures of
 # the dominant kernels (each only after its command exited 0 without ncu).
 set -u
-OUT=gpurun_out; mkdir -p $OUT
+OUT=gpurun_out; mkdir -p $OUT/profiles
 TAG=${TAG:-r02}
+# the per-kernel DRAM bytes merge into the committed file's other entries
+cp profiles/${TAG}_traffic.json $OUT/profiles/ 2>/dev/null
 for c in ${CONFIGS:-C2 C3 C4 C5 C1}; do
   timeout -s KILL 900 python bench.py --config $c --steps ${STEPS:-200} --warmup 10 \
      > $OUT/bench_${TAG}_$c.json 2> $OUT/bench_${TAG}_$c.err; echo "bench $c rc=$?"
