@@ -570,6 +570,9 @@ struct LongParams {
   unsigned long long* ticket;         // dynamic row counter
   uint32_t* ovf;                      // cluster variant: rows handed on to k_long
   const uint32_t* dom;                // k_esc_dom: the dominant entry of each of its rows
+  const uint32_t* first;              // k_esc_dom: its rows past first_min products (taken first)
+  const unsigned long long* n_first;
+  uint32_t first_min;
   // ESC mode (esc.cuh): column-range parts of the huge rows
   struct PartDesc* parts;             // [max parts]
   uint64_t* part_off;                 // staging offset per part

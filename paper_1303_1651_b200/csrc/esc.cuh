@@ -319,6 +319,11 @@ constexpr int kDomWarps = 8;
 #define SPMMM_DOM_BLOCKS 4
 #endif
 constexpr int kDomBlocks = SPMMM_DOM_BLOCKS;  // resident blocks per SM
+// (2, 3, 4, 6 measured the same on C5 once the long rows start first)
+#ifndef SPMMM_DOM_AHEAD
+#define SPMMM_DOM_AHEAD 2
+#endif
+constexpr int kDomAhead = SPMMM_DOM_AHEAD;  // steps of the dominant run in flight
 constexpr int kDomQBits = kDomRCap <= 256 ? 8 : 9;
 static_assert(kDomRCap <= 512 && kDomQBits <= kEscQBits, "the others: one warp sort, ESC-mode column bits");
 static_assert((1u << kDomQBits) >= kDomRCap, "qR bits");
@@ -338,16 +343,20 @@ __global__ void __launch_bounds__(kDomWarps * 32, kDomBlocks) k_esc_dom(const Lo
   p.B.pol = policy_evict_last();
   p.A.pol = policy_evict_first();
   const uint32_t n_rows = uint32_t(*(volatile const unsigned long long*)p.n_sub);
+  const uint32_t n_first = p.first ? uint32_t(*(volatile const unsigned long long*)p.n_first) : 0u;
   constexpr uint32_t qmask = (1u << kDomQBits) - 1u;
 #pragma unroll 1
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(p.ticket, 1ull);
     const uint32_t tr = uint32_t(__shfl_sync(kFull, t, 0));
-    if (tr >= n_rows) break;
-    const uint32_t li = p.sub[tr];
+    // the longer rows first (a 4096-entry dominant run is 128 dependent
+    // steps: started last it would be the kernel's tail), then the others
+    if (tr >= n_first + n_rows) break;
+    const uint32_t li = tr < n_first ? p.first[tr] : p.sub[tr - n_first];
     const uint32_t r = p.list[li];
     const uint32_t P = p.prod[r];
+    if (tr >= n_first && P > p.first_min) continue;  // taken above
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
     const uint64_t ed = lo + p.dom[r];  // the dominant entry
     const uint64_t kd = ld_idx(p.A.ci + ed, p.A.pol);
@@ -414,20 +423,31 @@ __global__ void __launch_bounds__(kDomWarps * 32, kDomBlocks) k_esc_dom(const Lo
     // ---- stream the dominant run, merging the others in ----
     uint32_t out = 0, rpos = 0, touches = 0, prev_last = 0;
     bool unsorted = false;
-    uint64_t ncol = 0;
-    double nval = 0.0;
-    if (lane < L) {
-      ncol = ld_idx(p.B.ci + bsd + lane, p.B.pol);
-      nval = ld_val(p.B.v + bsd + lane, p.B.pol);
+    // kDomAhead steps' loads in flight beside the one being merged
+    uint32_t ncol[kDomAhead];
+    double nval[kDomAhead];
+#pragma unroll
+    for (int a = 0; a < kDomAhead; ++a) {
+      ncol[a] = 0;
+      nval[a] = 0.0;
+      if (32u * a + lane < L) {
+        ncol[a] = uint32_t(ld_idx(p.B.ci + bsd + 32u * a + lane, p.B.pol));
+        nval[a] = ld_val(p.B.v + bsd + 32u * a + lane, p.B.pol);
+      }
     }
 #pragma unroll 1
     for (uint32_t j0 = 0; j0 < L; j0 += 32) {
       const bool valid = j0 + lane < L;
-      const uint32_t cd = valid ? uint32_t(ncol) : kEmptyKey;
-      const double pd = __dmul_rn(ad, nval);
-      if (j0 + 32 + lane < L) {  // the next step's loads, in flight during this one
-        ncol = ld_idx(p.B.ci + bsd + j0 + 32 + lane, p.B.pol);
-        nval = ld_val(p.B.v + bsd + j0 + 32 + lane, p.B.pol);
+      const uint32_t cd = valid ? ncol[0] : kEmptyKey;
+      const double pd = __dmul_rn(ad, nval[0]);
+#pragma unroll
+      for (int a = 0; a + 1 < kDomAhead; ++a) {
+        ncol[a] = ncol[a + 1];
+        nval[a] = nval[a + 1];
+      }
+      if (j0 + 32u * kDomAhead + lane < L) {
+        ncol[kDomAhead - 1] = uint32_t(ld_idx(p.B.ci + bsd + j0 + 32u * kDomAhead + lane, p.B.pol));
+        nval[kDomAhead - 1] = ld_val(p.B.v + bsd + j0 + 32u * kDomAhead + lane, p.B.pol);
       }
       uint32_t prevc = __shfl_up_sync(kFull, cd, 1);
       if (lane == 0) prevc = prev_last;

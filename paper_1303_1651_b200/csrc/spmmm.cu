@@ -674,6 +674,9 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
         dp.n_sub = dp.ctrl + kCtrlDomRows;
         dp.ticket = dp.ctrl + kCtrlHugeTicket;  // (the cluster variant's: unused in ESC mode)
         dp.dom = dom;
+        dp.first = mid_list + 4 * rows;  // (RowLists.dom_big: the rows past the warp-row limit)
+        dp.n_first = dp.ctrl + kCtrlDomBigRows;
+        dp.first_min = long_min;
         dp.st_min = rp.st_min;
         dp.st_max = rp.st_max;
         dp.st_touch = rp.st_touch;
