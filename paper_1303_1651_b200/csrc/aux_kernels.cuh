@@ -45,7 +45,10 @@ enum Ctrl : int {
 
 // rows past this many products are split into column-range parts in ESC mode
 // (esc.cuh); k_count sums their products for the host
-constexpr uint32_t kHugeMin = 5120;
+#ifndef SPMMM_HUGE_MIN
+#define SPMMM_HUGE_MIN 5120
+#endif
+constexpr uint32_t kHugeMin = SPMMM_HUGE_MIN;
 
 // Rows with a dominant B row (skewed inputs: an A row that hits a long B
 // row — a third of C5's products sit in such rows): the longest B row of the

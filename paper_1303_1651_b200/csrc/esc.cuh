@@ -40,7 +40,10 @@ constexpr uint32_t kEscWarpLimit = 1u << kEscQBits;  // products per warp row
 constexpr int kEscColBits = 32 - kEscQBits;           // columns < 2^23
 
 constexpr int kEscThreads = 512;
-constexpr uint32_t kEscBucketAvg = 48;  // target keys per bucket (measured: 24 and 64 slower)
+#ifndef SPMMM_BUCKET_AVG
+#define SPMMM_BUCKET_AVG 48
+#endif
+constexpr uint32_t kEscBucketAvg = SPMMM_BUCKET_AVG;  // target keys per bucket (measured: 24 and 64 slower)
 constexpr uint32_t kEscMaxBuckets = 1024;
 // rows of (kEscWarpLimit, kEscBlockCap] products; two blocks per SM. In-bucket
 // keys: qb = log2(cap) = 12 bits of q, so a bucket spans <= 2^20 columns
@@ -583,7 +586,10 @@ __device__ __forceinline__ uint32_t div_small(uint32_t x, uint32_t w, float inv_
   return q;
 }
 
-constexpr uint32_t kPartTarget = 3584;  // products per part (1536-2816 measured slower)
+#ifndef SPMMM_PART_TARGET
+#define SPMMM_PART_TARGET 3584
+#endif
+constexpr uint32_t kPartTarget = SPMMM_PART_TARGET;  // products per part (1536-2816 measured slower)
 constexpr uint32_t kMaxParts = 64;
 constexpr uint32_t kGiantRow = 16384;  // planned first
 constexpr int kPlanThreads = 512;
