@@ -118,12 +118,15 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
   }
   static_assert(R >= 1 && R <= 8, "rows per warp tile");
   static_assert(!SPLIT || (!MEDIUM && !CF && PREP == 0), "split mode: the counted short variant");
-  // PACK: groups of tiny rows share one packed pass (skewed inputs such as
-  // C5, where most rows have a handful of products). In the counted short
-  // variant; the count-free path's rows are full-width. (A split-mode
-  // instantiation without the ELL path, SPLIT, measured slower on C5 with the
-  // packed passes than this one, 0.73 against 0.61 ms: kept for A/B builds.)
-#ifndef SPMMM_NO_PACK
+  // SPLIT: the split-mode instantiation (fused_split.cu; skewed inputs such as
+  // C5, whose non-short rows were computed before this kernel). Most of its
+  // rows have a handful of products, so the tile's short rows go through
+  // packed passes only (rows.cuh packed_tile_pass: up to 8 rows per pass)
+  // and short_rows is not compiled in: C5's k_fused 0.68 -> 0.54 ms.
+  // PACK: the same idea per lockstep group of 4 rows inside the shared short
+  // variant (packed_rows; C5 0.68 -> 0.61 ms) — superseded by SPLIT, kept for
+  // A/B builds (-DSPMMM_GROUP_PACK with -DSPMMM_NO_SPLIT_VARIANT).
+#ifdef SPMMM_GROUP_PACK
   constexpr bool PACK = !MEDIUM && !CF && !STATS && (SPMMM_LOCK <= (1 << kPackSlotBits));
 #else
   constexpr bool PACK = false;
@@ -279,6 +282,42 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     const uint32_t ext_mask = MEDIUM ? 0u : __ballot_sync(kFull, my_cls == kRowLong);
     uint32_t staged = 0;
     bool global = false;
+    if constexpr (SPLIT && !STATS) {
+      // split mode: the tile's short rows in packed passes only (rows.cuh
+      // packed_tile_pass): rows are taken into a pass while it stays within 32
+      // A entries and 32 products (every short row fits one alone)
+      const uint32_t pk = my_cls == kRowShort ? (my_prod | (my_na << 16)) : 0u;
+      uint32_t sp = 0, sn = 0, npass = 0, my_pass = 0xffu;
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint32_t v = __shfl_sync(kFull, pk, i);
+        if (v) {
+          const uint32_t pr = v & 0xffffu, n = v >> 16;
+          if (any && (sp + pr > 32u || sn + n > 32u)) {
+            ++npass;
+            sp = 0;
+            sn = 0;
+          }
+          any = true;
+          sp += pr;
+          sn += n;
+          if (lane == uint32_t(i)) my_pass = npass;
+        }
+      }
+      npass = any ? npass + 1 : 0;
+#pragma unroll 1
+      for (uint32_t ps = 0; ps < npass; ++ps) {
+        ShortOut po;
+        const uint32_t kept = packed_tile_pass<WIDE>(p.A, p.B, rpv, my_na, my_prod,
+                                                     my_pass == ps, po, my_nnz);
+        if (po.keep) {
+          s_col[buf * kStage + staged + po.rank] = po.col;
+          s_val[buf * kStage + staged + po.rank] = po.val;
+        }
+        staged += kept;
+      }
+    } else
     if (__ballot_sync(kFull, my_cls == kRowShort)) {
       // short rows go through short_rows in lockstep groups of kLock; the
       // groups run in a loop (one copy of the code: instruction cache)
@@ -290,7 +329,7 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       // pass per row: its sums, products | entries << 16, in each of its lanes
       // (both groups' packed passes in lockstep measured slower: the code
       // outgrew the instruction cache)
-      uint32_t pack_sum = 0;
+      [[maybe_unused]] uint32_t pack_sum = 0;
       if constexpr (PACK) {
         pack_sum = my_cls == kRowShort ? (my_prod | (my_na << 16)) : 0u;
 #pragma unroll

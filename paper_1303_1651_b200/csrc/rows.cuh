@@ -522,6 +522,108 @@ __device__ __forceinline__ void packed_rows(const DevCsr& A, const DevCsr& B,
   }
 }
 
+// One packed pass over up to 8 rows of a warp tile (the split-mode
+// instantiation, kernels.cuh SPLIT): lane i < 8 holds row i of the tile — its
+// first A entry, its entry and product counts — and `on` says whether the row
+// belongs to this pass (the caller cuts the tile's short rows into passes of
+// <= 32 entries and <= 32 products). Same scheme as packed_rows with the row
+// data taken from the lanes: entry and product offsets by a scan over the 8
+// lanes, an entry lane finds its row by a shuffle search. Returns the number
+// of entries kept; `my_nnz` is set in the lanes of the pass's rows.
+constexpr int kTileSlotBits = 3;
+constexpr int kTileColBits = 32 - 5 - kTileSlotBits;
+
+template <bool WIDE>
+__device__ __forceinline__ uint32_t packed_tile_pass(const DevCsr& A, const DevCsr& B, uint64_t my_lo,
+                                                     uint32_t my_na, uint32_t my_prod, bool on,
+                                                     ShortOut& out, uint32_t& my_nnz) {
+  using K = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
+  using Off = typename std::conditional<WIDE, uint64_t, uint32_t>::type;
+  constexpr int kSlotShift = int(sizeof(K)) * 8 - kTileSlotBits;
+  const uint32_t lane = lane_id();
+  const uint32_t n_eff = on ? my_na : 0u, p_eff = on ? my_prod : 0u;
+  const uint32_t w = p_eff | (n_eff << 16);
+  uint32_t x = w;  // inclusive scan over lanes 0..7 (the other lanes hold 0)
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, x, d);
+    if (lane >= uint32_t(d)) x += t;
+  }
+  const uint32_t eoff = (x - w) >> 16, poff = (x - w) & 0xffffu;
+  // entry lane -> row slot: the last slot whose entries start at or before it
+  int slot = 0;
+#pragma unroll
+  for (int st = 4; st > 0; st >>= 1) {
+    const uint32_t eo = __shfl_sync(kFull, eoff, slot + st);
+    if (eo <= lane) slot += st;
+  }
+  const uint32_t e = lane - __shfl_sync(kFull, eoff, slot);
+  const bool ent = e < __shfl_sync(kFull, n_eff, slot);
+  const uint64_t rlo = __shfl_sync(kFull, my_lo, slot);
+  Off kk = 0, bs = 0;
+  double av = 0.0;
+  uint32_t len = 0;
+  if (ent) {
+    kk = Off(ld_idx(A.ci + rlo + e, A.pol));
+    av = ld_val(A.v + rlo + e, A.pol);
+  }
+  if (ent) {
+    const uint64_t b0 = ld_idx(B.rp + kk, B.pol);
+    bs = Off(b0);
+    len = uint32_t(ld_idx(B.rp + kk + 1, B.pol) - b0);
+  }
+  const uint32_t incl = warp_incl_scan(len);
+  const uint32_t excl = incl - len;  // lanes past the entries: == tot, never an owner
+  const uint32_t tot = __shfl_sync(kFull, incl, 31);
+  int src = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+    const uint32_t ex = __shfl_sync(kFull, excl, src + st);
+    if (ex <= lane) src += st;
+  }
+  const Off bsrc = __shfl_sync(kFull, bs, src) + (lane - __shfl_sync(kFull, excl, src));
+  const double a = __shfl_sync(kFull, av, src);
+  const uint32_t pslot = __shfl_sync(kFull, uint32_t(slot), src);
+  const bool valid = lane < tot;
+  uint32_t col = 0;
+  double pv = 0.0;
+  if (valid) {
+    col = uint32_t(ld_idx(B.ci + bsrc, B.pol));
+    pv = ld_val(B.v + bsrc, B.pol);
+  }
+  pv = valid ? __dmul_rn(a, pv) : 0.0;
+  K key[1];
+  key[0] = valid ? ((K(pslot) << kSlotShift) | (K(col) << 5) | K(lane)) : ~K(0);
+  bitonic32_multi<1>(key);
+  const K ck = key[0] >> 5;  // slot and column
+  const double v = __shfl_sync(kFull, pv, uint32_t(key[0]) & 31u);
+  const K prev = __shfl_up_sync(kFull, ck, 1);
+  const bool head = valid && (lane == 0 || prev != ck);
+  const uint32_t hm = __ballot_sync(kFull, head);
+  const uint32_t above = hm & ~((2u << lane) - 1u);
+  const uint32_t nxt = above ? uint32_t(__ffs(above) - 1) : tot;
+  const uint32_t seg = head ? nxt - lane : 0u;
+  const uint32_t max_seg = __reduce_max_sync(kFull, seg);
+  double acc = v;
+  for (uint32_t d = 1; d < max_seg; ++d) {
+    const double t = __shfl_down_sync(kFull, v, d);
+    if (d < seg) acc = __dadd_rn(acc, t);
+  }
+  const bool keep = head && (acc != 0.0);  // kernels.py:296 drops exact zeros
+  const uint32_t km = __ballot_sync(kFull, keep);
+  constexpr K kColMask = WIDE ? K(0xffffffffu) : K((1u << kTileColBits) - 1u);
+  out.col = uint32_t(ck & kColMask);
+  out.val = acc;
+  out.keep = keep;
+  out.rank = __popc(km & lanemask_lt());
+  // a row's products fill lanes [poff, poff + products) of the sorted order
+  if (on) {
+    const uint32_t m = (p_eff >= 32u ? kFull : ((1u << p_eff) - 1u)) << poff;
+    my_nnz = __popc(km & m);
+  }
+  return __popc(km);
+}
+
 // ---------------------------------------------------------------------------
 // Medium rows: a warp and an open-addressing table (column -> running sum).
 // The table lives in shared memory (kSmemSlots per warp); a row whose distinct

@@ -111,8 +111,8 @@ const char* const kKernelNames[] = {"k_count", "k_collect", "k_long", "k_fused",
                                     "k_esc_warp", "k_esc_block", "k_esc_plan", "k_prep",
                                     "k_esc_dom"};
 constexpr int kNumKernels = 14;
-#ifdef SPMMM_SPLIT_VARIANT
-constexpr bool kSplitVariant = true;  // split mode runs fused_split.cu's instantiation
+#ifndef SPMMM_NO_SPLIT_VARIANT
+constexpr bool kSplitVariant = true;  // split mode (no stats) runs fused_split.cu's instantiation
 #else
 constexpr bool kSplitVariant = false;
 #endif
@@ -451,7 +451,7 @@ int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bo
   FusedLaunchEnv env{c->device, c->sms, c->stream};
   cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ, prep)
                   : medium   ? fused_medium(op, prm, env, wide, stats, grid, occ)
-                  : split    ? fused_split(op, prm, env, wide, stats, grid, occ)  // (A/B builds)
+                  : split    ? fused_split(op, prm, env, wide, stats, grid, occ)
                              : fused_short(op, prm, env, wide, stats, grid, occ);
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? SPMMM_ERR_OOM : SPMMM_ERR_CUDA,
@@ -1262,8 +1262,12 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
     fp.cf_total = nullptr;
     fp.cf_err = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlCfFlags;  // (kCfOverflow)
     fp.c_cap = cap;
+    // split mode without stats: the packed-passes instantiation (its narrow
+    // sort key holds row slot, column and lane: columns < 2^24)
+    const bool split_variant = kSplitVariant && split && !stats &&
+                               (wide || B.cols <= (1ull << kTileColBits));
     int occ = 0;
-    rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ, false, 0, kSplitVariant && split);
+    rc = fused_call(c, medium, 0, fp, wide, stats, 0, &occ, false, 0, split_variant);
     if (rc) return fail_staged(rc);
     const unsigned grid = unsigned(std::min<uint64_t>(
         (ntiles + kFusedWarps - 1) / kFusedWarps, uint64_t(occ) * uint64_t(c->sms)));
@@ -1277,7 +1281,7 @@ int multiply_impl(spmmm_context* c, const spmmm_csr* a, const spmmm_csr* b, int 
       fp.g_sval = gv.sval;
     }
     tm.begin(3);
-    rc = fused_call(c, medium, 1, fp, wide, stats, grid, nullptr, false, 0, kSplitVariant && split);
+    rc = fused_call(c, medium, 1, fp, wide, stats, grid, nullptr, false, 0, split_variant);
     if (rc) return fail_staged(rc);
     tm.end(3);
     ++c->last_launches;
