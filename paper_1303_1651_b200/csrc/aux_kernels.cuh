@@ -145,10 +145,16 @@ __global__ void __launch_bounds__(256, SPMMM_COUNT_BLOCKS) k_count(DevCsr A, Dev
   const uint32_t lane = lane_id();
   uint64_t tot = 0, mx = 0, nonshort = 0, bmax = 0, kmin = ~0ull, kmax1 = 0, huge = 0;
   uint32_t need = 0, err = 0;
-  const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-  const uint64_t gw = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   constexpr uint64_t kSerial = 32;  // rows up to this many entries: one thread
-  for (uint64_t base = gw * 32; base < A.rows; base += nwarps * 32) {
+  // chunks of 32 rows, taken dynamically (ctrl word kCtrlDone: the count-free
+  // path's, unused in a counted product): with a static assignment the warps
+  // that met the long rows of a skewed input were the kernel's tail (23% of
+  // the stall samples sat at the block's final barrier on C5)
+  while (true) {
+    unsigned long long chunk = 0;
+    if (lane == 0) chunk = atomicAdd(ctrl + kCtrlDone, 1ull);
+    const uint64_t base = __shfl_sync(kFull, chunk, 0) * 32;
+    if (base >= A.rows) break;
     const uint64_t r = base + lane;
     uint64_t lo = 0, hi = 0;
     if (r < A.rows) {
