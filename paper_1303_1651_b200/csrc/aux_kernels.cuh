@@ -9,6 +9,7 @@
 namespace spmmm {
 
 // ctrl words (device, zeroed before every multiply)
+constexpr int kCtrlCfWords = 32;
 enum Ctrl : int {
   kCtrlTotal = 0,     // Σ products (estimate_nnz)
   kCtrlMaxProd = 1,   // max products of one row
@@ -40,7 +41,11 @@ enum Ctrl : int {
   kCtrlDone = 29,       // count-free path: k_fused warps finished (the last one reports)
   kCtrlCfEll = 30,      // count-free path: B's referenced rows were packed into ELL records
   kCtrlDomRows = 31,    // sub-list: rows dominated by one long B row (k_esc_dom)
-  kCtrlWords = 32
+  // (words past 31 belong to the counted path only: the count-free path's
+  // last warp reports and clears words 0..31, kCtrlCfWords)
+  kCtrlWarpRows = 32,   // sub-list: rows for k_esc_warp (one warp per row)
+  kCtrlCountTicket = 33, // k_count's dynamic row-chunk counter
+  kCtrlWords = 40
 };
 
 // rows past this many products are split into column-range parts in ESC mode
@@ -94,6 +99,7 @@ struct RowLists {
   uint32_t* huge_list;  // rows past huge_min products (column-range parts)
   uint32_t* dom_list;   // dominated rows (k_esc_dom), whatever their size
   uint32_t* dom_big;    // ... those past mid_min (block copy)
+  uint32_t* warp_list;  // the other rows up to mid_min products (one warp each)
   uint32_t mid_min, huge_min;
 };
 
@@ -104,14 +110,18 @@ __device__ __forceinline__ void list_rows(const RowLists& L, unsigned long long*
   const uint32_t m = __ballot_sync(kFull, is_long);
   if (!m) return;
   const bool is_dom = is_long && dv != 0xffffffffu;
+  const bool is_warp = is_long && !is_dom && pr <= L.mid_min;
   const uint32_t md = __ballot_sync(kFull, is_dom);
-  uint32_t base = 0, dbase = 0;
+  const uint32_t mw = __ballot_sync(kFull, is_warp);
+  uint32_t base = 0, dbase = 0, wbase = 0;
   if (lane_id() == 0) {
     base = uint32_t(atomicAdd(ctrl + kCtrlLongRows, (unsigned long long)__popc(m)));
     if (md) dbase = uint32_t(atomicAdd(ctrl + kCtrlDomRows, (unsigned long long)__popc(md)));
+    if (mw) wbase = uint32_t(atomicAdd(ctrl + kCtrlWarpRows, (unsigned long long)__popc(mw)));
   }
   base = __shfl_sync(kFull, base, 0);
   dbase = __shfl_sync(kFull, dbase, 0);
+  wbase = __shfl_sync(kFull, wbase, 0);
   if (is_long) {
     const uint32_t idx = base + __popc(m & lanemask_lt());
     L.list[idx] = uint32_t(r);
@@ -124,6 +134,8 @@ __device__ __forceinline__ void list_rows(const RowLists& L, unsigned long long*
       L.huge_list[atomicAdd(ctrl + kCtrlHugeRows, 1ull)] = idx;
     } else if (pr > L.mid_min) {
       L.mid_list[atomicAdd(ctrl + kCtrlMidRows, 1ull)] = idx;
+    } else {
+      L.warp_list[wbase + __popc(mw & lanemask_lt())] = idx;
     }
   }
 }
@@ -146,13 +158,12 @@ __global__ void __launch_bounds__(256, SPMMM_COUNT_BLOCKS) k_count(DevCsr A, Dev
   uint64_t tot = 0, mx = 0, nonshort = 0, bmax = 0, kmin = ~0ull, kmax1 = 0, huge = 0;
   uint32_t need = 0, err = 0;
   constexpr uint64_t kSerial = 32;  // rows up to this many entries: one thread
-  // chunks of 32 rows, taken dynamically (ctrl word kCtrlDone: the count-free
-  // path's, unused in a counted product): with a static assignment the warps
+  // chunks of 32 rows, taken dynamically: with a static assignment the warps
   // that met the long rows of a skewed input were the kernel's tail (23% of
   // the stall samples sat at the block's final barrier on C5)
   while (true) {
     unsigned long long chunk = 0;
-    if (lane == 0) chunk = atomicAdd(ctrl + kCtrlDone, 1ull);
+    if (lane == 0) chunk = atomicAdd(ctrl + kCtrlCountTicket, 1ull);
     const uint64_t base = __shfl_sync(kFull, chunk, 0) * 32;
     if (base >= A.rows) break;
     const uint64_t r = base + lane;

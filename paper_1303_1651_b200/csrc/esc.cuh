@@ -199,17 +199,16 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
   RowsParams p = p_in;
   p.B.pol = policy_evict_last();
   p.A.pol = policy_evict_first();
-  const uint64_t n_list = *p.n_list;
+  const uint64_t n_sub = *p.n_sub;  // this kernel's own sub-list: no rows to skip
 #pragma unroll 1
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(p.ticket, 1ull);
-    const uint64_t li = __shfl_sync(kFull, t, 0);
-    if (li >= n_list) break;
+    const uint64_t ti = __shfl_sync(kFull, t, 0);
+    if (ti >= n_sub) break;
+    const uint64_t li = p.sub[ti];
     const uint32_t r = p.list[li];
     const uint32_t P = p.prod[r];
-    if (P > kEscWarpLimit) continue;  // block kernel
-    if (p.dom && p.dom[r] != kNoDom) continue;  // k_esc_dom
     const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
     // ---- expand: product q -> skey[q] = col << 9 | q, sval[q] = a * b ----
     uint32_t base = 0;

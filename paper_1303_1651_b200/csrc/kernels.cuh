@@ -575,6 +575,8 @@ struct RowsParams {
   DevCsr A, B;
   const uint32_t* prod;
   const uint32_t* dom;  // rows with a dominant entry are k_esc_dom's (null: none are)
+  const uint32_t* sub;  // k_esc_warp: its rows, as indices into list
+  const unsigned long long* n_sub;
   const uint32_t* list;
   const unsigned long long* n_list;
   unsigned long long* cursor;  // staging allocator

@@ -350,7 +350,7 @@ uint64_t lb_counters_max(uint64_t rows) {
 }
 
 // The row lists in the context's buffers (list, lmap; sub: mid, huge, overflow,
-// dominated, dominated past the block-copy limit — `rows` entries each).
+// dominated, dominated past the block-copy limit, warp rows — `rows` entries each).
 RowLists row_lists(spmmm_context* c, uint64_t rows, uint32_t mid_min, uint32_t huge_min) {
   RowLists l{};
   l.list = static_cast<uint32_t*>(c->list.p);
@@ -359,6 +359,7 @@ RowLists row_lists(spmmm_context* c, uint64_t rows, uint32_t mid_min, uint32_t h
   l.huge_list = l.mid_list + rows;
   l.dom_list = l.mid_list + 3 * rows;
   l.dom_big = l.mid_list + 4 * rows;
+  l.warp_list = l.mid_list + 5 * rows;
   l.mid_min = mid_min;
   l.huge_min = huge_min;
   return l;
@@ -377,7 +378,7 @@ int run_count(spmmm_context* c, const DevCsr& A, const DevCsr& B, Timer& tm, boo
       B.cols <= (1ull << kEscColBits)) {
     CUDA_TRY(ensure(c->lmap, A.rows * sizeof(uint32_t), c->stream));
     CUDA_TRY(ensure(c->list, A.rows * sizeof(uint32_t), c->stream));
-    CUDA_TRY(ensure(c->sub, 5 * A.rows * sizeof(uint32_t), c->stream));
+    CUDA_TRY(ensure(c->sub, 6 * A.rows * sizeof(uint32_t), c->stream));
     lists = row_lists(c, A.rows, kEscWarpLimit, kEscBlockCap);
     c->lists_from_count = true;
   }
@@ -556,7 +557,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
   CUDA_TRY(ensure(c->list, rows * sizeof(uint32_t), c->stream));
   CUDA_TRY(ensure(c->l_off, rows * sizeof(uint64_t), c->stream));
   CUDA_TRY(ensure(c->l_nnz, rows * sizeof(uint32_t), c->stream));
-  CUDA_TRY(ensure(c->sub, 5 * rows * sizeof(uint32_t), c->stream));
+  CUDA_TRY(ensure(c->sub, 6 * rows * sizeof(uint32_t), c->stream));
   uint32_t* mid_list = static_cast<uint32_t*>(c->sub.p);
   uint32_t* huge_list = mid_list + rows;
   uint32_t* ovf_list = mid_list + 2 * rows;
@@ -616,7 +617,7 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
       CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlLongRows, 0, 8, c->stream));
       CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlMidRows, 0, 16, c->stream));  // (and kCtrlHugeRows)
       CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlDomBigRows, 0, 8, c->stream));
-      CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlDomRows, 0, 8, c->stream));
+      CUDA_TRY(cudaMemsetAsync(ctrl + kCtrlDomRows, 0, 16, c->stream));  // (and kCtrlWarpRows)
     }
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, uint64_t(c->sms) * 8);
     tm.begin(1);
@@ -633,6 +634,8 @@ int run_long(spmmm_context* c, const DevCsr& A, const DevCsr& B, uint64_t max_pr
     rp.B = B;
     rp.prod = static_cast<const uint32_t*>(c->prod.p);
     rp.dom = dom;
+    rp.sub = mid_list + 5 * rows;  // (RowLists.warp_list)
+    rp.n_sub = static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlWarpRows;
     rp.list = static_cast<const uint32_t*>(c->list.p);
     rp.n_list = static_cast<const unsigned long long*>(c->ctrl.p) + kCtrlLongRows;
     rp.cursor = static_cast<unsigned long long*>(c->ctrl.p) + kCtrlStageCursor;
@@ -1034,7 +1037,7 @@ int multiply_count_free(spmmm_context* c, const DevCsr& A, const DevCsr& B, bool
   fp.ctrl = ctrl;
   fp.host_ctrl = c->h_ctrl;
   fp.done = ctrl + kCtrlDone;
-  fp.ctrl_words = kCtrlWords;
+  fp.ctrl_words = kCtrlCfWords;
   fp.cf_words = CfWords{ctrl + kCtrlCfFlags, ctrl + kCtrlKMinInv, ctrl + kCtrlKMax1, ctrl + kCtrlCfEll};
   fp.cf_zero = zero;
   fp.cf_nzero = ncnt;
