@@ -200,16 +200,36 @@ __global__ void __launch_bounds__(kEscWarps * 32, 4) k_esc_warp(const RowsParams
   p.B.pol = policy_evict_last();
   p.A.pol = policy_evict_first();
   const uint64_t n_sub = *p.n_sub;  // this kernel's own sub-list: no rows to skip
+  // rows are taken kEscWarpTake at a time (they are small: one atomic per
+  // row was 16% of the kernel's stall samples); lane j keeps row j's index
+  constexpr uint32_t kEscWarpTake = 4;
+  // the batch: rows taken, next one; lane j holds row j's list index, row,
+  // products and entry range (the chain sub -> list -> prod / row_ptr once
+  // per batch, not per row)
+  uint32_t nb = 0, pos = 0, my_li = 0, my_r = 0, my_P = 0;
+  uint64_t my_lo = 0, my_hi = 0;
 #pragma unroll 1
   while (true) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(p.ticket, 1ull);
-    const uint64_t ti = __shfl_sync(kFull, t, 0);
-    if (ti >= n_sub) break;
-    const uint64_t li = p.sub[ti];
-    const uint32_t r = p.list[li];
-    const uint32_t P = p.prod[r];
-    const uint64_t lo = ld_idx(p.A.rp + r), hi = ld_idx(p.A.rp + r + 1);
+    if (pos == nb) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(p.ticket, (unsigned long long)kEscWarpTake);
+      const uint64_t t0 = __shfl_sync(kFull, t, 0);
+      if (t0 >= n_sub) break;
+      nb = uint32_t(n_sub - t0 < kEscWarpTake ? n_sub - t0 : kEscWarpTake);
+      pos = 0;
+      if (lane < nb) {
+        my_li = p.sub[t0 + lane];
+        my_r = p.list[my_li];
+        my_P = p.prod[my_r];
+        my_lo = ld_idx(p.A.rp + my_r);
+        my_hi = ld_idx(p.A.rp + my_r + 1);
+      }
+    }
+    const uint64_t li = __shfl_sync(kFull, my_li, pos);
+    const uint32_t r = __shfl_sync(kFull, my_r, pos);
+    const uint32_t P = __shfl_sync(kFull, my_P, pos);
+    const uint64_t lo = __shfl_sync(kFull, my_lo, pos), hi = __shfl_sync(kFull, my_hi, pos);
+    ++pos;
     // ---- expand: product q -> skey[q] = col << 9 | q, sval[q] = a * b ----
     uint32_t base = 0;
 #pragma unroll 1
