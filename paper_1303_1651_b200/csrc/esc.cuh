@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(kEscThreads, 2) k_esc_block(LongParams p, uint
   __shared__ uint64_t s_bs[NT];
   __shared__ double s_av[NT];
   __shared__ uint32_t s_scan[NT / 32 + 1];
-  __shared__ uint32_t s_li, s_min, s_max, s_touch, s_bt;
+  __shared__ uint32_t s_min, s_max, s_touch, s_bt;
   __shared__ unsigned long long s_off;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   uint32_t qb = 1;
@@ -911,32 +911,54 @@ __global__ void __launch_bounds__(kEscThreads, 2) k_esc_block(LongParams p, uint
   const uint32_t n_sub = uint32_t(*(volatile const unsigned long long*)p.n_sub);
   const uint32_t n_parts =
       p.parts ? uint32_t(*(volatile const unsigned long long*)(p.ctrl + kCtrlParts)) : 0u;
+  // A work item's descriptor — ticket -> sub-list / part -> list -> products and
+  // entry range, a chain of four dependent loads — is fetched by thread 0 one
+  // item ahead, while the block sorts the current item's buckets (the items
+  // are independent; at the top of an item the chain was ~2.5 us with all 16
+  // warps waiting on it, ~50 times per block).
+  struct ItemDesc {
+    uint32_t t_row, li, r, P;
+    unsigned long long scr, lo, hi;
+  };
+  __shared__ ItemDesc s_next;
+  auto fetch_item = [&]() {  // thread 0
+    ItemDesc d;
+    d.t_row = uint32_t(atomicAdd(p.ticket, 1ull));
+    d.li = d.r = d.P = 0;
+    d.scr = d.lo = d.hi = 0;
+    if (d.t_row < n_sub + n_parts) {
+      if (d.t_row >= n_sub) {
+        const PartDesc pd = p.parts[d.t_row - n_sub];
+        d.li = pd.li;
+        d.P = pd.cnt;
+        d.scr = pd.off;
+        d.r = p.list[d.li];
+      } else {
+        d.li = p.sub[d.t_row];
+        d.r = p.list[d.li];
+        d.P = p.prod[d.r];
+        d.lo = ld_idx(pp.A.rp + d.r);
+        d.hi = ld_idx(pp.A.rp + d.r + 1);
+      }
+    }
+    s_next = d;
+  };
+  if (tid == 0) fetch_item();
 #pragma unroll 1
   while (true) {
     if (tid == 0) {
-      s_li = uint32_t(atomicAdd(p.ticket, 1ull));
       s_min = kEmptyKey;
       s_max = 0;
       s_touch = 0;
     }
     __syncthreads();
-    const uint32_t t_row = s_li;
+    const ItemDesc cur = s_next;
+    const uint32_t t_row = cur.t_row;
     if (t_row >= n_sub + n_parts) break;
     // work item: a whole mid row, or one column-range part of a huge row
     const bool is_part = t_row >= n_sub;
-    uint32_t li, P;
-    uint64_t scr = 0;
-    if (is_part) {
-      const PartDesc d = p.parts[t_row - n_sub];
-      li = d.li;
-      P = d.cnt;
-      scr = d.off;
-    } else {
-      li = p.sub[t_row];
-    }
-    const uint32_t r = p.list[li];
-    if (!is_part) P = p.prod[r];
-    const uint64_t lo = is_part ? 0 : ld_idx(pp.A.rp + r), hi = is_part ? 0 : ld_idx(pp.A.rp + r + 1);
+    const uint32_t li = cur.li, P = cur.P, r = cur.r;
+    const uint64_t scr = cur.scr, lo = cur.lo, hi = cur.hi;
     uint32_t base = 0, cmn = kEmptyKey, cmx = 0;
     // part: its products are staged in q order by k_esc_plan
     for (uint32_t i = tid; is_part && i < P; i += NT) {
@@ -1046,6 +1068,8 @@ __global__ void __launch_bounds__(kEscThreads, 2) k_esc_block(LongParams p, uint
     }
     __syncthreads();
     // ---- per bucket (one warp): sort, fold; heads' sums go to sval[q] ----
+    // (every thread has read s_next; thread 0 fetches the next item's now)
+    if (tid == 0) fetch_item();
     uint32_t touches = 0;
 #pragma unroll 1
     // buckets taken dynamically (sort costs vary with the bucket size)
