@@ -28,7 +28,7 @@ struct FusedLaunchEnv {
 };
 
 template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0,
-          bool SPLIT = false>
+          bool SPLIT = false, bool SELF = false>
 struct FusedVariant {
   static constexpr size_t smem() {
     return FusedSmem<R, MEDIUM>::bytes(WARPS);
@@ -38,7 +38,7 @@ struct FusedVariant {
     static int cache[64] = {};
     int& c = cache[device & 63];
     if (c == 0) {
-      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP, SPLIT>;
+      auto kern = k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP, SPLIT, SELF>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(smem()));
       if (e != cudaSuccess) return e;
@@ -54,7 +54,7 @@ struct FusedVariant {
     FusedParams prm = prm_in;
     void* args[] = {&prm};
     return cudaLaunchCooperativeKernel(
-        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP, SPLIT>), dim3(grid),
+        reinterpret_cast<void*>(k_fused<WARPS, R, MEDIUM, WIDE, STATS, CF, PREP, SPLIT, SELF>), dim3(grid),
         dim3(WARPS * 32), args, smem(), env.stream);
   }
 };
@@ -69,15 +69,17 @@ cudaError_t fused_medium(int op, const FusedParams& prm, const FusedLaunchEnv& e
                          bool stats, unsigned grid, int* occ);
 // the count-free short variant (fused_cf.cu); prep 1 / 2: with the prep pass
 // of mode 0 / 1 inside (small products)
+// self: C = A·A (the instantiations with the self-record path compiled in)
 cudaError_t fused_cf(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
-                     bool stats, unsigned grid, int* occ, int prep);
+                     bool stats, unsigned grid, int* occ, int prep, bool self);
 
-template <int WARPS, int R, bool MEDIUM, bool CF = false, int PREP = 0, bool SPLIT = false>
+template <int WARPS, int R, bool MEDIUM, bool CF = false, int PREP = 0, bool SPLIT = false,
+          bool SELF = false>
 cudaError_t fused_dispatch(int op, const FusedParams& prm, const FusedLaunchEnv& env, bool wide,
                            bool stats, unsigned grid, int* occ) {
 #define SPMMM_FUSED_CASE(W, S)                                                  \
   if (wide == W && stats == S) {                                                \
-    using V = FusedVariant<WARPS, R, MEDIUM, W, S, CF, PREP, SPLIT>;                   \
+    using V = FusedVariant<WARPS, R, MEDIUM, W, S, CF, PREP, SPLIT, SELF>;                   \
     return op == 0 ? V::occupancy(env.device, occ) : V::launch(prm, env, grid); \
   }
   SPMMM_FUSED_CASE(false, false)

@@ -102,7 +102,7 @@ struct FusedSmem {
 };
 
 template <int WARPS, int R, bool MEDIUM, bool WIDE, bool STATS, bool CF = false, int PREP = 0,
-          bool SPLIT = false>
+          bool SPLIT = false, bool SELF = false>
 __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k_fused(const FusedParams p_in) {
   static_assert(!MEDIUM || R == 1, "one medium row per warp tile");
   static_assert(!(MEDIUM && CF), "the count-free path is short rows only");
@@ -177,9 +177,12 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
   }
   // C = A·A through the ELL records: rows are read from their own records
   // (short_rows), so the tile needs no A.row_ptr at all
+  // (SELF: the instantiation launched for C = A·A — with the path compiled
+  // into the one A != B products run, C3's k_fused was 2.8% slower)
+  static_assert(!SELF || CF, "the self-record path belongs to the count-free variant");
   bool self = false;
 #ifndef SPMMM_NO_SELF
-  if constexpr (CF) self = p.self_ell != 0 && p.ell != nullptr;
+  if constexpr (SELF) self = p.self_ell != 0 && p.ell != nullptr;
 #endif
   uint64_t cf_prods = 0;
 

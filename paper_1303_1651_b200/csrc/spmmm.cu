@@ -450,7 +450,7 @@ int fused_call(spmmm_context* c, bool medium, int op, const FusedParams& prm, bo
                bool stats, unsigned grid, int* occ, bool count_free = false, int prep = 0,
                bool split = false) {
   FusedLaunchEnv env{c->device, c->sms, c->stream};
-  cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ, prep)
+  cudaError_t e = count_free ? fused_cf(op, prm, env, wide, stats, grid, occ, prep, prm.self_ell != 0)
                   : medium   ? fused_medium(op, prm, env, wide, stats, grid, occ)
                   : split    ? fused_split(op, prm, env, wide, stats, grid, occ)
                              : fused_short(op, prm, env, wide, stats, grid, occ);
