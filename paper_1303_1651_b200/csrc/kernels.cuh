@@ -23,6 +23,9 @@
 #ifndef SPMMM_SHORT_BLOCKS
 #define SPMMM_SHORT_BLOCKS 4
 #endif
+#ifndef SPMMM_PF_AHEAD
+#define SPMMM_PF_AHEAD 1024
+#endif
 #ifndef SPMMM_LOCK
 #define SPMMM_LOCK 4
 #endif
@@ -258,6 +261,17 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     const uint64_t tile = base + bj;
     const int buf = half * kBatch + bj;
     const uint64_t r0 = tile * R;
+    // Stream prefetch (C = A·A, the self-record path): the tile kPfAhead
+    // tickets from here is some warp's in a few microseconds — its rows'
+    // records into L2 now, so that tile's first loads are L2 hits instead of
+    // DRAM round trips (C2 1.363 -> 1.340 ms; 1024 and 4096 tickets ahead
+    // measured the same). Not in the A != B instantiations: prefetching A's
+    // row pointers and entries there cost C3 2.3% (0.678 -> 0.694 ms).
+    if constexpr (SELF && SPMMM_PF_AHEAD > 0) {
+      const uint64_t ft = tile + SPMMM_PF_AHEAD;
+      if (self && ft < p.ntiles && lane < 4)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ell + ft * R * kEllWords + lane * 32));
+    }
     // ---- row bounds and classes of the tile: lane i owns row r0 + i ----
     uint64_t rpv = 0;
     uint32_t my_cls = kRowZero, my_na = 0, my_prod = 0;
