@@ -188,6 +188,9 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
   if constexpr (SELF) self = p.self_ell != 0 && p.ell != nullptr;
 #endif
   uint64_t cf_prods = 0;
+  // (stream prefetch: the average number of A entries in SPMMM_PF_AHEAD tiles)
+  [[maybe_unused]] const uint64_t pf_entries =
+      rows ? uint64_t(SPMMM_PF_AHEAD) * R * p.A.nnz / rows : 0;
 
   // the previous batch waits for its offsets; its metadata lives in s_meta*
   int nprev = 0;
@@ -278,6 +281,23 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     if (!self && lane <= uint32_t(R) && r0 + lane <= rows)
       rpv = ld_idx(p.A.rp + r0 + lane, p.A.pol);
     const uint64_t rpn = __shfl_down_sync(kFull, rpv, 1);
+    // Stream prefetch, count-free A != B (C3): the tile SPMMM_PF_AHEAD tickets
+    // ahead gets its row pointers and — at this tile's entry offset plus the
+    // average entries per tile: exact for uniform rows, near enough otherwise,
+    // and a wrong guess only wastes a line — its entries into L2: C3 k_fused
+    // 0.678 -> 0.657 ms. (Going on to load those entries a stage later and
+    // prefetch the B records they address: no gain, 0.68 ms.)
+    if constexpr (CF && !SELF && PREP == 0 && SPMMM_PF_AHEAD > 0) {
+      const uint64_t ft = tile + SPMMM_PF_AHEAD;
+      if (ft < p.ntiles) {
+        const uint64_t fe = __shfl_sync(kFull, rpv, 0) + pf_entries;
+        if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.rp + ft * R));
+        if (lane >= 2 && lane < 6)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.ci + fe + (lane - 2) * 16));
+        if (lane >= 6 && lane < 10)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.v + fe + (lane - 6) * 16));
+      }
+    }
     if (self) {
       if (lane < uint32_t(R) && r0 + lane < rows) {
         my_cls = kRowShort;  // (an empty row's record is empty: no products)
