@@ -83,3 +83,21 @@ def test_built_for_sm_100a():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_row_classes_are_reported_without_a_device():
+    """spmmm_row_classes (bench.py attributes a skewed input's products to the
+    kernels that compute them): the split-mode limits, consistent with each
+    other, and NULL is rejected."""
+    import ctypes
+
+    from paper_1303_1651_b200 import _lib
+
+    lib = _lib.lib()
+    assert lib.spmmm_row_classes(None) == _lib.ERR_INVALID
+    lim = (ctypes.c_uint32 * 5)()
+    assert lib.spmmm_row_classes(lim) == _lib.OK
+    warp_limit, part_limit, rcap, minrun, half = (int(x) for x in lim)
+    assert 32 < warp_limit < part_limit      # warp rows, then block rows, then parts
+    assert 0 < rcap <= warp_limit            # the others are sorted by one warp
+    assert minrun >= 32 and half in (0, 1)
