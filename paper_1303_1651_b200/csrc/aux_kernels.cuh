@@ -56,17 +56,20 @@ enum Ctrl : int {
 constexpr uint32_t kHugeMin = SPMMM_HUGE_MIN;
 
 // Rows with a dominant B row (skewed inputs: an A row that hits a long B
-// row — a third of C5's products sit in such rows): the longest B row of the
-// row has L >= kDomMinRun entries, at least half of the row's P products,
-// and at most kDomRCap products come from the other entries. Such a row is the dominant run —
-// already sorted, distinct columns — merged with the few sorted others
-// (esc.cuh k_esc_dom) instead of P keys sorted from scratch. k_count records
-// the dominant entry (its offset in the A row; the first of the longest).
-// (measured on C5: cap 256 / run >= 64 / at least half of the row, the rule
-// below, 3.33 ms; cap 512 / run >= 32 / any share moves 9M more products here
-// and ties, 3.33 ms — the others cost about what they cost the block kernels)
+// row — 40% of C5's products sit in such rows): the longest B row of the row
+// has L >= kDomMinRun entries and at most kDomRCap of the row's P products
+// come from the other entries (one warp sorts those). Such a row is the
+// dominant run — already sorted, distinct columns — merged with the sorted
+// others (esc.cuh k_esc_dom) instead of P keys sorted from scratch. k_count
+// records the dominant entry (its offset in the A row; the first of the
+// longest).
+// (measured on C5, final kernels: others <= 512 / run >= 64 / any share of the
+// row, the rule below, 2.82 ms; run >= 32: 2.84, >= 96: 2.84, >= 128: 2.86;
+// others <= 384: 2.88; others <= 256 and at least half of the row — the rule
+// before k_esc_dom took its long rows first and k_esc_block fetched its items
+// ahead: 2.90. -DSPMMM_DOM_HALF asks for half of the row again.)
 #ifndef SPMMM_DOM_RCAP
-#define SPMMM_DOM_RCAP 256
+#define SPMMM_DOM_RCAP 512
 #endif
 #ifndef SPMMM_DOM_MINRUN
 #define SPMMM_DOM_MINRUN 64
@@ -75,18 +78,12 @@ constexpr uint32_t kDomRCap = SPMMM_DOM_RCAP;
 constexpr uint32_t kDomMinRun = SPMMM_DOM_MINRUN;
 constexpr uint32_t kNoDom = 0xffffffffu;
 __host__ __device__ inline bool dom_eligible(uint64_t P, uint64_t L) {
-#ifndef SPMMM_DOM_ANY_SHARE
+#ifdef SPMMM_DOM_HALF
   if (2 * L < P) return false;
 #endif
   return L >= kDomMinRun && P - L <= kDomRCap;
 }
 
-
-// ---------------------------------------------------------------------------
-// K1: per-row product counts. formats.py:276-289 per row. A warp takes 32
-// consecutive rows (one per lane); rows with many A entries are summed by the
-// whole warp so a 4096-entry row does not stall its 31 neighbours.
-// Also zeroes k_fused's look-back counters (`zero`, `nzero` words) on the way.
 // Split-mode row lists, built by k_count itself on the assumption that the
 // product will run in split mode with the ESC kernels (the host knows only
 // after reading k_count's totals; when it decides otherwise it resets the

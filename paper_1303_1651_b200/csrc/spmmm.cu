@@ -2379,7 +2379,7 @@ int spmmm_row_classes(uint32_t out[5]) {
   out[1] = kHugeMin;
   out[2] = kDomRCap;
   out[3] = kDomMinRun;
-#ifndef SPMMM_DOM_ANY_SHARE
+#ifdef SPMMM_DOM_HALF
   out[4] = 1;
 #else
   out[4] = 0;
