@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
     // row pointers and entries there cost C3 2.3% (0.678 -> 0.694 ms).
     if constexpr (SELF && SPMMM_PF_AHEAD > 0) {
       const uint64_t ft = tile + SPMMM_PF_AHEAD;
-      if (self && ft < p.ntiles && lane < 4)
+      // (whole tiles only: every prefetched line lies inside the record array)
+      if (self && (ft + 1) * R <= rows && lane < 4)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ell + ft * R * kEllWords + lane * 32));
     }
     // ---- row bounds and classes of the tile: lane i owns row r0 + i ----
@@ -292,10 +293,13 @@ __global__ void __launch_bounds__(WARPS * 32, MEDIUM ? 4 : SPMMM_SHORT_BLOCKS) k
       if (ft < p.ntiles) {
         const uint64_t fe = __shfl_sync(kFull, rpv, 0) + pf_entries;
         if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.rp + ft * R));
-        if (lane >= 2 && lane < 6)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.ci + fe + (lane - 2) * 16));
-        if (lane >= 6 && lane < 10)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.v + fe + (lane - 6) * 16));
+        // (the estimate may pass the arrays' end: only lines inside them)
+        if (fe + 64 <= p.A.nnz) {
+          if (lane >= 2 && lane < 6)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.ci + fe + (lane - 2) * 16));
+          if (lane >= 6 && lane < 10)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.A.v + fe + (lane - 6) * 16));
+        }
       }
     }
     if (self) {
